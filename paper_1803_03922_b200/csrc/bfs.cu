@@ -1,0 +1,763 @@
+// bfs.cu -- BFS engines (engine.py:98-330 restated for B200).
+//
+//   persistent: one cooperative launch runs the whole BFS (init, seed, every
+//               level's V/F phases separated by grid barriers, assembly).  No
+//               host round trip per level; used whenever all workers live on
+//               this device (p == 1, or the reference's simulated p workers).
+//   host loop : one launch per phase with the NCCL exchange between V and F;
+//               used with one worker per process (torchrun, NCCL over NVLink).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "bfs_device.cuh"
+
+namespace dbfs {
+
+// ------------------------------------------------------------- grid barrier
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Sense-counting grid barrier with a watchdog: a block that waits > 4 s sets
+// `abort`, every block then leaves the kernel (reported as DBFS_ETIMEOUT).
+__device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks) {
+    __shared__ int s_ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned gen = ld_acquire_u32(&bar->gen);
+        __threadfence();
+        unsigned arrived = atomicAdd(&bar->count, 1u);
+        if (arrived == nblocks - 1) {
+            atomicExch(&bar->count, 0u);
+            __threadfence();
+            atomicAdd(&bar->gen, 1u);
+        } else {
+            unsigned long long t0 = globaltimer_ns();
+            while (ld_acquire_u32(&bar->gen) == gen) {
+                if (ld_acquire_u32(&bar->abort)) break;
+                if (globaltimer_ns() - t0 > 4000000000ull) {
+                    atomicExch(&bar->abort, 1u);
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        __threadfence();
+        s_ok = ld_acquire_u32(&bar->abort) == 0;
+    }
+    __syncthreads();
+    return s_ok;
+}
+
+// ---------------------------------------------------------------- assembly
+
+struct AsmArgs {
+    int64_t n;
+    int p;
+    PDiv pd;
+    const uint32_t *del_id;
+    const int32_t *nlevel[MAXW];
+    const int64_t *nparent[MAXW];
+    int64_t stride;  // dist: gathered arrays are [p][stride]
+    const int32_t *dlevel;
+    const int64_t *dparent;
+    int32_t *glevel;
+    int64_t *gparent;
+    int parents;
+};
+
+// levels[v] for normals from worker v mod p, then delegates (engine.py:308-314).
+__device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
+    for (int64_t v = tid; v < a.n; v += nth) {
+        uint32_t di = a.del_id[v];
+        if (di != 0xffffffffu) {
+            a.glevel[v] = a.dlevel[di];
+            if (a.parents) a.gparent[v] = a.dlevel[di] >= 0 ? a.dparent[di] : -1;
+        } else {
+            uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
+            a.glevel[v] = a.nlevel[w][i];
+            if (a.parents) a.gparent[v] = a.nparent[w][i];
+        }
+    }
+}
+
+// ----------------------------------------------------------------- kernels
+
+__global__ void __launch_bounds__(BT) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
+                                                       uint32_t src_del, GridBar *bar, int rec_cap,
+                                                       AsmArgs asm_args, int do_assemble) {
+    __shared__ Smem sm;
+    const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
+    const View &V = views[wsel];
+    const unsigned nblocks = gridDim.x;
+    phase_init(V, wb, nb);
+    if (!grid_sync(bar, nblocks)) return;
+    if (wb == 0 && threadIdx.x == 0) seed_worker(V, source, src_del);
+    if (!grid_sync(bar, nblocks)) return;
+    int L = 0;
+    for (;; L++) {
+        if (L > 0) {
+            bool cont = level_continue(views, W, L - 1);
+            if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
+            if (!cont) break;
+        }
+        phase_visit(V, L, wb, nb, sm);
+        if (!grid_sync(bar, nblocks)) return;
+        phase_finish(V, L, wb, nb);
+        if (!grid_sync(bar, nblocks)) return;
+    }
+    if (wb == 0 && threadIdx.x == 0) V.ctl->last_level = L;
+    if (do_assemble) phase_assemble(asm_args, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
+}
+
+__global__ void __launch_bounds__(BT) k_init(const View *__restrict__ views, int W) {
+    phase_init(views[blockIdx.x % W], blockIdx.x / W, gridDim.x / W);
+}
+
+__global__ void k_seed(const View *__restrict__ views, int W, int64_t source, uint32_t src_del) {
+    if (threadIdx.x == 0 && (int)blockIdx.x < W) seed_worker(views[blockIdx.x], source, src_del);
+}
+
+__global__ void __launch_bounds__(BT) k_visit(const View *__restrict__ views, int W, int L) {
+    __shared__ Smem sm;
+    phase_visit(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W, sm);
+}
+
+__global__ void __launch_bounds__(BT) k_finish(const View *__restrict__ views, int W, int L) {
+    phase_finish(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W);
+}
+
+__global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
+    phase_assemble(a, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
+}
+
+// --------------------------------------------------------------- resources
+
+static constexpr int HUB = 256;
+static constexpr int CHUNK = 256;
+
+Graph::~Graph() {}
+
+int32_t *Graph::levels_dev() { return (p == 1 && !dist) ? workers[0].nlevel.p : glevel.p; }
+int64_t *Graph::parents_dev() { return (p == 1 && !dist) ? workers[0].nparent.p : gparent.p; }
+
+static void ensure_resources(Graph &g) {
+    if (g.bfs_ready) return;
+    Ctx &ctx = *g.ctx;
+    const int W = (int)g.workers.size();
+    g.W = W;
+    g.rec_cap = (int)std::min<int64_t>(std::max<int64_t>(g.n + 2, 16), 1 << 16);
+    const int64_t nw_d = nwords(g.d);
+    // per-destination inbox capacities
+    std::vector<int64_t> inbox_cap(g.p, 0);
+    if (!g.dist) {
+        for (auto &W0 : g.workers)
+            for (int o = 0; o < g.p; o++) inbox_cap[o] += W0.remote_cap[o];
+    } else {
+        // all ranks' caps towards me: all-gather the cap vectors
+        DArray<int64_t> s, r;
+        s.alloc(g.p);
+        r.alloc((int64_t)g.p * g.p);
+        std::vector<int64_t> mine(g.p);
+        for (int o = 0; o < g.p; o++) mine[o] = g.workers[0].remote_cap[o];
+        DBFS_CUDA(cudaMemcpy(s.p, mine.data(), 8 * g.p, cudaMemcpyHostToDevice));
+        nccl_allgather_bytes(ctx, s.p, r.p, 8 * g.p);
+        std::vector<int64_t> all((size_t)g.p * g.p);
+        DBFS_CUDA(cudaMemcpy(all.data(), r.p, 8 * g.p * g.p, cudaMemcpyDeviceToHost));
+        for (int src = 0; src < g.p; src++) inbox_cap[ctx.rank] += all[(size_t)src * g.p + ctx.rank];
+    }
+    for (auto &Wk : g.workers) {
+        const int64_t nl = Wk.n_local, nw_n = nwords(nl);
+        Wk.nlevel.alloc(std::max<int64_t>(nl, 1));
+        Wk.nparent.alloc(std::max<int64_t>(nl, 1));
+        Wk.dlevel.alloc(std::max<int64_t>(g.d, 1));
+        Wk.dparent.alloc(std::max<int64_t>(g.d, 1));
+        Wk.dcand.alloc(std::max<int64_t>(g.d, 1));
+        Wk.nvis.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.nfront0.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.nfront1.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.dvis.alloc(std::max<int64_t>(nw_d, 1));
+        Wk.dfront.alloc(std::max<int64_t>(nw_d, 1));
+        Wk.dnext0.alloc(std::max<int64_t>(nw_d, 1));
+        Wk.dnext1.alloc(std::max<int64_t>(nw_d, 1));
+        Wk.chunk_cap = (Wk.nnz[KIND_DN] + Wk.nnz[KIND_DD]) / CHUNK + (Wk.nnz[KIND_DN] + Wk.nnz[KIND_DD]) / HUB + 8;
+        Wk.chunks0.alloc(Wk.chunk_cap);
+        Wk.chunks1.alloc(Wk.chunk_cap);
+        Wk.inbox_cap = std::max<int64_t>(inbox_cap[Wk.w], 1);
+        Wk.inbox0.alloc(Wk.inbox_cap);
+        Wk.inbox1.alloc(Wk.inbox_cap);
+        if (g.dist) {
+            int64_t acc = 0;
+            for (int o = 0; o < g.p; o++) {
+                Wk.send_off[o] = acc;
+                acc += Wk.remote_cap[o];
+            }
+            Wk.send_off[g.p] = acc;
+            Wk.sendbuf.alloc(std::max<int64_t>(acc, 1));
+        }
+        Wk.ctl.alloc(1);
+        Wk.rec.alloc(g.rec_cap);
+    }
+    if (g.p > 1 || g.dist) {
+        g.glevel.alloc(std::max<int64_t>(g.n, 1));
+        g.gparent.alloc(std::max<int64_t>(g.n, 1));
+    }
+    if (g.dist) g.mask_gather.alloc(std::max<int64_t>(nw_d, 1) * g.p);
+    // views
+    g.views_h.assign(W, View{});
+    for (int i = 0; i < W; i++) {
+        WorkerHost &Wk = g.workers[i];
+        View &V = g.views_h[i];
+        memset(&V, 0, sizeof(View));
+        V.w = Wk.w;
+        V.W = W;
+        V.p = g.p;
+        V.p_rank = g.p_rank;
+        V.dist = g.dist;
+        V.cand_all = !g.dist;
+        V.P_sources = g.dist ? g.p : W;
+        V.rec_cap = g.rec_cap;
+        V.hub = HUB;
+        V.chunk = CHUNK;
+        V.pd.init((uint32_t)g.p);
+        V.n = g.n;
+        V.n_local = Wk.n_local;
+        V.d = g.d;
+        V.nw_n = nwords(Wk.n_local);
+        V.nw_d = nw_d;
+        for (int k = 0; k < 4; k++) {
+            V.off[k] = g.off_all.p + Wk.base[k];
+            V.col[k] = g.col_all.p;
+            V.src_bits[k] = Wk.src_bits[k].p;
+            V.total_src[k] = (unsigned long long)Wk.n_src[k];
+        }
+        V.del_gid = g.del_gid.p;
+        V.nlevel = Wk.nlevel.p;
+        V.nparent = Wk.nparent.p;
+        V.dlevel = Wk.dlevel.p;
+        V.dparent = Wk.dparent.p;
+        V.dcand = Wk.dcand.p;
+        V.nvis = Wk.nvis.p;
+        V.nfront[0] = Wk.nfront0.p;
+        V.nfront[1] = Wk.nfront1.p;
+        V.dvis = Wk.dvis.p;
+        V.dfront = Wk.dfront.p;
+        V.dnext[0] = Wk.dnext0.p;
+        V.dnext[1] = Wk.dnext1.p;
+        V.chunks[0] = Wk.chunks0.p;
+        V.chunks[1] = Wk.chunks1.p;
+        V.chunk_cap = Wk.chunk_cap;
+        V.inbox[0] = Wk.inbox0.p;
+        V.inbox[1] = Wk.inbox1.p;
+        V.inbox_cap = Wk.inbox_cap;
+        V.ctl = Wk.ctl.p;
+        V.rec = Wk.rec.p;
+        if (g.dist) {
+            for (int o = 0; o < g.p; o++) {
+                V.sendbin[o] = Wk.sendbuf.p + Wk.send_off[o];
+                V.sendcap[o] = Wk.remote_cap[o];
+                V.mask_src[0][o] = g.mask_gather.p + (int64_t)o * std::max<int64_t>(nw_d, 1);
+                V.mask_src[1][o] = V.mask_src[0][o];
+            }
+        } else {
+            for (int j = 0; j < W; j++) {
+                WorkerHost &Wj = g.workers[j];
+                V.ctl_all[j] = Wj.ctl.p;
+                V.inbox_all[0][j] = Wj.inbox0.p;
+                V.inbox_all[1][j] = Wj.inbox1.p;
+                V.mask_src[0][j] = Wj.dnext0.p;
+                V.mask_src[1][j] = Wj.dnext1.p;
+                V.cand_src[j] = Wj.dcand.p;
+            }
+        }
+        if (g.p == 1 && !g.dist) {
+            V.glevel = Wk.nlevel.p;
+            V.gparent = Wk.nparent.p;
+        }
+    }
+    g.views.alloc(W);
+    DBFS_CUDA(cudaMemcpy(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice));
+    g.dist_scratch.alloc(64);
+    g.bfs_ready = true;
+    (void)ctx;
+}
+
+static int persistent_grid(Graph &g, int *blocks_per_sm) {
+    int occ = 0;
+    DBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_persistent, BT, 0));
+    DBFS_CHECK(occ >= 1, DBFS_EINTERNAL, "persistent kernel cannot be resident");
+    *blocks_per_sm = occ;
+    int grid = g.ctx->num_sms * occ;
+    grid = (grid / g.W) * g.W;
+    DBFS_CHECK(grid >= g.W, DBFS_EINTERNAL, "too many workers for one device");
+    return grid;
+}
+
+static AsmArgs make_asm(Graph &g, bool parents) {
+    AsmArgs a{};
+    a.n = g.n;
+    a.p = g.p;
+    a.pd.init((uint32_t)g.p);
+    a.del_id = g.del_id.p;
+    for (auto &Wk : g.workers) {
+        a.nlevel[Wk.w] = Wk.nlevel.p;
+        a.nparent[Wk.w] = Wk.nparent.p;
+    }
+    a.dlevel = g.workers[0].dlevel.p;
+    a.dparent = g.workers[0].dparent.p;
+    a.glevel = g.glevel.p;
+    a.gparent = g.gparent.p;
+    a.parents = parents;
+    return a;
+}
+
+// --------------------------------------------------------------- dist glue
+
+// NCCL exchange between V(L) and F(L) for one rank: delegate masks
+// (all-gather of d/8 bytes, OR-folded in F) and the alltoallv of nn records.
+static void dist_exchange(Graph &g, int L, std::vector<unsigned long long> &send_counts) {
+    Ctx &ctx = *g.ctx;
+    WorkerHost &Wk = g.workers[0];
+    const int p = g.p;
+    const int64_t nw_d = std::max<int64_t>(nwords(g.d), 1);
+    uint32_t *own = (L & 1) ? Wk.dnext1.p : Wk.dnext0.p;
+    nccl_allgather_bytes(ctx, own, g.mask_gather.p, nw_d * 4);
+    // send counts of this level (slot L%3)
+    Ctl hc;
+    DBFS_CUDA(cudaMemcpyAsync(&hc, Wk.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    const LevelSlot &A = hc.s[L % 3];
+    send_counts.assign(A.send, A.send + MAXW);
+    std::vector<int64_t> mine(p);
+    for (int o = 0; o < p; o++) mine[o] = (int64_t)A.send[o];
+    DArray<int64_t> s, r;
+    s.alloc(p);
+    r.alloc((int64_t)p * p);
+    DBFS_CUDA(cudaMemcpy(s.p, mine.data(), 8 * p, cudaMemcpyHostToDevice));
+    nccl_allgather_bytes(ctx, s.p, r.p, 8 * p);
+    std::vector<int64_t> all((size_t)p * p);
+    DBFS_CUDA(cudaMemcpy(all.data(), r.p, 8 * p * p, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
+    int64_t racc = 0;
+    for (int o = 0; o < p; o++) {
+        soff[o] = Wk.send_off[o] * 8;
+        sbytes[o] = o == ctx.rank ? 0 : mine[o] * 8;
+        int64_t c = o == ctx.rank ? 0 : all[(size_t)o * p + ctx.rank];
+        roff[o] = racc * 8;
+        rbytes[o] = c * 8;
+        racc += c;
+    }
+    uint2 *inbox = (L & 1) ? Wk.inbox1.p : Wk.inbox0.p;
+    nccl_alltoallv_bytes(ctx, Wk.sendbuf.p, soff.data(), sbytes.data(), inbox, roff.data(), rbytes.data());
+    unsigned long long rin = (unsigned long long)racc;
+    DBFS_CUDA(cudaMemcpyAsync(&Wk.ctl.p->s[L % 3].inbox, &rin, 8, cudaMemcpyHostToDevice, ctx.stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+// ------------------------------------------------------------------ driver
+
+void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
+    Ctx &ctx = *g.ctx;
+    DBFS_CHECK(o.mode == 0 || o.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
+    DBFS_CHECK(0 <= o.source && o.source < g.n, DBFS_ERANGE,
+               "source " + std::to_string(o.source) + " out of range [0, " + std::to_string(g.n) + ")");
+    ensure_resources(g);
+    const int W = g.W;
+    const bool parents = o.parent_mode != 0;
+    // per-run options into the views
+    for (auto &V : g.views_h) {
+        V.mode = o.mode;
+        V.allow_back = o.allow_switch_back;
+        V.parents = parents;
+        for (int k = 0; k < 4; k++) {
+            V.f0[k] = o.factor0[k];
+            V.f1[k] = o.factor1[k];
+        }
+    }
+    DBFS_CUDA(cudaMemcpyAsync(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice, ctx.stream));
+    uint32_t src_del = 0xffffffffu;
+    DBFS_CUDA(cudaMemcpyAsync(&src_del, g.del_id.p + o.source, 4, cudaMemcpyDeviceToHost, ctx.stream));
+    for (auto &Wk : g.workers) DBFS_CUDA(cudaMemsetAsync(Wk.ctl.p, 0, sizeof(Ctl), ctx.stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+
+    int engine = o.engine;
+    if (engine == 0) engine = g.dist ? 1 : 2;
+    DBFS_CHECK(!(g.dist && engine == 2), DBFS_EINVAL, "persistent engine needs all workers on one device");
+    const int64_t launches0 = g_kernel_launches;
+    const bool assemble = g.p > 1 && !g.dist;
+    AsmArgs aa = make_asm(g, parents);
+    int iterations = 0;
+    bool timeout = false;
+
+    DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
+    if (engine == 2) {
+        int bps = 0;
+        int grid = persistent_grid(g, &bps);
+        GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
+        DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
+        const View *vp = g.views.p;
+        int64_t src = o.source;
+        int rec_cap = g.rec_cap;
+        int do_asm = assemble ? 1 : 0;
+        void *args[] = {(void *)&vp, (void *)&W, (void *)&src, (void *)&src_del, (void *)&bar,
+                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm};
+        DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, 0, ctx.stream));
+        DBFS_LAUNCHED();
+        DBFS_CUDA(cudaEventRecord(ctx.ev1, ctx.stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+        GridBar hb;
+        DBFS_CUDA(cudaMemcpy(&hb, bar, sizeof(hb), cudaMemcpyDeviceToHost));
+        timeout = hb.abort != 0;
+        Ctl c0;
+        DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+        iterations = c0.last_level;
+    } else {
+        const int grid = std::max(W, (ctx.num_sms * 4 / W) * W);
+        k_init<<<grid, BT, 0, ctx.stream>>>(g.views.p, W);
+        DBFS_LAUNCHED();
+        k_seed<<<W, 32, 0, ctx.stream>>>(g.views.p, W, o.source, src_del);
+        DBFS_LAUNCHED();
+        std::vector<unsigned long long> sc;
+        std::vector<Ctl> hc(W);
+        int L = 0;
+        for (;; L++) {
+            k_visit<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L);
+            DBFS_LAUNCHED();
+            if (g.dist) dist_exchange(g, L, sc);
+            k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L);
+            DBFS_LAUNCHED();
+            for (int i = 0; i < W; i++)
+                DBFS_CUDA(cudaMemcpyAsync(&hc[i], g.workers[i].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+            DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+            // per-iteration record for level L (host copy of the device rule)
+            if (L < g.rec_cap) {
+                for (int i = 0; i < W; i++) {
+                    IterRec r;
+                    make_record(g.views_h[i], hc[i], L, r);
+                    DBFS_CUDA(cudaMemcpyAsync(g.workers[i].rec.p + L, &r, sizeof(r), cudaMemcpyHostToDevice,
+                                              ctx.stream));
+                }
+            }
+            unsigned long long act = hc[0].s[L % 3].new_del;
+            for (int i = 0; i < W; i++) act += hc[i].s[L % 3].local_claims + hc[i].s[L % 3].records;
+            if (g.dist) {
+                int64_t *buf = (int64_t *)g.dist_scratch.p;
+                int64_t v = (int64_t)act;
+                DBFS_CUDA(cudaMemcpyAsync(buf, &v, 8, cudaMemcpyHostToDevice, ctx.stream));
+                nccl_allreduce_i64(ctx, buf, 1, 0);
+                DBFS_CUDA(cudaMemcpyAsync(&v, buf, 8, cudaMemcpyDeviceToHost, ctx.stream));
+                DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+                act = (unsigned long long)v;
+            }
+            if (!act) break;
+        }
+        iterations = L + 1;
+        if (g.dist) {
+            // delegate parents: each rank holds its own candidates -> min over ranks
+            if (parents && g.d) nccl_allreduce_i64(ctx, g.workers[0].dparent.p, g.d, 1);
+            // gather every rank's normal levels/parents, then assemble the global arrays
+            WorkerHost &Wk = g.workers[0];
+            int64_t stride = ceil_div(g.n, g.p);
+            DArray<int32_t> lv;
+            DArray<int64_t> pv;
+            lv.alloc(stride * g.p);
+            pv.alloc(stride * g.p);
+            DArray<int32_t> mylv;
+            DArray<int64_t> mypv;
+            mylv.alloc(stride);
+            mypv.alloc(stride);
+            DBFS_CUDA(cudaMemsetAsync(mylv.p, 0xff, 4 * stride, ctx.stream));
+            DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, 8 * stride, ctx.stream));
+            if (Wk.n_local) {
+                DBFS_CUDA(cudaMemcpyAsync(mylv.p, Wk.nlevel.p, 4 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
+                DBFS_CUDA(cudaMemcpyAsync(mypv.p, Wk.nparent.p, 8 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
+            }
+            nccl_allgather_bytes(ctx, mylv.p, lv.p, 4 * stride);
+            if (parents) nccl_allgather_bytes(ctx, mypv.p, pv.p, 8 * stride);
+            for (int w = 0; w < g.p; w++) {
+                aa.nlevel[w] = lv.p + (int64_t)w * stride;
+                aa.nparent[w] = pv.p + (int64_t)w * stride;
+            }
+            k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
+            DBFS_LAUNCHED();
+            DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+        } else if (assemble) {
+            k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
+            DBFS_LAUNCHED();
+        }
+        DBFS_CUDA(cudaEventRecord(ctx.ev1, ctx.stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    DBFS_CUDA(cudaGetLastError());
+    DBFS_CHECK(!timeout, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
+    float ms = 0.f;
+    DBFS_CUDA(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1));
+
+    // collect per-iteration records
+    g.last_iterations = iterations;
+    g.last_truncated = iterations > g.rec_cap;
+    int nrec = std::min(iterations, g.rec_cap);
+    g.last_rec.assign((size_t)nrec * W, IterRec{});
+    for (int i = 0; i < W; i++) {
+        std::vector<IterRec> tmp(nrec);
+        if (nrec) DBFS_CUDA(cudaMemcpy(tmp.data(), g.workers[i].rec.p, sizeof(IterRec) * nrec, cudaMemcpyDeviceToHost));
+        for (int L = 0; L < nrec; L++) g.last_rec[(size_t)L * W + i] = tmp[L];
+    }
+    g.last_source = o.source;
+    g.last_parent_mode = o.parent_mode;
+    g.last_valid = true;
+    g.last_mode = o.mode;
+    g.last_la = o.local_all2all;
+    g.last_uq = o.uniquify;
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        st->iterations = iterations;
+        for (int L = 0; L < nrec; L++)
+            for (int i = 0; i < W; i++) {
+                const IterRec &r = g.last_rec[(size_t)L * W + i];
+                for (int k = 0; k < 4; k++) st->inspections[k][r.dir[k]] += (int64_t)r.insp[k];
+            }
+        st->device_ms = ms;
+        st->kernel_launches = g_kernel_launches - launches0;
+        st->per_iteration_truncated = g.last_truncated;
+        st->engine_used = engine;
+        int64_t wire = 0;
+        for (int L = 0; L < nrec; L++)
+            for (int i = 0; i < W; i++) {
+                const IterRec &r = g.last_rec[(size_t)L * W + i];
+                wire += (int64_t)r.records * 8;
+                if (r.new_del && g.p > 1) wire += (int64_t)(g.p - 1) * nwords(g.d) * 4 / W;
+            }
+        st->wire_bytes = wire;
+        int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
+        st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
+    }
+    if (g.dist && st) {
+        // inspections are per rank; sum over ranks
+        DArray<int64_t> t;
+        t.alloc(8);
+        int64_t h[8];
+        for (int k = 0; k < 4; k++) {
+            h[2 * k] = st->inspections[k][0];
+            h[2 * k + 1] = st->inspections[k][1];
+        }
+        DBFS_CUDA(cudaMemcpy(t.p, h, sizeof(h), cudaMemcpyHostToDevice));
+        nccl_allreduce_i64(ctx, t.p, 8, 0);
+        DBFS_CUDA(cudaMemcpy(h, t.p, sizeof(h), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < 4; k++) {
+            st->inspections[k][0] = h[2 * k];
+            st->inspections[k][1] = h[2 * k + 1];
+        }
+        int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
+        st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
+    }
+}
+
+// ----------------------------------------------------------------- results
+
+__global__ void k_count_reached(const int32_t *__restrict__ lv, int64_t n, unsigned long long *out) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += lv[i] >= 0;
+    c = warp_sum(c);
+    if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+void fetch_result(Graph &g, int32_t *levels, int64_t *parents) {
+    DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+    Ctx &ctx = *g.ctx;
+    if (levels) DBFS_CUDA(cudaMemcpyAsync(levels, g.levels_dev(), 4 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+    if (parents) {
+        DBFS_CHECK(g.last_parent_mode != 0, DBFS_EINVAL, "last BFS ran without parents");
+        DBFS_CUDA(cudaMemcpyAsync(parents, g.parents_dev(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+    }
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+// ------------------------------------------------ min-ID parents (A19) / A20
+
+struct EdgeWalk {
+    const int64_t *off;
+    const uint32_t *col;
+    int64_t rows;
+    int kind, w;
+    PDiv pd;
+    const int64_t *del_gid;
+};
+
+__device__ __forceinline__ int64_t row_gid(const EdgeWalk &e, int64_t r) {
+    return (e.kind == KIND_NN || e.kind == KIND_ND) ? r * e.pd.p + e.w : e.del_gid[r];
+}
+__device__ __forceinline__ int64_t col_gid(const EdgeWalk &e, uint32_t c) {
+    if (e.kind == KIND_NN) return c;
+    if (e.kind == KIND_DN) return (int64_t)c * e.pd.p + e.w;
+    return e.del_gid[c];
+}
+
+// parent[v] = min{u : (u->v) in E, level[u] = level[v]-1}
+__global__ void k_min_parents(EdgeWalk e, const int32_t *__restrict__ lv, unsigned long long *__restrict__ par) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (int64_t r = gw; r < e.rows; r += TW) {
+        int64_t u = row_gid(e, r);
+        int32_t lu = lv[u];
+        if (lu < 0) continue;
+        for (int64_t j = e.off[r] + lane; j < e.off[r + 1]; j += 32) {
+            int64_t v = col_gid(e, e.col[j]);
+            if (lv[v] == lu + 1) atomicMin(&par[v], (unsigned long long)u);
+        }
+    }
+}
+
+__global__ void k_par_init(const int32_t *__restrict__ lv, int64_t n, unsigned long long *par) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        par[v] = lv[v] >= 0 ? 0x7fffffffffffffffull : 0xffffffffffffffffull;
+}
+
+static EdgeWalk walk_of(Graph &g, WorkerHost &Wk, int k) {
+    EdgeWalk e;
+    e.off = g.off_all.p + Wk.base[k];
+    e.col = g.col_all.p;
+    e.rows = Wk.rows[k];
+    e.kind = k;
+    e.w = Wk.w;
+    e.pd.init((uint32_t)g.p);
+    e.del_gid = g.del_gid.p;
+    return e;
+}
+
+void min_parents(Graph &g, int64_t *out) {
+    DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+    Ctx &ctx = *g.ctx;
+    DArray<unsigned long long> par;
+    par.alloc(std::max<int64_t>(g.n, 1));
+    const int32_t *lv = g.levels_dev();
+    k_par_init<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(lv, g.n, par.p);
+    DBFS_LAUNCHED();
+    for (auto &Wk : g.workers)
+        for (int k = 0; k < 4; k++) {
+            EdgeWalk e = walk_of(g, Wk, k);
+            if (e.rows == 0) continue;
+            k_min_parents<<<ctx.num_sms * 8, BT, 0, ctx.stream>>>(e, lv, par.p);
+            DBFS_LAUNCHED();
+        }
+    if (g.dist) nccl_allreduce_i64(ctx, (int64_t *)par.p, g.n, 1);  // unsigned -1 stays max; reached < INT64_MAX
+    DBFS_CUDA(cudaMemcpyAsync(out, par.p, 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    int64_t root = g.last_source;
+    out[root] = root;
+    for (int64_t v = 0; v < g.n; v++)
+        if ((uint64_t)out[v] == 0xffffffffffffffffull) out[v] = -1;
+}
+
+__global__ void k_validate_edges(EdgeWalk e, const int32_t *__restrict__ lv, const int64_t *__restrict__ par,
+                                 uint8_t *__restrict__ ok, unsigned int *__restrict__ bad) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    unsigned b = 0;
+    for (int64_t r = gw; r < e.rows; r += TW) {
+        int64_t u = row_gid(e, r);
+        int32_t lu = lv[u];
+        for (int64_t j = e.off[r] + lane; j < e.off[r + 1]; j += 32) {
+            int64_t v = col_gid(e, e.col[j]);
+            int32_t lvv = lv[v];
+            if ((lu >= 0) != (lvv >= 0)) b |= 4;
+            else if (lu >= 0 && (lu - lvv > 1 || lvv - lu > 1)) b |= 2;
+            if (lvv >= 0 && par[v] == u) ok[v] = 1;
+        }
+    }
+    b = __reduce_or_sync(0xffffffffu, b);
+    if (lane == 0 && b) atomicOr(bad, b);
+}
+
+__global__ void k_validate_vertices(const int32_t *__restrict__ lv, const int64_t *__restrict__ par,
+                                    const uint8_t *__restrict__ ok, int64_t n, int64_t root,
+                                    unsigned int *__restrict__ bad) {
+    unsigned b = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int32_t l = lv[v];
+        int64_t pv = par[v];
+        if (v == root) {
+            if (l != 0 || pv != root) b |= 1;
+            continue;
+        }
+        if (l < 0) {
+            if (pv != -1) b |= 32;
+            continue;
+        }
+        if (pv < 0 || pv >= n) {
+            b |= 32;
+            continue;
+        }
+        if (lv[pv] != l - 1) b |= 8;
+        if (!ok[v]) b |= 16;
+    }
+    b = __reduce_or_sync(0xffffffffu, b);
+    if (lane_id() == 0 && b) atomicOr(bad, b);
+}
+
+int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents) {
+    Ctx &ctx = *g.ctx;
+    DBFS_CHECK(0 <= root && root < g.n, DBFS_ERANGE, "root out of range");
+    DArray<int32_t> lvh;
+    DArray<int64_t> pah;
+    const int32_t *lv;
+    const int64_t *pa;
+    if (levels) {
+        lvh.alloc(std::max<int64_t>(g.n, 1));
+        DBFS_CUDA(cudaMemcpy(lvh.p, levels, 4 * g.n, cudaMemcpyHostToDevice));
+        lv = lvh.p;
+    } else {
+        DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+        lv = g.levels_dev();
+    }
+    if (parents) {
+        pah.alloc(std::max<int64_t>(g.n, 1));
+        DBFS_CUDA(cudaMemcpy(pah.p, parents, 8 * g.n, cudaMemcpyHostToDevice));
+        pa = pah.p;
+    } else {
+        DBFS_CHECK(g.last_valid && g.last_parent_mode != 0, DBFS_EINVAL, "no parents on device");
+        pa = g.parents_dev();
+    }
+    DArray<uint8_t> ok;
+    ok.alloc(std::max<int64_t>(g.n, 1));
+    DBFS_CUDA(cudaMemsetAsync(ok.p, 0, ok.bytes(), ctx.stream));
+    DArray<unsigned int> bad;
+    bad.alloc(1);
+    DBFS_CUDA(cudaMemsetAsync(bad.p, 0, 4, ctx.stream));
+    for (auto &Wk : g.workers)
+        for (int k = 0; k < 4; k++) {
+            EdgeWalk e = walk_of(g, Wk, k);
+            if (e.rows == 0) continue;
+            k_validate_edges<<<ctx.num_sms * 8, BT, 0, ctx.stream>>>(e, lv, pa, ok.p, bad.p);
+            DBFS_LAUNCHED();
+        }
+    if (g.dist) nccl_allreduce_u8_max(ctx, ok.p, g.n);  // tree-edge marks OR-ed over ranks
+    k_validate_vertices<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(lv, pa, ok.p, g.n, root, bad.p);
+    DBFS_LAUNCHED();
+    unsigned int hb = 0;
+    if (g.dist) {  // failure bits OR-ed over ranks
+        DArray<unsigned int> all;
+        all.alloc(g.p);
+        nccl_allgather_bytes(ctx, bad.p, all.p, 4);
+        std::vector<unsigned int> h(g.p);
+        DBFS_CUDA(cudaMemcpy(h.data(), all.p, 4 * g.p, cudaMemcpyDeviceToHost));
+        for (unsigned x : h) hb |= x;
+    } else {
+        DBFS_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    return (int)hb;
+}
+
+}  // namespace dbfs

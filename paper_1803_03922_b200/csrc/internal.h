@@ -1,0 +1,239 @@
+// internal.h -- host/device data structures of libdbfs.
+//
+// Layout in HBM (per worker w, all on the worker's device):
+//   CSR  : one concatenated int64 offset array and one uint32 column array for
+//          all local workers and kinds (nn | nd | dn | dd rows per worker).  A
+//          kind's offsets are absolute positions into the column array, so the
+//          kernels never rebase.  nn columns are global vertex ids (uint32; the
+//          reference's int64 ids are restored on export), nd/dd columns are
+//          delegate ids, dn columns are local normal ids (partition.py:319-326).
+//   state: int32 level + int64 parent per local normal (the global arrays when
+//          p == 1), int32 level + int64 parent per delegate, bitmaps
+//          (1 bit/vertex) for visited / frontier / next-frontier of normals and
+//          delegates, double-buffered by level parity.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace dbfs {
+
+// Per-level counters of one worker.  Slot L%3 holds the stats of the frontier
+// at level L (accumulated while level L-1 ran) and the activity of level L.
+struct LevelSlot {
+    unsigned long long fv[4];        // FV per kind of this level's frontier (traversal.py:72)
+    unsigned long long q[4];         // |queue| per kind (previsit queue sizes)
+    unsigned long long nfront;       // normals in the frontier
+    unsigned long long dfront;       // delegates in the frontier
+    unsigned long long chunks;       // hub chunk entries for the delegate frontier
+    unsigned long long insp_bwd[4];  // backward inspections at this level
+    unsigned long long records;      // remote normal records sent at this level
+    unsigned long long local_claims; // local normals claimed for level+1 (engine.py:280-289)
+    unsigned long long dirty;        // this worker found >= 1 new delegate (comm.py:33-36)
+    unsigned long long new_del;      // delegates discovered at the barrier
+    unsigned long long inbox;        // records delivered to this worker
+    unsigned long long send[MAXW];   // records per destination worker
+};
+
+struct Ctl {
+    LevelSlot s[3];
+    int dir[2][4];                   // sticky DirectionState by level parity
+    unsigned long long cumq[2][4];   // visited source counts through the level, by parity
+    unsigned int bar_count, bar_gen; // grid barrier (persistent engine)
+    unsigned int abort;              // watchdog / error flag
+    int last_level;                  // iterations when the loop ended
+    int cont;                        // host-loop: continue flag
+    int pad;
+};
+
+// Per worker per level record (BfsRun.per_iteration before summing workers).
+struct IterRec {
+    int dir[4];
+    double bv[4];
+    unsigned long long fv[4];
+    unsigned long long insp[4];
+    unsigned long long records;
+    unsigned long long dirty;
+    unsigned long long messages;
+    unsigned long long new_del;
+    unsigned long long send[MAXW];
+};
+
+// Device-visible description of one worker (lives in device memory).
+struct View {
+    int w, W, p, p_rank, dist;       // global index, local worker count, shape
+    int mode, allow_back, parents;
+    int cand_all;                    // all workers' delegate candidates readable
+    int P_sources;                   // mask sources for the OR
+    int rec_cap;
+    int hub;                         // rows longer than this go to hub chunks
+    int chunk;                       // edges per hub chunk
+    int pad0;
+    PDiv pd;
+    int64_t n, n_local, d, nw_n, nw_d;
+    double f0[4], f1[4];
+    unsigned long long total_src[4]; // |nd_src|, |dn_src|, |dd_src| (index by kind)
+    const int64_t *off[4];
+    const uint32_t *col[4];
+    const uint32_t *src_bits[4];     // [ND] nd sources (n_local bits), [DN] dn, [DD] dd (d bits)
+    const int64_t *del_gid;
+    int32_t *nlevel;
+    int64_t *nparent;
+    int32_t *dlevel;
+    int64_t *dparent;
+    int64_t *dcand;
+    uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
+    uint64_t *chunks[2];
+    int64_t chunk_cap;
+    uint2 *inbox[2];
+    int64_t inbox_cap;
+    uint2 *sendbin[MAXW];            // dist: per destination segment
+    int64_t sendcap[MAXW];
+    Ctl *ctl;
+    Ctl *ctl_all[MAXW];              // in-process: every worker's control block
+    uint2 *inbox_all[2][MAXW];       // in-process: every worker's inboxes
+    const uint32_t *mask_src[2][MAXW];
+    const int64_t *cand_src[MAXW];
+    IterRec *rec;
+    int32_t *glevel;                 // global outputs when p == 1 (alias nlevel)
+    int64_t *gparent;
+};
+
+template <typename T>
+struct DArray {
+    T *p = nullptr;
+    int64_t n = 0;
+    DArray() = default;
+    DArray(const DArray &) = delete;
+    DArray &operator=(const DArray &) = delete;
+    DArray(DArray &&o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DArray &operator=(DArray &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DArray() { release(); }
+    void alloc(int64_t count) {
+        release();
+        n = count;
+        if (count > 0) DBFS_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)count));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return sizeof(T) * (size_t)n; }
+};
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int nranks = 1, rank = 0;
+    void *comm = nullptr;            // ncclComm_t
+    DArray<unsigned char> scratch;   // reusable device scratch
+    void *ensure_scratch(size_t bytes);
+};
+
+struct WorkerHost {
+    int w = 0;
+    int64_t n_local = 0;
+    int64_t base[4] = {0, 0, 0, 0};  // first offset index of each kind in off_all
+    int64_t rows[4] = {0, 0, 0, 0};
+    int64_t nnz[4] = {0, 0, 0, 0};
+    int64_t n_src[4] = {0, 0, 0, 0}; // |nd_src| at [ND], |dn_src| at [DN], |dd_src| at [DD]
+    int64_t remote_cap[MAXW];        // nn edges on this worker whose column is owned by dest
+    DArray<uint32_t> src_bits[4];
+    // BFS state
+    DArray<int32_t> nlevel, dlevel;
+    DArray<int64_t> nparent, dparent, dcand;
+    DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
+    DArray<uint64_t> chunks0, chunks1;
+    DArray<uint2> inbox0, inbox1, sendbuf;
+    DArray<Ctl> ctl;
+    DArray<IterRec> rec;
+    int64_t chunk_cap = 0, inbox_cap = 0;
+    int64_t send_off[MAXW + 1];
+};
+
+struct Graph {
+    Ctx *ctx = nullptr;
+    int64_t n = 0, m = 0, d = 0, theta = 0;
+    int p_rank = 1, p_gpu = 1, p = 1;
+    int W = 1, first_worker = 0;
+    bool dist = false;
+    int64_t kind_totals[4] = {0, 0, 0, 0};
+    DArray<uint32_t> degree;         // out-degree per global vertex
+    DArray<uint32_t> del_id;         // delegate id per global vertex, 0xffffffff for normals
+    DArray<int64_t> del_gid;         // delegate global ids (ascending)
+    DArray<int64_t> off_all;         // concatenated CSR offsets (absolute)
+    DArray<uint32_t> col_all;        // concatenated CSR columns
+    std::vector<WorkerHost> workers; // local workers
+    // BFS engine resources (allocated on first BFS)
+    bool bfs_ready = false;
+    DArray<View> views;
+    std::vector<View> views_h;
+    DArray<int32_t> glevel;          // assembled outputs (p > 1)
+    DArray<int64_t> gparent;
+    DArray<uint32_t> mask_gather;    // dist: allgather of dnext slices
+    DArray<unsigned long long> dist_scratch;
+    int rec_cap = 0;
+    // last run
+    int64_t last_iterations = 0;
+    int64_t last_source = -1;
+    int last_parent_mode = 0;
+    bool last_valid = false;
+    bool last_truncated = false;
+    std::vector<IterRec> last_rec;   // [iteration][local worker]
+    std::vector<std::vector<unsigned long long>> last_send_matrix;
+    int last_mode = 1, last_la = 0, last_uq = 0;
+    ~Graph();
+    int32_t *levels_dev();
+    int64_t *parents_dev();
+};
+
+// build.cu
+void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm);
+void build_graph_edges(Graph &g, const int64_t *src, const int64_t *dst, int64_t m_local);
+void export_csr(const Graph &g, int worker, int kind, int64_t *off, void *cols);
+void export_sources(const Graph &g, int worker, int64_t *nd_src, uint8_t *dn, uint8_t *dd);
+void export_classification(const Graph &g, int64_t *deg, int64_t *del);
+void hash_vertices_host(Ctx &ctx, int64_t n, uint64_t seed, const int64_t *in, int64_t *out, int64_t count);
+void rmat_generate_host(Ctx &ctx, const dbfs_rmat_params &prm, int64_t begin, int64_t end,
+                        int64_t *src, int64_t *dst);
+
+// bfs.cu
+void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st);
+void fetch_result(Graph &g, int32_t *levels, int64_t *parents);
+void min_parents(Graph &g, int64_t *out);
+int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents);
+
+// dist.cu (NCCL)
+void nccl_unique_id(uint8_t *out);
+void nccl_init(Ctx &ctx, const uint8_t *uid, int nranks, int rank);
+void nccl_destroy(Ctx &ctx);
+void nccl_allreduce_u32_sum(Ctx &ctx, uint32_t *dbuf, int64_t count);
+void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op_min);
+void nccl_allreduce_f64_max(Ctx &ctx, double *dbuf, int64_t count);
+void nccl_allgather_bytes(Ctx &ctx, const void *send, void *recv, int64_t bytes);
+void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, const int64_t *send_bytes,
+                          void *recv, const int64_t *recv_off, const int64_t *recv_bytes);
+void nccl_barrier(Ctx &ctx);
+void nccl_allreduce_u8_max(Ctx &ctx, uint8_t *dbuf, int64_t count);
+
+// scan.cu helpers (device-wide exclusive scans)
+void exclusive_scan_u32_to_i64(Ctx &ctx, const uint32_t *in, int64_t *out, int64_t n);  // out has n+1
+void radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, uint32_t *vals_alt,
+                      int64_t n, int bits, bool *result_in_alt);
+
+}  // namespace dbfs

@@ -1,0 +1,255 @@
+"""BFS driver API (mirror of delegate_bfs.engine) over the libdbfs GPU engine.
+
+``run_bfs(pg, BfsOptions)`` has the reference's signature and result type
+(engine.py:98-330): identical ``levels``, ``iterations``, ``per_iteration``
+records, ``inspections``, ``comm_stats`` and ``levels_digest``.  Timing
+(``elapsed``/``teps``) is the wall clock of the call, like the reference;
+``device_ms`` adds the CUDA-event time of the traversal alone.
+
+New on top of the reference: ``bfs(pg, root)`` returns
+(depth, parent) like Graph500, and ``validate_bfs_tree`` runs the O(m)
+certificate on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import hashlib
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, traversal
+from .comm import CommStats
+from .partition import PartitionedGraph
+from .traversal import BACKWARD, DO_KINDS, FORWARD
+
+MODES = ("bfs", "dobfs")
+KINDS = ("nn", "nd", "dn", "dd")
+PARENT_MODES = {None: 0, "none": 0, "any": 1, "min": 2}
+ENGINES = {"auto": 0, "host": 1, "persistent": 2}
+
+
+class EmptyReportError(RuntimeError):
+    """Every benchmark run was discarded (S <= 1)."""
+
+
+@dataclass
+class BfsOptions:
+    """engine.py:33-46, plus ``parents`` / ``engine`` switches of this build."""
+
+    mode: str = "dobfs"
+    source: int = 0
+    factor0: dict = field(default_factory=lambda: dict(traversal.DEFAULT_FACTOR0))
+    factor1: dict = field(default_factory=lambda: dict(traversal.DEFAULT_FACTOR1))
+    local_all2all: bool = False
+    uniquify: bool = False
+    allow_switch_back: bool = True
+    seed: int = 0
+    parents: str | None = "any"
+    engine: str = "auto"
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.parents not in PARENT_MODES:
+            raise ValueError(f"parents must be one of {list(PARENT_MODES)}")
+        if self.engine not in ENGINES:
+            raise ValueError(f"engine must be one of {list(ENGINES)}")
+
+    def to_c(self) -> _lib.BfsOptionsC:
+        o = _lib.BfsOptionsC()
+        o.mode = MODES.index(self.mode)
+        o.allow_switch_back = int(self.allow_switch_back)
+        o.source = int(self.source)
+        for i, k in enumerate(KINDS):
+            o.factor0[i] = float(self.factor0.get(k, 0.0)) if k != "nn" else 0.0
+            o.factor1[i] = float(self.factor1.get(k, 0.0)) if k != "nn" else 0.0
+        o.local_all2all = int(self.local_all2all)
+        o.uniquify = int(self.uniquify)
+        o.parent_mode = PARENT_MODES[self.parents]
+        o.engine = ENGINES[self.engine]
+        o.record_iterations = 1
+        return o
+
+
+@dataclass
+class BfsRun:
+    levels: np.ndarray
+    iterations: int
+    per_iteration: list
+    inspections: dict
+    comm_stats: CommStats
+    b_measured: float
+    elapsed: float
+    teps: float
+    levels_digest: str
+    m_prime: int | None = None
+    parents: np.ndarray | None = None
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+    @property
+    def total_inspections(self) -> int:
+        return sum(v["forward"] + v["backward"] for v in self.inspections.values())
+
+    def to_dict(self) -> dict:
+        return {
+            "iterations": self.iterations,
+            "per_iteration": self.per_iteration,
+            "inspections": self.inspections,
+            "total_inspections": self.total_inspections,
+            "comm": self.comm_stats.to_dict(),
+            "b_measured": self.b_measured,
+            "m_prime": self.m_prime,
+            "elapsed": self.elapsed,
+            "teps": self.teps,
+            "levels_digest": self.levels_digest,
+        }
+
+
+def levels_digest(levels: np.ndarray) -> str:
+    """blake2b-8 over little-endian int32 levels (engine.py:81-83)."""
+    data = np.ascontiguousarray(levels, dtype="<i4").tobytes()
+    return hashlib.blake2b(data, digest_size=8).hexdigest()
+
+
+def compute_teps(m: int, elapsed: float) -> float:
+    """(m/2)/elapsed (engine.py:86-90)."""
+    if elapsed <= 0:
+        raise ValueError("elapsed must be positive")
+    return (m / 2) / elapsed
+
+
+def _bfs_raw(pg: PartitionedGraph, opts: BfsOptions, levels_out, parents_out):
+    st = _lib.RunStatsC()
+    o = opts.to_c()
+    lv = levels_out.ctypes.data_as(_lib.vp) if levels_out is not None else None
+    pa = parents_out.ctypes.data_as(_lib.vp) if parents_out is not None else None
+    _lib.check(_lib.load().dbfs_bfs(pg.handle, ctypes.byref(o), lv, pa, ctypes.byref(st)), "bfs")
+    return st
+
+
+def _per_iteration(pg: PartitionedGraph, iterations: int):
+    """BfsRun.per_iteration + CommStats from the device records (engine.py:291-302)."""
+    L = _lib.load()
+    p = pg.shape.p
+    recs, comm = [], CommStats()
+    rec = _lib.IterationC()
+    dirs = np.zeros(p * 4, dtype=np.int8)
+    bv = np.zeros(p * 4, dtype=np.float64)
+    for it in range(iterations):
+        rc = L.dbfs_bfs_iteration(pg.handle, it, ctypes.byref(rec), dirs.ctypes.data_as(_lib.vp),
+                                  bv.ctypes.data_as(_lib.vp))
+        if rc == _lib.DBFS_ERANGE:  # truncated record buffer
+            break
+        _lib.check(rc)
+        d = dirs.reshape(p, 4)
+        b = bv.reshape(p, 4)
+        recs.append({
+            "iteration": it,
+            "directions": {k: [FORWARD if d[w, i] == 0 else BACKWARD for w in range(p)] for i, k in enumerate(KINDS)},
+            "inspections": {k: int(rec.inspections[i]) for i, k in enumerate(KINDS)},
+            "fv": {k: int(rec.fv[i]) for i, k in enumerate(KINDS)},
+            "bv": {k: [None if not math.isfinite(b[w, KINDS.index(k)]) else float(b[w, KINDS.index(k)])
+                       for w in range(p)] for k in DO_KINDS},
+            "mask_bytes": float(rec.mask_bytes),
+            "normal_bytes": int(rec.normal_bytes),
+        })
+        comm.mask_bytes.append(float(rec.mask_bytes))
+        comm.normal_bytes.append(int(rec.normal_bytes))
+        comm.message_count.append(int(rec.message_count))
+        comm.pair_count.append(int(rec.pair_count))
+    return recs, comm
+
+
+def run_bfs(pg: PartitionedGraph, opts: BfsOptions) -> BfsRun:
+    """One BFS/DOBFS on the GPU with the reference's result (engine.py:98-330)."""
+    t0 = time.perf_counter()
+    n = pg.n
+    if not (0 <= opts.source < n):
+        raise ValueError(f"source {opts.source} out of range [0, {n})")
+    levels = np.empty(n, dtype=np.int32)
+    parents = np.empty(n, dtype=np.int64) if opts.parents else None
+    st = _bfs_raw(pg, opts, levels, parents)
+    elapsed = time.perf_counter() - t0
+    if opts.parents == "min":
+        parents = min_parents(pg)
+    per_it, comm = _per_iteration(pg, st.iterations)
+    comm.wire_bytes = int(st.wire_bytes)
+    insp = {k: {"forward": int(st.inspections[i][0]), "backward": int(st.inspections[i][1])}
+            for i, k in enumerate(KINDS)}
+    return BfsRun(levels=levels, iterations=int(st.iterations), per_iteration=per_it, inspections=insp,
+                  comm_stats=comm, b_measured=float(st.b_measured), elapsed=elapsed,
+                  teps=compute_teps(pg.m, elapsed), levels_digest=levels_digest(levels), parents=parents,
+                  device_ms=float(st.device_ms), kernel_launches=int(st.kernel_launches))
+
+
+def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
+    """Per-source runs, discard S <= 1, geometric-mean TEPS (engine.py:333-364);
+    the Graph500 harmonic mean is reported beside it."""
+    runs = []
+    sources = list(sources)
+    for s in sources:
+        run = run_bfs(pg, dataclasses.replace(opts, source=int(s)))
+        if run.iterations > 1:
+            runs.append((int(s), run))
+    if not runs:
+        raise EmptyReportError("all runs discarded (every source trivial)")
+    teps = np.array([r.teps for _, r in runs])
+    geomean = float(np.exp(np.log(teps).mean()))
+    harmonic = float(len(teps) / np.sum(1.0 / teps))
+    return {
+        "num_runs": len(runs),
+        "num_discarded": len(sources) - len(runs),
+        "geomean_teps": geomean,
+        "harmonic_teps": harmonic,
+        "runs": [
+            {
+                "source": s,
+                "iterations": r.iterations,
+                "teps": r.teps,
+                "total_inspections": r.total_inspections,
+                "mask_bytes": r.comm_stats.total_mask_bytes,
+                "normal_bytes": r.comm_stats.total_normal_bytes,
+                "s_prime": r.comm_stats.s_prime,
+                "levels_digest": r.levels_digest,
+            }
+            for s, r in runs
+        ],
+    }
+
+
+def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobfs"):
+    """Graph500-style BFS: (depth int32[n], parent int64[n]).  ``parents="min"``
+    gives the deterministic min-ID tree."""
+    opts = BfsOptions(mode=mode, source=int(root), parents="any")
+    levels = np.empty(pg.n, dtype=np.int32)
+    par = np.empty(pg.n, dtype=np.int64)
+    _bfs_raw(pg, opts, levels, par)
+    if parents == "min":
+        par = min_parents(pg)
+    return levels, par
+
+
+def min_parents(pg: PartitionedGraph) -> np.ndarray:
+    """Min-ID parents of the last BFS, computed on the GPU."""
+    out = np.empty(pg.n, dtype=np.int64)
+    _lib.check(_lib.load().dbfs_min_parents(pg.handle, out.ctypes.data_as(_lib.vp)), "min_parents")
+    return out
+
+
+def validate_bfs_tree(pg: PartitionedGraph, root: int, levels=None, parents=None) -> int:
+    """Graph500 certificate on the GPU.  0 = valid, else a bitmask:
+    1 root, 2 edge spans > 1 level, 4 reached-unreached edge, 8 parent level,
+    16 tree edge not in E, 32 parent of unreached / missing parent."""
+    rep = ctypes.c_int32()
+    lv = np.ascontiguousarray(levels, dtype=np.int32).ctypes.data_as(_lib.vp) if levels is not None else None
+    pa = np.ascontiguousarray(parents, dtype=np.int64).ctypes.data_as(_lib.vp) if parents is not None else None
+    keep = (levels, parents)
+    _lib.check(_lib.load().dbfs_validate(pg.handle, int(root), lv, pa, ctypes.byref(rep)), "validate")
+    del keep
+    return int(rep.value)
