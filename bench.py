@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py -- Graph500 harmonic-mean GTEPS of the B200 delegate BFS/DOBFS.
+
+Workload (BASELINE.json configs[1]): RMAT scale 24, edge factor 16 (Graph500
+quadrants, seed 0, hash-randomized, symmetrized), Θ = 16 (the reference's
+Θ curve, cli.py:22-26), DOBFS with the paper's factors, 64 Graph500 roots
+(first 64 distinct vertices with degree > 0 from default_rng(0)).
+A step is one BFS from one root; K steps cycle through the 64 roots.
+
+  value : sum over steps of (m/2) / sum of device times  == harmonic-mean TEPS
+          (graph already resident in HBM; depth + parent arrays complete in
+          device memory at the end of every step; L2 flushed between steps)
+  e2e   : the same through the public API ``bfs(pg, root, out=pinned)`` with
+          the depth/parent arrays copied to pinned host memory every step
+  roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md §Measurement
+
+Multi-GPU (torchrun, one process per GPU): weak scaling, scale = 24 + log2(N),
+one worker per GPU over NCCL; step time = max over ranks.
+``--impl reference`` times the CPU restatement of the reference (oracle/) on
+this host on the same config (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Graph500 harmonic-mean GTEPS, RMAT weak/strong scaling at 1/2/4/8 B200"
+UNIT = "GTEPS"
+L2_BYTES = 126 << 20
+
+
+def suggested_theta(scale: int) -> int:
+    """cli.py:22-26: 64 at scale 30, sqrt(2) per scale, clamped to [16, 512]."""
+    theta = 64.0 * math.sqrt(2.0) ** (scale - 30)
+    return int(min(max(round(theta), 16), 512))
+
+
+def graph500_roots(degrees: np.ndarray, count: int = 64, seed: int = 0) -> list[int]:
+    """First `count` distinct vertices with out-degree > 0 from default_rng(seed)
+    (the reference's RNG, cli.py:151, with Graph500's degree >= 1 rule)."""
+    rng = np.random.default_rng(seed)
+    n = len(degrees)
+    out, seen = [], set()
+    while len(out) < count:
+        for v in rng.integers(0, n, size=4096).tolist():
+            if v not in seen and degrees[v] > 0:
+                seen.add(v)
+                out.append(v)
+                if len(out) == count:
+                    break
+    return out
+
+
+def measured_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, val in zip(names, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def alg_bytes(st, n_total: int) -> float:
+    """Algorithmic bytes of one BFS: every inspection
+    reads a 4-byte column and tests one status bit; every expanded/scanned row
+    reads two 8-byte offsets; the depth (4 B) and parent (8 B) arrays are
+    written once per vertex."""
+    insp = sum(st.inspections[k][0] + st.inspections[k][1] for k in range(4))
+    return insp * (4.0 + 1.0 / 8.0) + 16.0 * st.rows_touched + 12.0 * n_total
+
+
+# ------------------------------------------------------------------- our arm
+
+def run_ours(args, world, rank, local_rank):
+    import paper_1803_03922_b200 as api
+    from paper_1803_03922_b200 import _lib
+    from paper_1803_03922_b200.engine import bfs, bfs_device
+
+    dist = world > 1
+    tdist = None
+    if dist:
+        import datetime
+
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=30))
+    ctx = _lib.Context(local_rank if dist else args.device)
+    _lib.set_default_context(ctx)
+    if dist:
+        uid = [_lib.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        ctx.init_dist(uid[0], world, rank)
+
+    scale = args.scale + (int(round(math.log2(world))) if (dist and args.scaling == "weak") else 0)
+    theta = args.theta if args.theta is not None else suggested_theta(scale)
+    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40)
+    t0 = time.perf_counter()
+    pg = api.partition_graph(api.build_rmat_graph(params), theta,
+                             api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
+    if dist:
+        ctx.barrier()
+    build_s = time.perf_counter() - t0
+    n, m = pg.n, pg.m
+    degrees = pg.classification.out_degree
+    roots = graph500_roots(degrees, args.roots)
+    parents = "any"
+
+    def step(root):
+        return bfs_device(pg, root, mode=args.mode, parents=parents)
+
+    for i in range(args.warmup):
+        step(roots[i % len(roots)])
+    sampler = ClockSampler(local_rank if dist else args.device)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        ctx.barrier()
+    launches0 = _lib.kernel_launches()
+    dev_ms, wall0 = [], time.perf_counter()
+    stats = []
+    for i in range(args.steps):
+        ctx.flush_l2()  # outside the CUDA-event window of the step
+        st = step(roots[i % len(roots)])
+        dev_ms.append(st.device_ms)
+        stats.append(st)
+    if dist:
+        ctx.barrier()
+    wall = time.perf_counter() - wall0
+    launches = _lib.kernel_launches() - launches0
+
+    # e2e through the public API: depth + parent to pinned host buffers every step
+    lv_buf = _lib.pinned_empty(n, np.int32)
+    pa_buf = _lib.pinned_empty(n, np.int64)
+    e2e_s, h2d, d2h = [], 0, 0
+    for i in range(args.steps):
+        ctx.flush_l2()
+        t = time.perf_counter()
+        _, _, st = bfs(pg, roots[i % len(roots)], mode=args.mode, out=(lv_buf.array, pa_buf.array), stats=True)
+        e2e_s.append(time.perf_counter() - t)
+        h2d += st.h2d_bytes + 8
+        d2h += st.d2h_bytes
+    clocks = sampler.stop()
+
+    # max over ranks, per step
+    if dist:
+        dev_ms = list(_allreduce_max(ctx, np.array(dev_ms, dtype=np.float64)))
+        e2e_s = list(_allreduce_max(ctx, np.array(e2e_s, dtype=np.float64)))
+    total_dev_s = sum(dev_ms) / 1e3
+    value = args.steps * (m / 2) / total_dev_s / 1e9
+    per_root = [(m / 2) / (t / 1e3) / 1e9 for t in dev_ms]
+    geomean = float(np.exp(np.mean(np.log(per_root))))
+    e2e_value = args.steps * (m / 2) / sum(e2e_s) / 1e9
+
+    # correctness of what was timed: certificate on a few roots, digest vs oracle sample
+    validated = 0
+    for r in roots[: min(4, len(roots))]:
+        bfs_device(pg, r, mode=args.mode, parents="any")
+        if api.validate_bfs_tree(pg, r) != 0:
+            raise SystemExit(f"Graph500 certificate failed for root {r}")
+        validated += 1
+
+    peaks = measured_peaks()
+    st_mean_bytes = float(np.mean([alg_bytes(s, n) for s in stats]))
+    kernel_ms = float(np.mean(dev_ms))
+    achieved = st_mean_bytes / (kernel_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _ncu_traffic(), "peak_source": peaks["source"],
+            "kernel": "k_bfs_persistent" if not dist else "k_visit+k_finish",
+            "alg_bytes_per_launch": st_mean_bytes}
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic RMAT (Graph500 quadrants, seed 0), generated on device",
+        "config": {"workload": f"RMAT scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
+                               f"{args.roots} Graph500 roots, {world}xB200",
+                   "scale": scale, "edge_factor": args.edge_factor, "theta": theta, "mode": args.mode,
+                   "roots": args.roots, "parents": "valid parent tree written in the timed region",
+                   "l2": "flushed between steps (256 MB write); graph also > L2",
+                   "parallelism": f"{world} worker(s), one per GPU" + (" (NCCL)" if dist else "")},
+        "geomean_gteps": round(geomean, 4),
+        "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+                "d2h_bytes_per_step": int(d2h / args.steps)},
+        "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
+        "build_s": round(build_s, 3), "wall_s_timed": round(wall, 4), "validated_roots": validated,
+        "graph": {"n": n, "m": m, "d": pg.classification.d, "kind_totals": pg.kind_totals,
+                  "device_bytes": pg.device_bytes},
+        "iterations_mean": float(np.mean([s.iterations for s in stats])),
+        "inspections_mean": float(np.mean([sum(s.inspections[k][0] + s.inspections[k][1] for k in range(4))
+                                           for s in stats])),
+    }
+    if rank == 0 and not args.no_cpu_baseline and not dist:
+        line["cpu_baseline"] = cpu_baseline_same_graph(pg, roots, args, n, m)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def _allreduce_max(ctx, arr):
+    from paper_1803_03922_b200 import _lib
+    import ctypes
+    buf = np.ascontiguousarray(arr, dtype=np.float64)
+    _lib.check(_lib.load().dbfs_ctx_allreduce_max_f64(ctx.handle, buf.ctypes.data_as(_lib.vp), len(buf)))
+    return buf
+
+
+def _ncu_traffic():
+    """dram read+write bytes per launch of the BFS kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_baseline_same_graph(pg, roots, args, n, m):
+    """The oracle (C restatement of the reference run_bfs) on this host, on the
+    very graph the GPU traverses (CSR exported from the device), for a bounded
+    sample of the roots; depth digests are cross-checked against the GPU."""
+    import oracle as O
+    from paper_1803_03922_b200.engine import bfs
+    t0 = time.perf_counter()
+    og = O.from_partition(pg)
+    load_s = time.perf_counter() - t0
+    times, match, used = [], True, []
+    budget = args.cpu_budget_s
+    tstart = time.perf_counter()
+    for r in roots:
+        t = time.perf_counter()
+        res = O.run_bfs(og, r, mode=args.mode)
+        times.append(time.perf_counter() - t)
+        used.append(r)
+        lv, _ = bfs(pg, r, mode=args.mode)
+        from paper_1803_03922_b200.engine import levels_digest
+        match &= levels_digest(lv) == res["levels_digest"]
+        if time.perf_counter() - tstart > budget:
+            break
+    value = len(times) * (m / 2) / sum(times) / 1e9
+    return {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(times)} of the {len(roots)} roots, same scale-{int(math.log2(n))} graph "
+                      f"(CSR exported from the device), oracle/dbfs_oracle.c single thread",
+            "depth_parity": bool(match), "graph_load_s": round(load_s, 2)}
+
+
+# ------------------------------------------------------------- reference arm
+
+def run_reference(args, world, rank):
+    """The reference's CPU path on this host: the oracle port (oracle/, a C
+    restatement of delegate_bfs run_bfs), rank 0 only."""
+    if rank != 0:
+        return
+    import oracle as O
+    scale = args.scale + (int(round(math.log2(world))) if (world > 1 and args.scaling == "weak") else 0)
+    theta = args.theta if args.theta is not None else suggested_theta(scale)
+    t0 = time.perf_counter()
+    og = O.partition_rmat(scale, theta, 1, world, edge_factor=args.edge_factor, load_arrays=False)
+    deg = _oracle_degrees(og, O)
+    build_s = time.perf_counter() - t0
+    roots = graph500_roots(deg, args.roots)
+    for i in range(args.warmup):
+        O.run_bfs(og, roots[i % len(roots)], mode=args.mode)
+    times = []
+    for i in range(args.steps):
+        t = time.perf_counter()
+        O.run_bfs(og, roots[i % len(roots)], mode=args.mode)
+        times.append(time.perf_counter() - t)
+    m = og.m
+    value = args.steps * (m / 2) / sum(times) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic RMAT (Graph500 quadrants, seed 0), generated on the host",
+        "config": {"workload": f"RMAT scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
+                               f"{args.roots} Graph500 roots, CPU", "scale": scale, "theta": theta,
+                   "mode": args.mode, "roots": args.roots, "shape": f"1x1x{world}"},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} BFS runs over the {args.roots} roots, "
+                                   "oracle/dbfs_oracle.c (C restatement of engine.run_bfs), single thread"},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_s": round(build_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_degrees(og, O):
+    L = O.lib()
+    return O._view(L.orc_graph_degrees(og._h), og.n, np.int64)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--theta", type=int, default=None)
+    ap.add_argument("--mode", choices=["bfs", "dobfs"], default="dobfs")
+    ap.add_argument("--roots", type=int, default=64)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        ap.error("need steps >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,9 @@ typedef struct {
     int64_t reached;            /* vertices with level >= 0 */
     int64_t kernel_launches;    /* kernels launched by this call */
     int64_t wire_bytes;         /* bytes actually moved between workers */
+    int64_t h2d_bytes;          /* host->device bytes copied by this call */
+    int64_t d2h_bytes;          /* device->host bytes copied by this call */
+    int64_t rows_touched;       /* CSR rows expanded (push) or scanned (pull), all levels */
     int32_t per_iteration_truncated;
     int32_t engine_used;        /* 1 host loop, 2 persistent */
 } dbfs_run_stats;
@@ -115,12 +118,17 @@ int32_t dbfs_abi_version(void);
 int32_t dbfs_device_count(int32_t *out);
 int64_t dbfs_kernel_launch_counter(void);
 
+/* Pinned (page-locked) host buffers for zero-staging D2H of results. */
+int32_t dbfs_host_alloc(int64_t bytes, void **out);
+int32_t dbfs_host_free(void *p);
+
 /* Contexts: one device + stream; optionally an NCCL communicator (one rank per process). */
 int32_t dbfs_ctx_create(int32_t device, dbfs_ctx **out);
 int32_t dbfs_ctx_destroy(dbfs_ctx *ctx);
 int32_t dbfs_nccl_unique_id(uint8_t *out, int64_t len);       /* len >= 128 */
 int32_t dbfs_ctx_init_dist(dbfs_ctx *ctx, const uint8_t *uid, int64_t len, int32_t nranks, int32_t rank);
-int32_t dbfs_ctx_barrier(dbfs_ctx *ctx);                      /* NCCL all-reduce barrier + stream sync */
+int32_t dbfs_ctx_barrier(dbfs_ctx *ctx);
+int32_t dbfs_ctx_flush_l2(dbfs_ctx *ctx);                     /* write 256 MB on the ctx stream, sync */                      /* NCCL all-reduce barrier + stream sync */
 int32_t dbfs_ctx_allreduce_max_f64(dbfs_ctx *ctx, double *inout, int64_t count);
 int32_t dbfs_ctx_allreduce_sum_i64(dbfs_ctx *ctx, int64_t *inout, int64_t count);
 

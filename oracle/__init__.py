@@ -35,7 +35,7 @@ vp = ctypes.c_void_p
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so in place (gcc, OpenMP)."""
+    """Compile liboracle.so in place (gcc, pthreads)."""
     src = os.path.join(_HERE, "dbfs_oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
         subprocess.check_call(["make", "-s", "-C", _HERE, "liboracle.so"])
@@ -60,6 +60,9 @@ def lib():
         "orc_partition": (c_int, [vp, vp, i64, i64, i64, c_int, c_int, ctypes.POINTER(vp)]),
         "orc_partition_rmat": (c_int, [c_int, i64, c_double, c_double, c_double, u64, i64, c_int, c_int, ctypes.POINTER(vp)]),
         "orc_graph_free": (None, [vp]),
+        "orc_graph_new": (vp, [i64, i64, i64, c_int, c_int, i64, vp]),
+        "orc_graph_set_csr": (c_int, [vp, c_int, c_int, i64, vp, vp]),
+        "orc_graph_finalize": (c_int, [vp]),
         "orc_graph_n": (i64, [vp]), "orc_graph_m": (i64, [vp]), "orc_graph_d": (i64, [vp]),
         "orc_graph_p": (c_int, [vp]), "orc_graph_kind_total": (i64, [vp, c_int]),
         "orc_graph_degrees": (vp, [vp]), "orc_graph_delegates": (vp, [vp]),
@@ -148,7 +151,7 @@ class OracleWorker:
 class OracleGraph:
     """Partitioned graph with the reference PartitionedGraph's fields."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, load_arrays=True):
         self._h = handle
         L = lib()
         self.n = L.orc_graph_n(handle)
@@ -156,9 +159,11 @@ class OracleGraph:
         self.d = L.orc_graph_d(handle)
         self.p = L.orc_graph_p(handle)
         self.kind_totals = {k: L.orc_graph_kind_total(handle, i) for i, k in enumerate(KINDS)}
+        self.workers = []
+        if not load_arrays:
+            return
         self.degrees = _view(L.orc_graph_degrees(handle), self.n, np.int64)
         self.delegate_global_ids = _view(L.orc_graph_delegates(handle), self.d, np.int64)
-        self.workers = []
         for w in range(self.p):
             W = OracleWorker()
             W.index = w
@@ -191,11 +196,28 @@ def partition(src, dst, n, theta, p_rank=1, p_gpu=1) -> OracleGraph:
 
 
 def partition_rmat(scale, theta, p_rank=1, p_gpu=1, edge_factor=16, a=0.57, b=0.19, c=0.19,
-                   seed=0) -> OracleGraph:
+                   seed=0, load_arrays=True) -> OracleGraph:
     h = vp()
     _check(lib().orc_partition_rmat(scale, edge_factor, a, b, c, seed & (2**64 - 1), theta,
                                     p_rank, p_gpu, ctypes.byref(h)), "partition_rmat")
-    return OracleGraph(h)
+    return OracleGraph(h, load_arrays=load_arrays)
+
+
+def from_partition(pg) -> OracleGraph:
+    """Oracle graph over an existing partition object exposing the reference
+    PartitionedGraph fields (e.g. the GPU one, exported to host)."""
+    L = lib()
+    dg = np.ascontiguousarray(pg.classification.delegate_global_ids, dtype=np.int64)
+    h = L.orc_graph_new(pg.n, pg.m, int(pg.classification.theta), pg.shape.p_rank, pg.shape.p_gpu,
+                        int(pg.classification.d), _ptr(dg))
+    for w in pg.workers:
+        for ki, k in enumerate(KINDS):
+            csr = w.subgraph(k)
+            off = np.ascontiguousarray(csr.row_offsets, dtype=np.int64)
+            cols = np.ascontiguousarray(csr.col_indices, dtype=np.int64 if k == "nn" else np.uint32)
+            _check(L.orc_graph_set_csr(h, w.index, ki, len(off) - 1, _ptr(off), _ptr(cols)), "set_csr")
+    L.orc_graph_finalize(h)
+    return OracleGraph(vp(h), load_arrays=False)
 
 
 # ----------------------------------------------------------------------- BFS

@@ -30,9 +30,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
-#ifdef _OPENMP
-#include <omp.h>
-#endif
+#include <pthread.h>
+#include <unistd.h>
 
 #define ORC_OK 0
 #define ORC_EINVAL 1
@@ -130,6 +129,34 @@ static inline void rmat_edge(const rmat_gen *g, uint64_t e, uint64_t *u, uint64_
 /* Edges [begin, end) of the (optionally symmetrized) RMAT edge list built by
  * build_rmat_graph (rmat.py:200-208): index e < m0 is original edge e, index
  * e >= m0 is the reverse of original edge e - m0 (rmat.py:185-189). */
+typedef struct {
+    const rmat_gen *g;
+    int64_t begin, lo, hi;
+    int64_t *src, *dst;
+} gen_job;
+
+static void *gen_worker(void *arg) {
+    gen_job *j = (gen_job *)arg;
+    const rmat_gen *g = j->g;
+    for (int64_t i = j->lo; i < j->hi; i++) {
+        uint64_t u, v;
+        int64_t e = i >= g->m0 ? i - g->m0 : i;
+        rmat_edge(g, (uint64_t)e, &u, &v);
+        if (i >= g->m0) { uint64_t t = u; u = v; v = t; }
+        j->src[i - j->begin] = (int64_t)u;
+        j->dst[i - j->begin] = (int64_t)v;
+    }
+    return NULL;
+}
+
+static int orc_threads(void) {
+    const char *e = getenv("ORC_THREADS");
+    long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    if (t < 1) t = 1;
+    if (t > 256) t = 256;
+    return (int)t;
+}
+
 int orc_rmat_edges(int scale, int64_t edge_factor, double a, double b, double c,
                    uint64_t seed, int randomize, int symmetrize, int64_t begin,
                    int64_t end, int64_t *src, int64_t *dst) {
@@ -138,15 +165,19 @@ int orc_rmat_edges(int scale, int64_t edge_factor, double a, double b, double c,
     rmat_gen_init(&g, scale, edge_factor, a, b, c, seed, randomize);
     int64_t m = symmetrize ? 2 * g.m0 : g.m0;
     if (begin < 0 || end > m || begin > end) return ORC_ERANGE;
-
-    for (int64_t i = begin; i < end; i++) {
-        uint64_t u, v;
-        int64_t e = i >= g.m0 ? i - g.m0 : i;
-        rmat_edge(&g, (uint64_t)e, &u, &v);
-        if (i >= g.m0) { uint64_t t = u; u = v; v = t; }
-        src[i - begin] = (int64_t)u;
-        dst[i - begin] = (int64_t)v;
+    int T = orc_threads();
+    if (end - begin < (1 << 16)) T = 1;
+    pthread_t th[256];
+    gen_job jobs[256];
+    int64_t per = (end - begin + T - 1) / T;
+    for (int t = 0; t < T; t++) {
+        jobs[t].g = &g; jobs[t].begin = begin; jobs[t].src = src; jobs[t].dst = dst;
+        jobs[t].lo = begin + per * t < end ? begin + per * t : end;
+        jobs[t].hi = jobs[t].lo + per < end ? jobs[t].lo + per : end;
+        if (T > 1) pthread_create(&th[t], NULL, gen_worker, &jobs[t]);
+        else gen_worker(&jobs[t]);
     }
+    if (T > 1) for (int t = 0; t < T; t++) pthread_join(th[t], NULL);
     return ORC_OK;
 }
 
@@ -355,6 +386,60 @@ int orc_partition_rmat(int scale, int64_t edge_factor, double a, double b, doubl
     free(src);
     free(dst);
     return rc;
+}
+
+/* Construct an oracle graph from an externally built partition (e.g. the CSR
+ * exported from the device): used to time the CPU restatement on exactly the
+ * graph the GPU traverses.  Arrays are copied.  cols are int64 for nn and
+ * uint32 otherwise, as in the reference (storage.py:19-31). */
+orc_graph *orc_graph_new(int64_t n, int64_t m, int64_t theta, int p_rank, int p_gpu, int64_t d,
+                         const int64_t *del_gid) {
+    orc_graph *g = calloc(1, sizeof(orc_graph));
+    g->n = n; g->m = m; g->theta = theta; g->d = d;
+    g->p_rank = p_rank; g->p_gpu = p_gpu; g->p = p_rank * p_gpu;
+    g->degree = calloc(n > 0 ? n : 1, sizeof(int64_t));
+    g->del_gid = malloc((d > 0 ? d : 1) * sizeof(int64_t));
+    g->del_id = malloc((n > 0 ? n : 1) * sizeof(int64_t));
+    memcpy(g->del_gid, del_gid, d * sizeof(int64_t));
+    for (int64_t v = 0; v < n; v++) g->del_id[v] = -1;
+    for (int64_t x = 0; x < d; x++) g->del_id[del_gid[x]] = x;
+    g->w = calloc(g->p, sizeof(orc_worker));
+    for (int w = 0; w < g->p; w++) g->w[w].n_local = n_local_of(n, g->p, w);
+    return g;
+}
+
+int orc_graph_set_csr(orc_graph *g, int w, int k, int64_t rows, const int64_t *off, const void *cols) {
+    if (w < 0 || w >= g->p || k < 0 || k > 3) return ORC_EINVAL;
+    orc_csr *c = &g->w[w].csr[k];
+    c->rows = rows;
+    c->nnz = off[rows];
+    c->off = malloc((rows + 1) * sizeof(int64_t));
+    memcpy(c->off, off, (rows + 1) * sizeof(int64_t));
+    size_t wdt = k == NN ? 8 : 4;
+    c->cols = malloc((c->nnz > 0 ? c->nnz : 1) * wdt);
+    memcpy(c->cols, cols, c->nnz * wdt);
+    g->kind_total[k] += c->nnz;
+    return ORC_OK;
+}
+
+int orc_graph_finalize(orc_graph *g) {
+    for (int w = 0; w < g->p; w++) {
+        orc_worker *W = &g->w[w];
+        orc_csr *nd = &W->csr[ND];
+        int64_t cnt = 0;
+        for (int64_t r = 0; r < nd->rows; r++) cnt += nd->off[r + 1] > nd->off[r];
+        W->n_nd_src = cnt;
+        W->nd_src = malloc((cnt > 0 ? cnt : 1) * sizeof(int64_t));
+        cnt = 0;
+        for (int64_t r = 0; r < nd->rows; r++) if (nd->off[r + 1] > nd->off[r]) W->nd_src[cnt++] = r;
+        W->dn_mask = malloc(g->d > 0 ? g->d : 1);
+        W->dd_mask = malloc(g->d > 0 ? g->d : 1);
+        for (int64_t r = 0; r < g->d; r++) {
+            W->dn_mask[r] = W->csr[DN].off[r + 1] > W->csr[DN].off[r];
+            W->dd_mask[r] = W->csr[DD].off[r + 1] > W->csr[DD].off[r];
+        }
+    }
+    return ORC_OK;
 }
 
 int64_t orc_graph_n(const orc_graph *g) { return g->n; }

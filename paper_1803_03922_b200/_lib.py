@@ -56,6 +56,7 @@ class BfsOptionsC(ctypes.Structure):
 class RunStatsC(ctypes.Structure):
     _fields_ = [("iterations", i64), ("inspections", (i64 * 2) * 4), ("b_measured", dbl),
                 ("device_ms", dbl), ("reached", i64), ("kernel_launches", i64), ("wire_bytes", i64),
+                ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64),
                 ("per_iteration_truncated", i32), ("engine_used", i32)]
 
 
@@ -72,6 +73,9 @@ SIGNATURES = {
     "dbfs_abi_version": (i32, []),
     "dbfs_device_count": (i32, [P(i32)]),
     "dbfs_kernel_launch_counter": (i64, []),
+    "dbfs_host_alloc": (i32, [i64, P(vp)]),
+    "dbfs_host_free": (i32, [vp]),
+    "dbfs_ctx_flush_l2": (i32, [vp]),
     "dbfs_ctx_create": (i32, [i32, P(vp)]),
     "dbfs_ctx_destroy": (i32, [vp]),
     "dbfs_nccl_unique_id": (i32, [vp, i64]),
@@ -174,6 +178,9 @@ class Context:
     def barrier(self):
         check(load().dbfs_ctx_barrier(self._h))
 
+    def flush_l2(self):
+        check(load().dbfs_ctx_flush_l2(self._h))
+
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.dbfs_ctx_destroy(self._h)
@@ -211,3 +218,30 @@ def nccl_unique_id() -> bytes:
 
 def kernel_launches() -> int:
     return int(load().dbfs_kernel_launch_counter())
+
+
+class PinnedArray:
+    """A numpy array over page-locked host memory (cudaHostAlloc) for fast D2H."""
+
+    def __init__(self, count, dtype):
+        import numpy as np
+        self.dtype = np.dtype(dtype)
+        nbytes = max(int(count) * self.dtype.itemsize, 1)
+        p = vp()
+        check(load().dbfs_host_alloc(nbytes, ctypes.byref(p)), "host_alloc")
+        self._p = p
+        buf = (ctypes.c_char * nbytes).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(count))
+
+    def __del__(self):
+        try:
+            if self._p and _lib is not None:
+                _lib.dbfs_host_free(self._p)
+                self._p = None
+        except Exception:
+            pass
+
+
+def pinned_empty(count, dtype):
+    """Page-locked numpy array; keep the returned holder alive while using .array."""
+    return PinnedArray(count, dtype)

@@ -63,6 +63,29 @@ int32_t dbfs_device_count(int32_t *out) {
     });
 }
 
+int32_t dbfs_host_alloc(int64_t bytes, void **out) {
+    return guard([&] {
+        *out = nullptr;
+        DBFS_CUDA(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+    });
+}
+
+int32_t dbfs_host_free(void *p) {
+    return guard([&] {
+        if (p) DBFS_CUDA(cudaFreeHost(p));
+    });
+}
+
+int32_t dbfs_ctx_flush_l2(dbfs_ctx *ctx) {
+    return guard([&] {
+        DBFS_CUDA(cudaSetDevice(ctx->c.device));
+        const size_t B = (size_t)256 << 20;
+        if (ctx->c.flush.n < (int64_t)B) ctx->c.flush.alloc((int64_t)B);
+        DBFS_CUDA(cudaMemsetAsync(ctx->c.flush.p, ctx->c.flush_val++ & 0xff, B, ctx->c.stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
 int32_t dbfs_ctx_create(int32_t device, dbfs_ctx **out) {
     return guard([&] {
         *out = nullptr;
@@ -89,6 +112,7 @@ int32_t dbfs_ctx_destroy(dbfs_ctx *ctx) {
         cudaSetDevice(ctx->c.device);
         nccl_destroy(ctx->c);
         ctx->c.scratch.release();
+        ctx->c.flush.release();
         if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
         if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
         if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
@@ -279,6 +303,7 @@ int32_t dbfs_bfs(dbfs_graph *gg, const dbfs_bfs_options *opts, int32_t *levels_o
         DBFS_CUDA(cudaSetDevice(g.ctx->device));
         run_bfs(g, *opts, stats);
         if (levels_out || parents_out) fetch_result(g, levels_out, parents_out);
+        if (stats) stats->d2h_bytes += (levels_out ? 4 * g.n : 0) + (parents_out ? 8 * g.n : 0);
         if (stats && levels_out) {
             int64_t r = 0;
             for (int64_t i = 0; i < g.n; i++) r += levels_out[i] >= 0;

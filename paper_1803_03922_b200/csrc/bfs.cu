@@ -399,12 +399,12 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     int iterations = 0;
     bool timeout = false;
 
+    GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
+    if (engine == 2) DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
     DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
     if (engine == 2) {
         int bps = 0;
         int grid = persistent_grid(g, &bps);
-        GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
-        DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
         const View *vp = g.views.p;
         int64_t src = o.source;
         int rec_cap = g.rec_cap;
@@ -539,6 +539,13 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
                 if (r.new_del && g.p > 1) wire += (int64_t)(g.p - 1) * nwords(g.d) * 4 / W;
             }
         st->wire_bytes = wire;
+        int64_t rows = 0;
+        for (int L = 0; L < nrec; L++)
+            for (int i = 0; i < W; i++) rows += (int64_t)g.last_rec[(size_t)L * W + i].rows;
+        st->rows_touched = rows;
+        // library-side copies of this call: views + options up, control block / records down
+        st->h2d_bytes = (int64_t)(sizeof(View) * W);
+        st->d2h_bytes = 4 + (int64_t)sizeof(Ctl) + (int64_t)(sizeof(IterRec) * nrec * W);
         int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
         st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
     }

@@ -146,6 +146,9 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         r.insp[k] = r.dir[k] == FWD ? S.fv[k] : S.insp_bwd[k];
     }
     r.records = S.records;
+    r.rows = S.pull_rows;
+    for (int k = 0; k < 4; k++)
+        if (k == KIND_NN || r.dir[k] == FWD) r.rows += S.q[k];
     r.dirty = S.dirty;
     r.new_del = S.new_del;
     unsigned long long msgs = 0;
@@ -181,6 +184,7 @@ struct VisitCounters {
     unsigned long long local_claims, records;
     unsigned long long insp_bwd[4];
     unsigned long long dirty;
+    unsigned long long pull_rows;
 };
 
 struct FinishCounters {
@@ -357,6 +361,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             int64_t wi = base + lane;
             uint32_t word = wi < V.nw_n ? (srcb[wi] & ~(V.nvis[wi] | nfront_cur[wi])) : 0u;
             unsigned cnt = warp_compact(word, wi, list);
+            if (lane == 0) vc.pull_rows += cnt;
             for (unsigned i = lane; i < cnt; i += 32) {
                 uint32_t c = list[i];
                 int64_t b = __ldg(&off_nd[c]), e = __ldg(&off_nd[c + 1]);
@@ -385,6 +390,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             int64_t wi = base + lane;
             uint32_t word = wi < V.nw_d ? (srcb[wi] & ~V.dvis[wi]) : 0u;
             unsigned cnt = warp_compact(word, wi, list);
+            if (lane == 0) vc.pull_rows += cnt;
             for (unsigned i = lane; i < cnt; i += 32) {
                 uint32_t x = list[i];
                 int64_t b = __ldg(&off_dn[x]), e = __ldg(&off_dn[x + 1]);
@@ -412,6 +418,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             int64_t wi = base + lane;
             uint32_t word = wi < V.nw_d ? (srcb[wi] & ~V.dvis[wi]) : 0u;
             unsigned cnt = warp_compact(word, wi, list);
+            if (lane == 0) vc.pull_rows += cnt;
             for (unsigned i = lane; i < cnt; i += 32) {
                 uint32_t x = list[i];
                 int64_t b = __ldg(&off_dd[x]), e = __ldg(&off_dd[x + 1]);
@@ -454,6 +461,8 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     }
     v = warp_sum(vc.dirty);
     if (lane == 0 && v) atomicOr(&A.dirty, 1ull);
+    v = warp_sum(vc.pull_rows);
+    if (lane == 0) atomic_add_u64(&A.pull_rows, v);
 }
 
 // -------------------------------------------------------------- phase F(L)

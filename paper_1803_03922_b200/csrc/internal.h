@@ -32,6 +32,7 @@ struct LevelSlot {
     unsigned long long dirty;        // this worker found >= 1 new delegate (comm.py:33-36)
     unsigned long long new_del;      // delegates discovered at the barrier
     unsigned long long inbox;        // records delivered to this worker
+    unsigned long long pull_rows;    // reverse rows scanned by pulls at this level
     unsigned long long send[MAXW];   // records per destination worker
 };
 
@@ -56,6 +57,7 @@ struct IterRec {
     unsigned long long dirty;
     unsigned long long messages;
     unsigned long long new_del;
+    unsigned long long rows;         // rows expanded (push) + scanned (pull)
     unsigned long long send[MAXW];
 };
 
@@ -142,6 +144,8 @@ struct Ctx {
     int nranks = 1, rank = 0;
     void *comm = nullptr;            // ncclComm_t
     DArray<unsigned char> scratch;   // reusable device scratch
+    DArray<unsigned char> flush;     // L2 flush buffer (bench hygiene)
+    int flush_val = 1;
     void *ensure_scratch(size_t bytes);
 };
 

@@ -223,16 +223,29 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     }
 
 
-def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobfs"):
+def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobfs", out=None,
+        stats: bool = False):
     """Graph500-style BFS: (depth int32[n], parent int64[n]).  ``parents="min"``
-    gives the deterministic min-ID tree."""
+    gives the deterministic min-ID tree.  ``out=(levels, parents)``
+    writes into caller buffers (e.g. pinned, see ``_lib.pinned_empty``);
+    ``stats=True`` also returns the C run-stats struct."""
+    if not (0 <= root < pg.n):
+        raise ValueError(f"source {root} out of range [0, {pg.n})")
     opts = BfsOptions(mode=mode, source=int(root), parents="any")
-    levels = np.empty(pg.n, dtype=np.int32)
-    par = np.empty(pg.n, dtype=np.int64)
-    _bfs_raw(pg, opts, levels, par)
+    if out is None:
+        levels = np.empty(pg.n, dtype=np.int32)
+        par = np.empty(pg.n, dtype=np.int64)
+    else:
+        levels, par = out
+    st = _bfs_raw(pg, opts, levels, par)
     if parents == "min":
         par = min_parents(pg)
-    return levels, par
+    return (levels, par, st) if stats else (levels, par)
+
+
+def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any"):
+    """One BFS leaving depth/parents in device memory (for timing); returns run stats."""
+    return _bfs_raw(pg, BfsOptions(mode=mode, source=int(root), parents=parents), None, None)
 
 
 def min_parents(pg: PartitionedGraph) -> np.ndarray:
