@@ -98,6 +98,7 @@ typedef struct {
     int64_t h2d_bytes;          /* host->device bytes copied by this call */
     int64_t d2h_bytes;          /* device->host bytes copied by this call */
     int64_t rows_touched;       /* CSR rows expanded (push) or scanned (pull), all levels */
+    double init_us;             /* device time of state init + seeding */
     int32_t per_iteration_truncated;
     int32_t engine_used;        /* 1 host loop, 2 persistent */
 } dbfs_run_stats;
@@ -111,6 +112,10 @@ typedef struct {
     int64_t normal_bytes;
     int64_t message_count;
     int64_t pair_count;
+    int64_t frontier_normals;   /* normals at this level (all workers) */
+    int64_t frontier_delegates; /* delegates at this level */
+    double visit_us;            /* device time of the visit phase (worker 0's clock) */
+    double finish_us;           /* device time of the barrier/apply phase */
 } dbfs_iteration;
 
 const char *dbfs_last_error(void);

@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbfs.so")
+LIB_PATH = os.environ.get("DBFS_LIB", os.path.join(_HERE, "libdbfs.so"))
 
 i32, i64, u64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 vp = ctypes.c_void_p
@@ -56,13 +56,14 @@ class BfsOptionsC(ctypes.Structure):
 class RunStatsC(ctypes.Structure):
     _fields_ = [("iterations", i64), ("inspections", (i64 * 2) * 4), ("b_measured", dbl),
                 ("device_ms", dbl), ("reached", i64), ("kernel_launches", i64), ("wire_bytes", i64),
-                ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64),
+                ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64), ("init_us", dbl),
                 ("per_iteration_truncated", i32), ("engine_used", i32)]
 
 
 class IterationC(ctypes.Structure):
     _fields_ = [("iteration", i64), ("inspections", i64 * 4), ("fv", i64 * 4), ("mask_bytes", dbl),
-                ("normal_bytes", i64), ("message_count", i64), ("pair_count", i64)]
+                ("normal_bytes", i64), ("message_count", i64), ("pair_count", i64),
+                ("frontier_normals", i64), ("frontier_delegates", i64), ("visit_us", dbl), ("finish_us", dbl)]
 
 
 P = ctypes.POINTER

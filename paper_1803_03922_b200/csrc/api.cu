@@ -340,6 +340,12 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
                 r.fv[k] += (int64_t)x.fv[k];
             }
             any_new |= x.new_del > 0;
+            r.frontier_normals += (int64_t)x.nfront;
+            if (i == 0) {
+                r.frontier_delegates = (int64_t)x.dfront;
+                if (x.t[1] > x.t[0]) r.visit_us = (double)(x.t[1] - x.t[0]) / 1e3;
+                if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;
+            }
             records += (int64_t)x.records;
             msgs += (int64_t)x.messages;
             int w = g.workers[i].w;

@@ -12,6 +12,10 @@
 
 #include "bfs_device.cuh"
 
+#ifndef DBFS_MINB
+#define DBFS_MINB 3
+#endif
+
 namespace dbfs {
 
 // ------------------------------------------------------------- grid barrier
@@ -93,17 +97,20 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
 
 // ----------------------------------------------------------------- kernels
 
-__global__ void __launch_bounds__(BT) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
+__global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
                                                        uint32_t src_del, GridBar *bar, int rec_cap,
                                                        AsmArgs asm_args, int do_assemble) {
     __shared__ Smem sm;
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
     const View &V = views[wsel];
     const unsigned nblocks = gridDim.x;
+    const bool timer = wb == 0 && threadIdx.x == 0;
+    if (timer) V.ctl->t_start = globaltimer_ns();
     phase_init(V, wb, nb);
     if (!grid_sync(bar, nblocks)) return;
     if (wb == 0 && threadIdx.x == 0) seed_worker(V, source, src_del);
     if (!grid_sync(bar, nblocks)) return;
+    if (timer) V.ctl->t_seeded = globaltimer_ns();
     int L = 0;
     for (;; L++) {
         if (L > 0) {
@@ -111,10 +118,13 @@ __global__ void __launch_bounds__(BT) k_bfs_persistent(const View *__restrict__ 
             if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
             if (!cont) break;
         }
+        if (timer && L < rec_cap) V.rec[L].t[0] = globaltimer_ns();
         phase_visit(V, L, wb, nb, sm);
         if (!grid_sync(bar, nblocks)) return;
-        phase_finish(V, L, wb, nb);
+        if (timer && L < rec_cap) V.rec[L].t[1] = globaltimer_ns();
+        phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
         if (!grid_sync(bar, nblocks)) return;
+        if (timer && L < rec_cap) V.rec[L].t[2] = globaltimer_ns();
     }
     if (wb == 0 && threadIdx.x == 0) V.ctl->last_level = L;
     if (do_assemble) phase_assemble(asm_args, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
@@ -128,13 +138,14 @@ __global__ void k_seed(const View *__restrict__ views, int W, int64_t source, ui
     if (threadIdx.x == 0 && (int)blockIdx.x < W) seed_worker(views[blockIdx.x], source, src_del);
 }
 
-__global__ void __launch_bounds__(BT) k_visit(const View *__restrict__ views, int W, int L) {
+__global__ void __launch_bounds__(BT, DBFS_MINB) k_visit(const View *__restrict__ views, int W, int L) {
     __shared__ Smem sm;
     phase_visit(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W, sm);
 }
 
-__global__ void __launch_bounds__(BT) k_finish(const View *__restrict__ views, int W, int L) {
-    phase_finish(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W);
+__global__ void __launch_bounds__(BT) k_finish(const View *__restrict__ views, int W, int L, int parts) {
+    __shared__ Smem sm;
+    phase_finish(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W, sm, parts);
 }
 
 __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
@@ -143,8 +154,6 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 
 // --------------------------------------------------------------- resources
 
-static constexpr int HUB = 256;
-static constexpr int CHUNK = 256;
 
 Graph::~Graph() {}
 
@@ -190,10 +199,11 @@ static void ensure_resources(Graph &g) {
         Wk.dfront.alloc(std::max<int64_t>(nw_d, 1));
         Wk.dnext0.alloc(std::max<int64_t>(nw_d, 1));
         Wk.dnext1.alloc(std::max<int64_t>(nw_d, 1));
-        Wk.chunk_cap = (Wk.nnz[KIND_DN] + Wk.nnz[KIND_DD]) / CHUNK + (Wk.nnz[KIND_DN] + Wk.nnz[KIND_DD]) / HUB + 8;
-        Wk.chunks0.alloc(Wk.chunk_cap);
-        Wk.chunks1.alloc(Wk.chunk_cap);
-        Wk.inbox_cap = std::max<int64_t>(inbox_cap[Wk.w], 1);
+        for (int j = 0; j < 4; j++) {
+            Wk.dlist[j].alloc(std::max<int64_t>(g.d, 1));
+            Wk.dpre[j].alloc(g.d + 1);
+        }
+        Wk.inbox_cap = g.dist ? std::max<int64_t>(inbox_cap[Wk.w], 1) : 1;
         Wk.inbox0.alloc(Wk.inbox_cap);
         Wk.inbox1.alloc(Wk.inbox_cap);
         if (g.dist) {
@@ -227,8 +237,6 @@ static void ensure_resources(Graph &g) {
         V.cand_all = !g.dist;
         V.P_sources = g.dist ? g.p : W;
         V.rec_cap = g.rec_cap;
-        V.hub = HUB;
-        V.chunk = CHUNK;
         V.pd.init((uint32_t)g.p);
         V.n = g.n;
         V.n_local = Wk.n_local;
@@ -254,9 +262,11 @@ static void ensure_resources(Graph &g) {
         V.dfront = Wk.dfront.p;
         V.dnext[0] = Wk.dnext0.p;
         V.dnext[1] = Wk.dnext1.p;
-        V.chunks[0] = Wk.chunks0.p;
-        V.chunks[1] = Wk.chunks1.p;
-        V.chunk_cap = Wk.chunk_cap;
+        for (int kk = 0; kk < 2; kk++)
+            for (int par = 0; par < 2; par++) {
+                V.dlist[kk][par] = Wk.dlist[kk * 2 + par].p;
+                V.dpre[kk][par] = Wk.dpre[kk * 2 + par].p;
+            }
         V.inbox[0] = Wk.inbox0.p;
         V.inbox[1] = Wk.inbox1.p;
         V.inbox_cap = Wk.inbox_cap;
@@ -273,8 +283,11 @@ static void ensure_resources(Graph &g) {
             for (int j = 0; j < W; j++) {
                 WorkerHost &Wj = g.workers[j];
                 V.ctl_all[j] = Wj.ctl.p;
-                V.inbox_all[0][j] = Wj.inbox0.p;
-                V.inbox_all[1][j] = Wj.inbox1.p;
+                V.nvis_all[j] = Wj.nvis.p;
+                V.nfront_all[0][j] = Wj.nfront0.p;
+                V.nfront_all[1][j] = Wj.nfront1.p;
+                V.nlevel_all[j] = Wj.nlevel.p;
+                V.nparent_all[j] = Wj.nparent.p;
                 V.mask_src[0][j] = Wj.dnext0.p;
                 V.mask_src[1][j] = Wj.dnext1.p;
                 V.cand_src[j] = Wj.dcand.p;
@@ -434,22 +447,29 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
             k_visit<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L);
             DBFS_LAUNCHED();
             if (g.dist) dist_exchange(g, L, sc);
-            k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L);
-            DBFS_LAUNCHED();
+            if (g.dist) {
+                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_INGEST);
+                DBFS_LAUNCHED();
+                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_NORMALS);
+                DBFS_LAUNCHED();
+            } else {
+                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_NORMALS);
+                DBFS_LAUNCHED();
+            }
             for (int i = 0; i < W; i++)
                 DBFS_CUDA(cudaMemcpyAsync(&hc[i], g.workers[i].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
             DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
             // per-iteration record for level L (host copy of the device rule)
             if (L < g.rec_cap) {
                 for (int i = 0; i < W; i++) {
-                    IterRec r;
+                    IterRec r{};
                     make_record(g.views_h[i], hc[i], L, r);
                     DBFS_CUDA(cudaMemcpyAsync(g.workers[i].rec.p + L, &r, sizeof(r), cudaMemcpyHostToDevice,
                                               ctx.stream));
                 }
             }
             unsigned long long act = hc[0].s[L % 3].new_del;
-            for (int i = 0; i < W; i++) act += hc[i].s[L % 3].local_claims + hc[i].s[L % 3].records;
+            for (int i = 0; i < W; i++) act += hc[i].s[(L + 1) % 3].nfront + hc[i].s[L % 3].records;
             if (g.dist) {
                 int64_t *buf = (int64_t *)g.dist_scratch.p;
                 int64_t v = (int64_t)act;
@@ -545,6 +565,11 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         st->rows_touched = rows;
         // library-side copies of this call: views + options up, control block / records down
         st->h2d_bytes = (int64_t)(sizeof(View) * W);
+        if (engine == 2) {
+            Ctl c0;
+            DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+            st->init_us = (double)(c0.t_seeded - c0.t_start) / 1e3;
+        }
         st->d2h_bytes = 4 + (int64_t)sizeof(Ctl) + (int64_t)(sizeof(IterRec) * nrec * W);
         int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
         st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;

@@ -15,8 +15,13 @@
 //
 // Pre-state rule: every test made during V(L) must see the state at the start
 // of level L (the reference applies updates only after its barrier).  Hence
-//   visited(<= L) normal  = nvis | nfront[L&1]   (claims go to nfront[(L+1)&1])
-//   visited(<= L) delegate= dvis                 (finds go to dnext[L&1])
+//   visited(<= L) normal   = nvis   (claims go to nfront[(L+1)&1], folded in F)
+//   frontier L normal      = nfront[L&1]
+//   visited(<= L) delegate = dvis   (finds go to dnext[L&1], folded in F)
+// Discoveries are fire-and-forget (RED.OR on the next bitmap + plain stores of
+// level / parent; any concurrent writer's parent is a valid one), so no lane
+// ever waits on an atomic's return value in the traversal loops.  Frontier
+// statistics for the direction rule are counted from the bitmaps in F.
 #pragma once
 #include "internal.h"
 
@@ -146,6 +151,8 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         r.insp[k] = r.dir[k] == FWD ? S.fv[k] : S.insp_bwd[k];
     }
     r.records = S.records;
+    r.nfront = S.nfront;
+    r.dfront = S.dfront;
     r.rows = S.pull_rows;
     for (int k = 0; k < 4; k++)
         if (k == KIND_NN || r.dir[k] == FWD) r.rows += S.q[k];
@@ -160,6 +167,16 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
 }
 
 // ------------------------------------------------------------------ helpers
+
+#ifndef DBFS_UNR
+#define DBFS_UNR 4
+#endif
+constexpr int UNR = DBFS_UNR;    // independent column loads in flight per lane (push)
+constexpr int PULL_LANE = 16;    // columns a lane loads at once in a pull scan
+constexpr int PULL_LANE_MAX = 32;  // entries a lane scans alone before the row goes warp-wide
+constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
+constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned long long M38 = (1ull << 38) - 1;
 
 __device__ __forceinline__ bool tbit(const uint32_t *b, uint32_t i) { return (b[i >> 5] >> (i & 31)) & 1u; }
 
@@ -178,39 +195,54 @@ __device__ __forceinline__ unsigned warp_compact(uint32_t word, int64_t wi, uint
     return tot;
 }
 
+__device__ __forceinline__ unsigned long long warp_excl_scan64(unsigned long long v, unsigned long long *tot) {
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= (unsigned)o) x += y;
+    }
+    *tot = __shfl_sync(FULL, x, 31);
+    return x - v;
+}
+
+// Largest lane l with key_l <= x, for keys non-decreasing over lanes and
+// key_0 <= x (5 shuffle steps; all lanes must participate).
+template <typename T>
+__device__ __forceinline__ int owner_search(T key, T x) {
+    int lo = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        int cand = lo + s;
+        T v = __shfl_sync(FULL, key, cand & 31);
+        if (cand < 32 && v <= x) lo = cand;
+    }
+    return lo;
+}
+
 struct VisitCounters {
     unsigned long long fv_nn;       // FV_nn of this level's frontier (activity slot)
-    unsigned long long nfv_nd, nq_nd, ncount;  // next frontier (normals)
-    unsigned long long local_claims, records;
+    unsigned long long records;     // remote normal records (comm accounting)
     unsigned long long insp_bwd[4];
     unsigned long long dirty;
     unsigned long long pull_rows;
 };
 
-struct FinishCounters {
-    unsigned long long nfv_nd, nq_nd, ncount;
-    unsigned long long dfv_dn, dq_dn, dfv_dd, dq_dd, dcount, new_del;
-};
-
-// Claim local normal c for level L+1 (pre-state unvisited already checked or
-// checked here).  The atomicOr winner is the unique discoverer.
-__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool check,
-                                             VisitCounters &vc) {
+// Claim normal c of worker `wv` (this worker, or an in-process peer) for
+// level L+1: pre-state check on visited(<= L), then fire-and-forget.
+__device__ __forceinline__ void claim_on(uint32_t *__restrict__ nvis, uint32_t *__restrict__ nx,
+                                         int32_t *__restrict__ nlevel, int64_t *__restrict__ nparent, int parents,
+                                         int L, uint32_t c, int64_t parent, bool check) {
     const uint32_t wd = c >> 5, bit = 1u << (c & 31);
-    if (check) {
-        if ((V.nvis[wd] | V.nfront[L & 1][wd]) & bit) return;
-    }
-    uint32_t *nx = V.nfront[(L + 1) & 1];
-    if (nx[wd] & bit) return;
-    uint32_t old = atomicOr(&nx[wd], bit);
-    if (old & bit) return;
-    V.nlevel[c] = L + 1;
-    if (V.parents) V.nparent[c] = parent;
-    int64_t dnd = V.off[KIND_ND][c + 1] - V.off[KIND_ND][c];
-    vc.local_claims++;
-    vc.ncount++;
-    vc.nfv_nd += dnd;
-    vc.nq_nd += dnd > 0;
+    if (check && (nvis[wd] & bit)) return;
+    if (nx[wd] & bit) return;  // already claimed this level (possibly stale: then harmless)
+    atomicOr(&nx[wd], bit);    // result unused -> RED.OR
+    nlevel[c] = L + 1;
+    if (parents) nparent[c] = parent;
+}
+
+__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool check) {
+    claim_on(V.nvis, V.nfront[(L + 1) & 1], V.nlevel, V.nparent, V.parents, L, c, parent, check);
 }
 
 // Mark delegate x found at level L by this worker (delegate mask, comm.py:33-36).
@@ -218,24 +250,318 @@ __device__ __forceinline__ void find_delegate(const View &V, int L, uint32_t x, 
                                               unsigned long long &dirty) {
     const uint32_t wd = x >> 5, bit = 1u << (x & 31);
     uint32_t *dn = V.dnext[L & 1];
-    if (dn[wd] & bit) return;
-    uint32_t old = atomicOr(&dn[wd], bit);
-    if (old & bit) return;
-    if (V.parents) V.dcand[x] = parent;
     dirty = 1;
+    if (dn[wd] & bit) return;
+    atomicOr(&dn[wd], bit);
+    if (V.parents) V.dcand[x] = parent;
 }
 
-__device__ __forceinline__ void send_record(const View &V, int L, uint32_t owner, uint32_t local, int64_t parent,
-                                            VisitCounters &vc) {
+// Remote nn records of one warp step (engine.py:207-222 -> comm.py:138-197):
+// lanes with `need` send (owner o, local c, parent).  In-process peers are
+// claimed directly in their device arrays; distributed peers get an 8-byte
+// record in the per-destination send bin.  One atomic per destination per warp.
+__device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint32_t o, uint32_t c, uint32_t parent,
+                                          VisitCounters &vc) {
+    unsigned m = __ballot_sync(FULL, need);
+    if (!m) return;
+    unsigned key = need ? o : 0xffffffffu;
+    unsigned peers = __match_any_sync(FULL, key);
+    int leader = __ffs(peers) - 1;
+    unsigned rank = __popc(peers & ((1u << lane_id()) - 1));
+    unsigned long long base = 0;
+    if (need && (int)lane_id() == leader) {
+        base = atomicAdd(&V.ctl->s[L % 3].send[o], (unsigned long long)__popc(peers));
+    }
+    base = __shfl_sync(FULL, base, leader);
+    if (!need) return;
     vc.records++;
-    uint2 rec = make_uint2(local, (uint32_t)parent);
     if (V.dist) {
-        unsigned long long pos = atomicAdd(&V.ctl->s[L % 3].send[owner], 1ull);
-        V.sendbin[owner][pos] = rec;
+        V.sendbin[o][base + rank] = make_uint2(c, (uint32_t)parent);
     } else {
-        atomicAdd(&V.ctl->s[L % 3].send[owner], 1ull);
-        unsigned long long pos = atomicAdd(&V.ctl_all[owner]->s[L % 3].inbox, 1ull);
-        V.inbox_all[L & 1][owner][pos] = rec;
+        claim_on(V.nvis_all[o], V.nfront_all[(L + 1) & 1][o], V.nlevel_all[o], V.nparent_all[o], V.parents, L, c,
+                 parent, true);
+    }
+}
+
+enum { ACT_NN = 0, ACT_DELEG = 1, ACT_NORMAL = 2 };
+
+// One pushed edge; returns true (with owner/local) when an nn edge is remote.
+template <int ACT>
+__device__ __forceinline__ bool push_edge(const View &V, int L, uint32_t col, int64_t parent, VisitCounters &vc,
+                                          uint32_t &o, uint32_t &c) {
+    if (ACT == ACT_NN) {
+        if (V.p == 1) {
+            claim_normal(V, L, col, parent, true);
+            return false;
+        }
+        o = V.pd.mod(col);
+        c = V.pd.div(col);
+        if ((int)o == V.w) {
+            claim_normal(V, L, c, parent, true);
+            return false;
+        }
+        return true;
+    } else if (ACT == ACT_DELEG) {  // nd / dd: delegate mask (engine.py:225-228, 253-256)
+        if (!tbit(V.dvis, col)) find_delegate(V, L, col, parent, vc.dirty);
+    } else {  // dn: local normal (engine.py:238-241)
+        claim_normal(V, L, col, parent, true);
+    }
+    return false;
+}
+
+// Second stage of a push step: UNR columns per lane are resolved with all
+// status loads issued before any store (stores through the non-restrict state
+// pointers would otherwise serialise one L2 round trip per edge).
+template <int ACT>
+__device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t (&cc)[UNR], const uint32_t (&pp)[UNR],
+                                           const bool (&valid)[UNR], VisitCounters &vc) {
+    // map the column to the (worker-local) vertex it names
+    uint32_t tgt[UNR];
+    bool local[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        local[u] = true;
+        tgt[u] = cc[u];
+        if (ACT == ACT_NN && V.p > 1) {
+            local[u] = (int)V.pd.mod(cc[u]) == V.w;
+            tgt[u] = V.pd.div(cc[u]);
+        }
+    }
+    const uint32_t *vis = ACT == ACT_DELEG ? V.dvis : V.nvis;
+    uint32_t *nxt = ACT == ACT_DELEG ? V.dnext[L & 1] : V.nfront[(L + 1) & 1];
+    // stage 1: visited(<= L) words (read-only this phase: L1 is fine)
+    uint32_t s[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) s[u] = (valid[u] && local[u]) ? __ldca(&vis[tgt[u] >> 5]) : 0xffffffffu;
+    // stage 2: next-level words from L2 (written by other SMs this phase)
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        bool open = !((s[u] >> (tgt[u] & 31)) & 1u);
+        if (ACT == ACT_DELEG && open) vc.dirty = 1;
+        s[u] = open ? __ldcg(&nxt[tgt[u] >> 5]) : 0xffffffffu;
+    }
+    // stage 3: independent atomics, all in flight; only the winner stores
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        const uint32_t bit = 1u << (tgt[u] & 31);
+        s[u] = (s[u] & bit) ? bit : atomicOr(&nxt[tgt[u] >> 5], bit);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+        const uint32_t x = tgt[u];
+        if ((s[u] >> (x & 31)) & 1u) continue;
+        if (ACT == ACT_DELEG) {
+            if (V.parents) V.dcand[x] = pp[u];
+        } else {
+            V.nlevel[x] = L + 1;
+            if (V.parents) V.nparent[x] = pp[u];
+        }
+    }
+    if (ACT == ACT_NN && V.p > 1) {
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            bool remote = valid[u] && !local[u];
+            warp_send(V, L, remote, V.pd.mod(cc[u]), tgt[u], pp[u], vc);
+        }
+    }
+}
+
+// Expand <= 32 rows held one per lane (row start rb, length len, payload par)
+// with all lanes on consecutive edges and UNR independent loads per lane.
+template <int ACT>
+__device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint32_t *__restrict__ col, int64_t rb,
+                                               uint32_t len, uint32_t par, VisitCounters &vc) {
+    unsigned tot;
+    unsigned excl = warp_excl_scan(len, &tot);
+    const unsigned lane = lane_id();
+    for (unsigned base = 0; base < tot; base += 32 * UNR) {
+        uint32_t cc[UNR];
+        uint32_t pp[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            unsigned x = base + u * 32 + lane;
+            int o = owner_search<unsigned>(excl, x);
+            int64_t rbo = __shfl_sync(FULL, rb, o);
+            unsigned eo = __shfl_sync(FULL, excl, o);
+            pp[u] = __shfl_sync(FULL, par, o);
+            cc[u] = x < tot ? __ldg(&col[rbo + (x - eo)]) : 0u;
+        }
+        bool valid[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < tot;
+        push_stage<ACT>(V, L, cc, pp, valid, vc);
+    }
+}
+
+// Load-balanced push over a delegate frontier list (dlist, exclusive prefix
+// dpre, `cnt` rows, `total` edges): this warp handles edges [x0, x1).
+template <int ACT>
+__device__ __forceinline__ void list_push(const View &V, int L, const int64_t *__restrict__ off,
+                                          const uint32_t *__restrict__ col, const uint32_t *__restrict__ list,
+                                          const int64_t *__restrict__ pre, int64_t cnt, int64_t total, int64_t x0,
+                                          int64_t x1, VisitCounters &vc) {
+    if (x0 >= x1) return;
+    const unsigned lane = lane_id();
+    // 32-ary search: largest e with pre[e] <= x0
+    int64_t lo = 0, hi = cnt;
+    while (hi - lo > 32) {
+        int64_t step = (hi - lo + 31) / 32;
+        int64_t idx = lo + (int64_t)lane * step;
+        bool ok = idx < hi && pre[idx] <= x0;
+        unsigned m = __ballot_sync(FULL, ok);
+        int l = 31 - __clz(m);
+        lo = lo + (int64_t)l * step;
+        hi = lo + step < hi ? lo + step : hi;
+    }
+    {
+        int64_t idx = lo + lane;
+        bool ok = idx < hi && pre[idx] <= x0;
+        unsigned m = __ballot_sync(FULL, ok);
+        lo += 31 - __clz(m);
+    }
+    int64_t i = lo;
+    while (x0 < x1) {
+        int64_t e = i + lane;
+        int64_t pb = e < cnt ? pre[e] : total;
+        uint32_t v = e < cnt ? list[e] : 0u;
+        int64_t rb = e < cnt ? __ldg(&off[v]) : 0;
+        uint32_t gx = e < cnt ? (uint32_t)__ldg(&V.del_gid[v]) : 0u;
+        int64_t wend = 0;
+        if (lane == 0) wend = (i + 32 < cnt) ? pre[i + 32] : total;
+        wend = __shfl_sync(FULL, wend, 0);
+        int64_t lim = wend < x1 ? wend : x1;
+        for (int64_t base = x0; base < lim; base += 32 * UNR) {
+            uint32_t cc[UNR];
+            uint32_t pp[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                int64_t x = base + u * 32 + lane;
+                int o = owner_search<int64_t>(pb, x);
+                int64_t rbo = __shfl_sync(FULL, rb, o);
+                int64_t pbo = __shfl_sync(FULL, pb, o);
+                pp[u] = __shfl_sync(FULL, gx, o);
+                cc[u] = x < lim ? __ldg(&col[rbo + (x - pbo)]) : 0u;
+            }
+            bool valid[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < lim;
+            push_stage<ACT>(V, L, cc, pp, valid, vc);
+        }
+        x0 = lim;
+        i += 32;
+    }
+}
+
+// ------------------------------------------------------------------- pulls
+// Early-exit scan (traversal.py:111-139): the first column of row [b, e) whose
+// bit is set in `front`.  A lane loads PULL_LANE columns at once (their bit
+// tests also in flight), and hands rows still unresolved after PULL_LANE_MAX
+// entries to the whole warp (32 * PULL_U columns per step, ballot for order).
+
+struct PullRes {
+    int64_t pos;  // absolute index of the first hit, or -1
+    uint32_t col;
+};
+
+__device__ __forceinline__ bool lane_scan(const uint32_t *__restrict__ col, const uint32_t *__restrict__ front,
+                                          int64_t b, int64_t e, int64_t &j, PullRes &r) {
+    j = b;
+    const int64_t stop = b + PULL_LANE_MAX < e ? b + PULL_LANE_MAX : e;
+    while (j < stop) {
+        uint32_t c[PULL_LANE];
+        bool h[PULL_LANE];
+#pragma unroll
+        for (int u = 0; u < PULL_LANE; u++) c[u] = j + u < e ? __ldg(&col[j + u]) : 0u;
+#pragma unroll
+        for (int u = 0; u < PULL_LANE; u++) h[u] = j + u < e && tbit(front, c[u]);
+#pragma unroll
+        for (int u = 0; u < PULL_LANE; u++)
+            if (h[u]) {
+                r.pos = j + u;
+                r.col = c[u];
+                return true;
+            }
+        j += PULL_LANE;
+    }
+    if (j >= e) {
+        r.pos = -1;
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ PullRes warp_scan_row(const uint32_t *__restrict__ col, const uint32_t *__restrict__ front,
+                                                 int64_t j, int64_t e) {
+    const unsigned lane = lane_id();
+    PullRes r;
+    r.pos = -1;
+    r.col = 0;
+    for (; j < e; j += 32 * PULL_U) {
+        uint32_t c[PULL_U];
+        bool h[PULL_U];
+#pragma unroll
+        for (int u = 0; u < PULL_U; u++) {
+            int64_t x = j + u * 32 + lane;
+            c[u] = x < e ? __ldg(&col[x]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < PULL_U; u++) h[u] = (j + u * 32 + lane < e) && tbit(front, c[u]);
+#pragma unroll
+        for (int u = 0; u < PULL_U; u++) {
+            unsigned m = __ballot_sync(FULL, h[u]);
+            if (m) {
+                int l = __ffs(m) - 1;
+                r.pos = j + u * 32 + l;
+                r.col = __shfl_sync(FULL, c[u], l);
+                return r;
+            }
+        }
+    }
+    return r;
+}
+
+// One pull kind over its candidate words.  cand(wi) gives the candidate bits
+// of word wi; rows come from (off, col); `front` is the parent status bitmap;
+// on_hit(candidate, hit column) records the find.
+template <class CandF, class HitF>
+__device__ __forceinline__ void pull_kind(int64_t nw, int64_t gw, int64_t TW, uint32_t *list,
+                                          const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
+                                          const uint32_t *__restrict__ front, unsigned long long &insp,
+                                          unsigned long long &rows, CandF cand, HitF on_hit) {
+    const unsigned lane = lane_id();
+    for (int64_t base = gw * 32; base < nw; base += TW * 32) {
+        int64_t wi = base + lane;
+        uint32_t word = wi < nw ? cand(wi) : 0u;
+        unsigned cnt = warp_compact(word, wi, list);
+        if (lane == 0) rows += cnt;
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+            unsigned i = g0 + lane;
+            bool ok = i < cnt;
+            uint32_t v = ok ? list[i] : 0u;
+            int64_t b = ok ? __ldg(&off[v]) : 0, e = ok ? __ldg(&off[v + 1]) : 0;
+            PullRes r;
+            r.pos = -1;
+            r.col = 0;
+            int64_t j = e;
+            bool done = ok ? lane_scan(col, front, b, e, j, r) : true;
+            unsigned pend = __ballot_sync(FULL, !done);
+            while (pend) {
+                int l = __ffs(pend) - 1;
+                pend &= pend - 1;
+                int64_t jl = __shfl_sync(FULL, j, l), el = __shfl_sync(FULL, e, l);
+                PullRes rr = warp_scan_row(col, front, jl, el);
+                if ((int)lane == l) r = rr;
+            }
+            if (ok) {
+                if (r.pos >= 0) {
+                    insp += (unsigned long long)(r.pos - b + 1);
+                    on_hit(v, r.col);
+                } else {
+                    insp += (unsigned long long)(e - b);
+                }
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -260,10 +586,6 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     uint32_t *list = sm.list[warp];
     const int p = V.p, w = V.w;
     const uint32_t *nfront_cur = V.nfront[L & 1];
-    const int64_t *off_nn = V.off[KIND_NN], *off_nd = V.off[KIND_ND], *off_dn = V.off[KIND_DN],
-                  *off_dd = V.off[KIND_DD];
-    const uint32_t *col_nn = V.col[KIND_NN], *col_nd = V.col[KIND_ND], *col_dn = V.col[KIND_DN],
-                   *col_dd = V.col[KIND_DD];
 
     // T1: normal frontier -- nn push (always, engine.py:207-222) + nd push.
     if (S.nfront > 0) {
@@ -271,188 +593,71 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
             int64_t wi = base + lane;
             uint32_t word = wi < V.nw_n ? nfront_cur[wi] : 0u;
-            unsigned cnt = warp_compact(word, base + lane, list);
-            // warp_compact uses each lane's own wi; ids are absolute
-            for (unsigned i = lane; i < cnt; i += 32) {
-                uint32_t u = list[i];
-                int64_t gid_u = (int64_t)u * p + w;
-                int64_t b = __ldg(&off_nn[u]), e = __ldg(&off_nn[u + 1]);
-                vc.fv_nn += e - b;
-                for (int64_t j = b; j < e; j++) {
-                    uint32_t g = __ldg(&col_nn[j]);
-                    if (p == 1) {
-                        claim_normal(V, L, g, gid_u, true, vc);
-                    } else {
-                        uint32_t o = V.pd.mod(g), c = V.pd.div(g);
-                        if ((int)o == w) claim_normal(V, L, c, gid_u, true, vc);
-                        else send_record(V, L, o, c, gid_u, vc);
-                    }
-                }
-                if (nd_fwd) {
-                    int64_t b2 = __ldg(&off_nd[u]), e2 = __ldg(&off_nd[u + 1]);
-                    for (int64_t j = b2; j < e2; j++) {
-                        uint32_t x = __ldg(&col_nd[j]);
-                        if (!tbit(V.dvis, x)) find_delegate(V, L, x, gid_u, vc.dirty);
-                    }
-                }
-            }
-            __syncwarp();
-        }
-    }
-
-    // T2: delegate frontier, non-hub rows -- dn / dd push (engine.py:238-263).
-    const bool dn_fwd = dirs[KIND_DN] == FWD, dd_fwd = dirs[KIND_DD] == FWD;
-    if (S.dfront > 0 && (dn_fwd || dd_fwd)) {
-        for (int64_t base = gw * 32; base < V.nw_d; base += TW * 32) {
-            int64_t wi = base + lane;
-            uint32_t word = wi < V.nw_d ? V.dfront[wi] : 0u;
             unsigned cnt = warp_compact(word, wi, list);
-            for (unsigned i = 0; i < cnt; i++) {
-                uint32_t x = list[i];
-                int64_t gx = __ldg(&V.del_gid[x]);
-                if (dn_fwd) {
-                    int64_t b = __ldg(&off_dn[x]), e = __ldg(&off_dn[x + 1]);
-                    if (e - b <= V.hub)
-                        for (int64_t j = b + lane; j < e; j += 32) claim_normal(V, L, __ldg(&col_dn[j]), gx, true, vc);
-                }
-                if (dd_fwd) {
-                    int64_t b = __ldg(&off_dd[x]), e = __ldg(&off_dd[x + 1]);
-                    if (e - b <= V.hub)
-                        for (int64_t j = b + lane; j < e; j += 32) {
-                            uint32_t y = __ldg(&col_dd[j]);
-                            if (!tbit(V.dvis, y)) find_delegate(V, L, y, gx, vc.dirty);
-                        }
+            for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+                unsigned i = g0 + lane;
+                bool ok = i < cnt;
+                uint32_t u = ok ? list[i] : 0u;
+                uint32_t gid = u * (uint32_t)p + (uint32_t)w;
+                int64_t b = ok ? __ldg(&V.off[KIND_NN][u]) : 0, e = ok ? __ldg(&V.off[KIND_NN][u + 1]) : 0;
+                vc.fv_nn += (unsigned long long)(e - b);
+                warp_rows_push<ACT_NN>(V, L, V.col[KIND_NN], b, (uint32_t)(e - b), gid, vc);
+                if (nd_fwd) {
+                    int64_t b2 = ok ? __ldg(&V.off[KIND_ND][u]) : 0, e2 = ok ? __ldg(&V.off[KIND_ND][u + 1]) : 0;
+                    warp_rows_push<ACT_DELEG>(V, L, V.col[KIND_ND], b2, (uint32_t)(e2 - b2), gid, vc);
                 }
             }
             __syncwarp();
         }
     }
 
-    // T3: hub rows of the delegate frontier, split into fixed-size chunks.
-    if (S.chunks > 0 && (dn_fwd || dd_fwd)) {
-        const uint64_t *ch = V.chunks[L & 1];
-        const int64_t nch = (int64_t)S.chunks < V.chunk_cap ? (int64_t)S.chunks : V.chunk_cap;
-        for (int64_t ci = gw; ci < nch; ci += TW) {
-            uint64_t ent = ch[ci];
-            uint32_t x = (uint32_t)(ent >> 32);
-            int kind = (ent & 1) ? KIND_DD : KIND_DN;
-            if ((kind == KIND_DN && !dn_fwd) || (kind == KIND_DD && !dd_fwd)) continue;
-            int64_t idx = (int64_t)((ent >> 1) & 0x7fffffffu);
-            const int64_t *off = V.off[kind];
-            int64_t b0 = __ldg(&off[x]), e0 = __ldg(&off[x + 1]);
-            int64_t b = b0 + idx * V.chunk, e = b + V.chunk < e0 ? b + V.chunk : e0;
-            int64_t gx = __ldg(&V.del_gid[x]);
-            if (kind == KIND_DN) {
-                for (int64_t j = b + lane; j < e; j += 32) claim_normal(V, L, __ldg(&col_dn[j]), gx, true, vc);
-            } else {
-                for (int64_t j = b + lane; j < e; j += 32) {
-                    uint32_t y = __ldg(&col_dd[j]);
-                    if (!tbit(V.dvis, y)) find_delegate(V, L, y, gx, vc.dirty);
-                }
-            }
-        }
+    // T2: delegate frontier -- dn / dd push, load balanced over the level's
+    // edge space (engine.py:238-263).
+    if (dirs[KIND_DN] == FWD && (S.dpack[0] & M38)) {
+        int64_t cnt = (int64_t)(S.dpack[0] >> 38), total = (int64_t)(S.dpack[0] & M38);
+        int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
+        list_push<ACT_NORMAL>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1], cnt, total,
+                              x0, x1, vc);
+    }
+    if (dirs[KIND_DD] == FWD && (S.dpack[1] & M38)) {
+        int64_t cnt = (int64_t)(S.dpack[1] >> 38), total = (int64_t)(S.dpack[1] & M38);
+        int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
+        list_push<ACT_DELEG>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1], cnt, total,
+                             x0, x1, vc);
     }
 
     // T4: dn pull -- unvisited nd-source normals scan nd rows for frontier
-    // delegates (engine.py:242-248, traversal.py:111-139).
+    // delegates (engine.py:242-248).
     if (dirs[KIND_DN] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_ND];
-        for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
-            int64_t wi = base + lane;
-            uint32_t word = wi < V.nw_n ? (srcb[wi] & ~(V.nvis[wi] | nfront_cur[wi])) : 0u;
-            unsigned cnt = warp_compact(word, wi, list);
-            if (lane == 0) vc.pull_rows += cnt;
-            for (unsigned i = lane; i < cnt; i += 32) {
-                uint32_t c = list[i];
-                int64_t b = __ldg(&off_nd[c]), e = __ldg(&off_nd[c + 1]);
-                int64_t j = b;
-                uint32_t x = 0;
-                for (; j < e; j++) {
-                    x = __ldg(&col_nd[j]);
-                    if (tbit(V.dfront, x)) break;
-                }
-                if (j < e) {
-                    vc.insp_bwd[KIND_DN] += j - b + 1;
-                    claim_normal(V, L, c, __ldg(&V.del_gid[x]), false, vc);
-                } else {
-                    vc.insp_bwd[KIND_DN] += e - b;
-                }
-            }
-            __syncwarp();
-        }
+        const uint32_t *nvis = V.nvis;
+        pull_kind(V.nw_n, gw, TW, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, vc.insp_bwd[KIND_DN], vc.pull_rows,
+                  [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
+                  [&](uint32_t c, uint32_t x) { claim_normal(V, L, c, __ldg(&V.del_gid[x]), false); });
     }
-
     // T5: nd pull -- unvisited dn-source delegates scan dn rows for frontier
     // normals (engine.py:229-233).
     if (dirs[KIND_ND] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_DN];
-        for (int64_t base = gw * 32; base < V.nw_d; base += TW * 32) {
-            int64_t wi = base + lane;
-            uint32_t word = wi < V.nw_d ? (srcb[wi] & ~V.dvis[wi]) : 0u;
-            unsigned cnt = warp_compact(word, wi, list);
-            if (lane == 0) vc.pull_rows += cnt;
-            for (unsigned i = lane; i < cnt; i += 32) {
-                uint32_t x = list[i];
-                int64_t b = __ldg(&off_dn[x]), e = __ldg(&off_dn[x + 1]);
-                int64_t j = b;
-                uint32_t c = 0;
-                for (; j < e; j++) {
-                    c = __ldg(&col_dn[j]);
-                    if (tbit(nfront_cur, c)) break;
-                }
-                if (j < e) {
-                    vc.insp_bwd[KIND_ND] += j - b + 1;
-                    find_delegate(V, L, x, (int64_t)c * p + w, vc.dirty);
-                } else {
-                    vc.insp_bwd[KIND_ND] += e - b;
-                }
-            }
-            __syncwarp();
-        }
+        const uint32_t *dvis = V.dvis;
+        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, vc.insp_bwd[KIND_ND], vc.pull_rows,
+                  [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
+                  [&](uint32_t x, uint32_t c) { find_delegate(V, L, x, (int64_t)c * p + w, vc.dirty); });
     }
-
     // T6: dd pull -- unvisited dd-source delegates scan dd rows (engine.py:257-261).
     if (dirs[KIND_DD] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_DD];
-        for (int64_t base = gw * 32; base < V.nw_d; base += TW * 32) {
-            int64_t wi = base + lane;
-            uint32_t word = wi < V.nw_d ? (srcb[wi] & ~V.dvis[wi]) : 0u;
-            unsigned cnt = warp_compact(word, wi, list);
-            if (lane == 0) vc.pull_rows += cnt;
-            for (unsigned i = lane; i < cnt; i += 32) {
-                uint32_t x = list[i];
-                int64_t b = __ldg(&off_dd[x]), e = __ldg(&off_dd[x + 1]);
-                int64_t j = b;
-                uint32_t y = 0;
-                for (; j < e; j++) {
-                    y = __ldg(&col_dd[j]);
-                    if (tbit(V.dfront, y)) break;
-                }
-                if (j < e) {
-                    vc.insp_bwd[KIND_DD] += j - b + 1;
-                    find_delegate(V, L, x, __ldg(&V.del_gid[y]), vc.dirty);
-                } else {
-                    vc.insp_bwd[KIND_DD] += e - b;
-                }
-            }
-            __syncwarp();
-        }
+        const uint32_t *dvis = V.dvis;
+        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DD], V.col[KIND_DD], V.dfront, vc.insp_bwd[KIND_DD], vc.pull_rows,
+                  [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
+                  [&](uint32_t x, uint32_t y) { find_delegate(V, L, x, __ldg(&V.del_gid[y]), vc.dirty); });
     }
 
     // flush: one atomic per warp per counter
     LevelSlot &A = C.s[L % 3];
-    LevelSlot &N = C.s[(L + 1) % 3];
     unsigned long long v;
     v = warp_sum(vc.fv_nn);
     if (lane == 0) atomic_add_u64(&A.fv[KIND_NN], v);
-    v = warp_sum(vc.nfv_nd);
-    if (lane == 0) atomic_add_u64(&N.fv[KIND_ND], v);
-    v = warp_sum(vc.nq_nd);
-    if (lane == 0) atomic_add_u64(&N.q[KIND_ND], v);
-    v = warp_sum(vc.ncount);
-    if (lane == 0) atomic_add_u64(&N.nfront, v);
-    v = warp_sum(vc.local_claims);
-    if (lane == 0) atomic_add_u64(&A.local_claims, v);
     v = warp_sum(vc.records);
     if (lane == 0) atomic_add_u64(&A.records, v);
     for (int k = 1; k < 4; k++) {
@@ -465,99 +670,171 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (lane == 0) atomic_add_u64(&A.pull_rows, v);
 }
 
-// -------------------------------------------------------------- phase F(L)
+// ------------------------------------------------------------ phase F(L)
 
-__device__ __forceinline__ void append_chunks(const View &V, int L, uint32_t x, int kind, int64_t deg) {
-    int64_t nch = (deg + V.chunk - 1) / V.chunk;
-    unsigned long long pos = atomicAdd(&V.ctl->s[(L + 1) % 3].chunks, (unsigned long long)nch);
-    uint64_t *ch = V.chunks[(L + 1) & 1];
-    for (int64_t i = 0; i < nch && (int64_t)pos + i < V.chunk_cap; i++)
-        ch[pos + i] = ((uint64_t)x << 32) | ((uint64_t)i << 1) | (kind == KIND_DD ? 1ull : 0ull);
+struct FinishCounters {
+    unsigned long long dfv_dn, dq_dn, dfv_dd, dq_dd, new_del;
+    unsigned long long nfv_nd, nq_nd, ncount;
+};
+
+// Delegate state of new delegate x (lane-held): level, parent, global output,
+// push-list row lengths.
+__device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, uint64_t &ldn, uint64_t &ldd) {
+    const uint32_t xw = x >> 5, xb = x & 31;
+    ldn = (uint64_t)(__ldg(&V.off[KIND_DN][x + 1]) - __ldg(&V.off[KIND_DN][x]));
+    ldd = (uint64_t)(__ldg(&V.off[KIND_DD][x + 1]) - __ldg(&V.off[KIND_DD][x]));
+    const int64_t gx = V.glevel ? __ldg(&V.del_gid[x]) : 0;
+    V.dlevel[x] = L + 1;
+    int64_t par = 0x7fffffffffffffffLL;
+    if (V.parents) {
+        if (V.cand_all) {
+            for (int s = 0; s < V.P_sources; s++)
+                if ((V.mask_src[L & 1][s][xw] >> xb) & 1u) {
+                    int64_t c = V.cand_src[s][x];
+                    par = c < par ? c : par;
+                }
+        } else if ((V.dnext[L & 1][xw] >> xb) & 1u) {
+            par = V.dcand[x];
+        }
+        V.dparent[x] = par;
+    }
+    if (V.glevel) {
+        V.glevel[gx] = L + 1;
+        if (V.parents) V.gparent[gx] = par;
+    }
 }
 
-__device__ void phase_finish(const View &V, int L, int wb, int nb) {
-    Ctl &C = *V.ctl;
-    LevelSlot &A = C.s[L % 3];
-    LevelSlot &N = C.s[(L + 1) % 3];
-    FinishCounters fc = {};
-    VisitCounters vc = {};
-    const int64_t tid = (int64_t)wb * BT + threadIdx.x, nth = (int64_t)nb * BT;
-    const uint32_t *own_mask = V.dnext[L & 1];
+// F1: delegate mask OR-reduction (comm.py:75-98) -> delegates of level L+1,
+// their state, and the push lists of level L+1 (one packed atomic per warp
+// batch and kind keeps list positions and edge prefixes consistent).
+__device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, uint32_t *list, FinishCounters &fc) {
+    const unsigned lane = lane_id();
     uint32_t *next_mask = V.dnext[(L + 1) & 1];
-
-    // F1: delegate mask OR-reduction (comm.py:75-98) -> new delegates at L+1
-    for (int64_t wi = tid; wi < V.nw_d; wi += nth) {
-        uint32_t r = 0;
-        for (int s = 0; s < V.P_sources; s++) r |= V.mask_src[L & 1][s][wi];
-        uint32_t nw = r & ~V.dvis[wi];
-        next_mask[wi] = 0u;
-        V.dfront[wi] = nw;
-        if (!nw) continue;
-        V.dvis[wi] |= nw;
-        uint32_t own = own_mask[wi];
-        while (nw) {
-            int b = __ffs(nw) - 1;
-            nw &= nw - 1;
-            uint32_t x = (uint32_t)(wi << 5) + b;
-            V.dlevel[x] = L + 1;
-            int64_t par = 0x7fffffffffffffffLL;
-            if (V.parents) {
-                if (V.cand_all) {
-                    for (int s = 0; s < V.P_sources; s++)
-                        if ((V.mask_src[L & 1][s][wi] >> b) & 1u) {
-                            int64_t c = V.cand_src[s][x];
-                            par = c < par ? c : par;
-                        }
-                } else if ((own >> b) & 1u) {
-                    par = V.dcand[x];
-                }
-                V.dparent[x] = par;
-            }
-            if (V.glevel) {
-                int64_t gx = V.del_gid[x];
-                V.glevel[gx] = L + 1;
-                if (V.parents) V.gparent[gx] = par;
-            }
-            int64_t ddn = V.off[KIND_DN][x + 1] - V.off[KIND_DN][x];
-            int64_t ddd = V.off[KIND_DD][x + 1] - V.off[KIND_DD][x];
-            fc.dfv_dn += ddn;
-            fc.dq_dn += ddn > 0;
-            fc.dfv_dd += ddd;
-            fc.dq_dd += ddd > 0;
-            fc.dcount++;
-            fc.new_del++;
-            if (ddn > V.hub) append_chunks(V, L, x, KIND_DN, ddn);
-            if (ddd > V.hub) append_chunks(V, L, x, KIND_DD, ddd);
+    LevelSlot &N = V.ctl->s[(L + 1) % 3];
+    for (int64_t base = gw * 32; base < V.nw_d; base += TW * 32) {
+        int64_t wi = base + lane;
+        uint32_t nw = 0u;
+        if (wi < V.nw_d) {
+            uint32_t r = 0;
+            for (int s = 0; s < V.P_sources; s++) r |= V.mask_src[L & 1][s][wi];
+            uint32_t dv = V.dvis[wi];
+            nw = r & ~dv;
+            next_mask[wi] = 0u;
+            V.dfront[wi] = nw;
+            if (nw) V.dvis[wi] = dv | nw;
         }
+        unsigned cnt = warp_compact(nw, wi, list);
+        if (!cnt) continue;
+        // pass A: state + totals
+        unsigned long long cdn = 0, edn = 0, cdd = 0, edd = 0;
+#pragma unroll 4
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+            unsigned i = g0 + lane;
+            if (i < cnt) {
+                uint64_t ldn, ldd;
+                new_delegate(V, L, list[i], ldn, ldd);
+                cdn += ldn > 0;
+                edn += ldn;
+                cdd += ldd > 0;
+                edd += ldd;
+                fc.new_del++;
+            }
+        }
+        fc.dfv_dn += edn;
+        fc.dq_dn += cdn;
+        fc.dfv_dd += edd;
+        fc.dq_dd += cdd;
+        unsigned long long tdn = warp_sum(cdn), tedn = warp_sum(edn), tdd = warp_sum(cdd), tedd = warp_sum(edd);
+        unsigned long long bdn = 0, bdd = 0;
+        if (lane == 0) {
+            if (tdn) bdn = atomicAdd(&N.dpack[0], (tdn << 38) + tedn);
+            if (tdd) bdd = atomicAdd(&N.dpack[1], (tdd << 38) + tedd);
+        }
+        bdn = __shfl_sync(FULL, bdn, 0);
+        bdd = __shfl_sync(FULL, bdd, 0);
+        // pass B: list entries in batch order
+        unsigned long long pdn = bdn >> 38, qdn = bdn & M38, pdd = bdd >> 38, qdd = bdd & M38;
+        uint32_t *ldn_list = V.dlist[0][(L + 1) & 1], *ldd_list = V.dlist[1][(L + 1) & 1];
+        int64_t *ldn_pre = V.dpre[0][(L + 1) & 1], *ldd_pre = V.dpre[1][(L + 1) & 1];
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+            unsigned i = g0 + lane;
+            uint32_t x = i < cnt ? list[i] : 0u;
+            uint64_t a = i < cnt ? (uint64_t)(__ldg(&V.off[KIND_DN][x + 1]) - __ldg(&V.off[KIND_DN][x])) : 0;
+            uint64_t b = i < cnt ? (uint64_t)(__ldg(&V.off[KIND_DD][x + 1]) - __ldg(&V.off[KIND_DD][x])) : 0;
+            unsigned t1, t2;
+            unsigned long long e1, e2;
+            unsigned p1 = warp_excl_scan(a > 0 ? 1u : 0u, &t1);
+            unsigned long long s1 = warp_excl_scan64(a, &e1);
+            unsigned p2 = warp_excl_scan(b > 0 ? 1u : 0u, &t2);
+            unsigned long long s2 = warp_excl_scan64(b, &e2);
+            if (a > 0) {
+                ldn_list[pdn + p1] = x;
+                ldn_pre[pdn + p1] = (int64_t)(qdn + s1);
+            }
+            if (b > 0) {
+                ldd_list[pdd + p2] = x;
+                ldd_pre[pdd + p2] = (int64_t)(qdd + s2);
+            }
+            pdn += t1;
+            qdn += e1;
+            pdd += t2;
+            qdd += e2;
+        }
+        __syncwarp();
     }
+}
 
-    // F2: ingest remote records (engine.py:147-157): first claim wins.
-    const unsigned long long nin = A.inbox;
+// F2 (distributed only): ingest remote records (engine.py:147-157).
+__device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
+    const unsigned long long nin = V.ctl->s[L % 3].inbox;
     const uint2 *inbox = V.inbox[L & 1];
     for (int64_t i = tid; i < (int64_t)nin; i += nth) {
         uint2 rec = inbox[i];
-        int32_t lv = V.nlevel[rec.x];
-        if ((uint32_t)lv <= (uint32_t)L) continue;  // visited at <= L
-        claim_normal(V, L, rec.x, (int64_t)rec.y, false, vc);
+        claim_normal(V, L, rec.x, (int64_t)rec.y, true);
     }
+}
 
-    // F3: fold this level's frontier into visited and clear it for reuse.
+// F3: fold the new normal frontier into visited, clear the old one, and count
+// the new frontier's previsit statistics (FV_nd, q_nd, |frontier|).
+__device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uint32_t *list, FinishCounters &fc) {
+    const unsigned lane = lane_id();
     uint32_t *cur = V.nfront[L & 1];
-    for (int64_t wi = tid; wi < V.nw_n; wi += nth) {
-        uint32_t x = cur[wi];
-        if (x) {
-            V.nvis[wi] |= x;
-            cur[wi] = 0u;
+    const uint32_t *nxt = V.nfront[(L + 1) & 1];
+    for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
+        int64_t wi = base + lane;
+        uint32_t nw = 0u;
+        if (wi < V.nw_n) {
+            if (cur[wi]) cur[wi] = 0u;
+            nw = nxt[wi];
+            if (nw) V.nvis[wi] |= nw;
         }
+        if (!__any_sync(FULL, nw != 0u)) continue;
+        unsigned cnt = warp_compact(nw, wi, list);
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+            unsigned i = g0 + lane;
+            if (i < cnt) {
+                uint32_t c = list[i];
+                int64_t dnd = __ldg(&V.off[KIND_ND][c + 1]) - __ldg(&V.off[KIND_ND][c]);
+                fc.nfv_nd += (unsigned long long)dnd;
+                fc.nq_nd += dnd > 0;
+                fc.ncount++;
+            }
+        }
+        __syncwarp();
     }
+}
 
+__device__ void flush_finish(const View &V, int L, FinishCounters &fc, int wb, bool zero_slot) {
+    Ctl &C = *V.ctl;
+    LevelSlot &A = C.s[L % 3];
+    LevelSlot &N = C.s[(L + 1) % 3];
     const unsigned lane = lane_id();
     unsigned long long v;
-    v = warp_sum(vc.nfv_nd + fc.nfv_nd);
+    v = warp_sum(fc.nfv_nd);
     if (lane == 0) atomic_add_u64(&N.fv[KIND_ND], v);
-    v = warp_sum(vc.nq_nd + fc.nq_nd);
+    v = warp_sum(fc.nq_nd);
     if (lane == 0) atomic_add_u64(&N.q[KIND_ND], v);
-    v = warp_sum(vc.ncount + fc.ncount);
+    v = warp_sum(fc.ncount);
     if (lane == 0) atomic_add_u64(&N.nfront, v);
     v = warp_sum(fc.dfv_dn);
     if (lane == 0) atomic_add_u64(&N.fv[KIND_DN], v);
@@ -567,16 +844,30 @@ __device__ void phase_finish(const View &V, int L, int wb, int nb) {
     if (lane == 0) atomic_add_u64(&N.fv[KIND_DD], v);
     v = warp_sum(fc.dq_dd);
     if (lane == 0) atomic_add_u64(&N.q[KIND_DD], v);
-    v = warp_sum(fc.dcount);
-    if (lane == 0) atomic_add_u64(&N.dfront, v);
     v = warp_sum(fc.new_del);
-    if (lane == 0) atomic_add_u64(&A.new_del, v);
-    if (wb == 0 && threadIdx.x == 0) {
+    if (lane == 0) {
+        atomic_add_u64(&N.dfront, v);
+        atomic_add_u64(&A.new_del, v);
+    }
+    if (zero_slot && wb == 0 && threadIdx.x == 0) {
         // slot (L+2)%3 is idle during level L: clear it for level L+2
         LevelSlot &Z = C.s[(L + 2) % 3];
         unsigned long long *z = (unsigned long long *)&Z;
         for (size_t i = 0; i < sizeof(LevelSlot) / 8; i++) z[i] = 0ull;
     }
+}
+
+enum { F_DELEGATES = 1, F_INGEST = 2, F_NORMALS = 4 };
+
+__device__ void phase_finish(const View &V, int L, int wb, int nb, Smem &sm, int parts) {
+    FinishCounters fc = {};
+    const int64_t gw = (int64_t)wb * WPB + warp_id(), TW = (int64_t)nb * WPB;
+    const int64_t tid = (int64_t)wb * BT + threadIdx.x, nth = (int64_t)nb * BT;
+    uint32_t *list = sm.list[warp_id()];
+    if (parts & F_DELEGATES) finish_delegates(V, L, gw, TW, list, fc);
+    if (parts & F_INGEST) finish_ingest(V, L, tid, nth);
+    if (parts & F_NORMALS) finish_normals(V, L, gw, TW, list, fc);
+    flush_finish(V, L, fc, wb, (parts & F_DELEGATES) != 0);
 }
 
 // ------------------------------------------------------------ init / seed
@@ -622,13 +913,22 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         S.fv[KIND_DD] = ddd;
         S.q[KIND_DD] = ddd > 0;
         S.dfront = 1;
-        if (ddn > V.hub) append_chunks(V, -1, x, KIND_DN, ddn);
-        if (ddd > V.hub) append_chunks(V, -1, x, KIND_DD, ddd);
+        if (ddn > 0) {
+            V.dlist[0][0][0] = x;
+            V.dpre[0][0][0] = 0;
+            S.dpack[0] = (1ull << 38) | (unsigned long long)ddn;
+        }
+        if (ddd > 0) {
+            V.dlist[1][0][0] = x;
+            V.dpre[1][0][0] = 0;
+            S.dpack[1] = (1ull << 38) | (unsigned long long)ddd;
+        }
     } else if ((int)(source % V.p) == V.w) {
         uint32_t c = (uint32_t)(source / V.p);
         V.nlevel[c] = 0;
         if (V.parents) V.nparent[c] = source;
         V.nfront[0][c >> 5] |= 1u << (c & 31);
+        V.nvis[c >> 5] |= 1u << (c & 31);
         int64_t dnd = V.off[KIND_ND][c + 1] - V.off[KIND_ND][c];
         S.fv[KIND_ND] = dnd;
         S.q[KIND_ND] = dnd > 0;
@@ -636,14 +936,13 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
     }
 }
 
-// Continue after level L?  engine.py:303-306: local news, new delegates, or
-// any record in flight (over all in-process workers).
+// Continue after level L?  engine.py:303-306: new local normals, new
+// delegates, or any record in flight (over all in-process workers).
 __device__ __forceinline__ bool level_continue(const View *views, int W, int L) {
-    const LevelSlot &A0 = views[0].ctl->s[L % 3];
-    if (A0.new_del) return true;
+    if (views[0].ctl->s[L % 3].new_del) return true;
     for (int i = 0; i < W; i++) {
-        const LevelSlot &A = views[i].ctl->s[L % 3];
-        if (A.local_claims || A.records) return true;
+        const Ctl &c = *views[i].ctl;
+        if (c.s[(L + 1) % 3].nfront || c.s[L % 3].records) return true;
     }
     return false;
 }

@@ -25,10 +25,9 @@ struct LevelSlot {
     unsigned long long q[4];         // |queue| per kind (previsit queue sizes)
     unsigned long long nfront;       // normals in the frontier
     unsigned long long dfront;       // delegates in the frontier
-    unsigned long long chunks;       // hub chunk entries for the delegate frontier
+    unsigned long long dpack[2];     // delegate frontier lists (dn, dd): count << 38 | edges
     unsigned long long insp_bwd[4];  // backward inspections at this level
     unsigned long long records;      // remote normal records sent at this level
-    unsigned long long local_claims; // local normals claimed for level+1 (engine.py:280-289)
     unsigned long long dirty;        // this worker found >= 1 new delegate (comm.py:33-36)
     unsigned long long new_del;      // delegates discovered at the barrier
     unsigned long long inbox;        // records delivered to this worker
@@ -43,6 +42,7 @@ struct Ctl {
     unsigned int bar_count, bar_gen; // grid barrier (persistent engine)
     unsigned int abort;              // watchdog / error flag
     int last_level;                  // iterations when the loop ended
+    unsigned long long t_start, t_seeded;  // globaltimer: kernel start, after init+seed
     int cont;                        // host-loop: continue flag
     int pad;
 };
@@ -58,6 +58,8 @@ struct IterRec {
     unsigned long long messages;
     unsigned long long new_del;
     unsigned long long rows;         // rows expanded (push) + scanned (pull)
+    unsigned long long nfront, dfront;
+    unsigned long long t[3];         // globaltimer at V start, V end, F end (persistent engine)
     unsigned long long send[MAXW];
 };
 
@@ -68,9 +70,7 @@ struct View {
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
     int rec_cap;
-    int hub;                         // rows longer than this go to hub chunks
-    int chunk;                       // edges per hub chunk
-    int pad0;
+    int pad0, pad1, pad2;
     PDiv pd;
     int64_t n, n_local, d, nw_n, nw_d;
     double f0[4], f1[4];
@@ -85,15 +85,18 @@ struct View {
     int64_t *dparent;
     int64_t *dcand;
     uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
-    uint64_t *chunks[2];
-    int64_t chunk_cap;
+    uint32_t *dlist[2][2];           // delegate frontier per push kind (0 dn, 1 dd) and parity
+    int64_t *dpre[2][2];             // exclusive edge prefix of dlist rows
     uint2 *inbox[2];
     int64_t inbox_cap;
     uint2 *sendbin[MAXW];            // dist: per destination segment
     int64_t sendcap[MAXW];
     Ctl *ctl;
     Ctl *ctl_all[MAXW];              // in-process: every worker's control block
-    uint2 *inbox_all[2][MAXW];       // in-process: every worker's inboxes
+    uint32_t *nvis_all[MAXW];        // in-process: peers' normal state (direct remote claims)
+    uint32_t *nfront_all[2][MAXW];
+    int32_t *nlevel_all[MAXW];
+    int64_t *nparent_all[MAXW];
     const uint32_t *mask_src[2][MAXW];
     const int64_t *cand_src[MAXW];
     IterRec *rec;
@@ -162,11 +165,12 @@ struct WorkerHost {
     DArray<int32_t> nlevel, dlevel;
     DArray<int64_t> nparent, dparent, dcand;
     DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
-    DArray<uint64_t> chunks0, chunks1;
+    DArray<uint32_t> dlist[4];       // [kind*2 + parity]
+    DArray<int64_t> dpre[4];
     DArray<uint2> inbox0, inbox1, sendbuf;
     DArray<Ctl> ctl;
     DArray<IterRec> rec;
-    int64_t chunk_cap = 0, inbox_cap = 0;
+    int64_t inbox_cap = 0;
     int64_t send_off[MAXW + 1];
 };
 

@@ -1,0 +1,13 @@
+"""Small driver for ncu: s24 graph, a few BFS roots (device-resident results)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1803_03922_b200 as api
+from paper_1803_03922_b200.engine import bfs_device
+from bench import graph500_roots
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+mode = sys.argv[2] if len(sys.argv) > 2 else "dobfs"
+pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40)), 16, api.ClusterShape(1, 1))
+roots = graph500_roots(pg.classification.out_degree, 8)
+for r in roots[:4]:
+    st = bfs_device(pg, r, mode=mode)
+    print(r, st.device_ms)
