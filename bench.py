@@ -128,7 +128,7 @@ def alg_bytes(st, n_total: int) -> float:
     reads a 4-byte column and tests one status bit; every expanded/scanned row
     reads two 8-byte offsets; the depth (4 B) and parent (8 B) arrays are
     written once per vertex."""
-    insp = sum(st.inspections[k][0] + st.inspections[k][1] for k in range(4))
+    insp = st.work_inspections  # executed (<= reference-accounted when pulls replace pushes)
     return insp * (4.0 + 1.0 / 8.0) + 16.0 * st.rows_touched + 12.0 * n_total
 
 
@@ -251,6 +251,7 @@ def run_ours(args, world, rank, local_rank):
         "iterations_mean": float(np.mean([s.iterations for s in stats])),
         "inspections_mean": float(np.mean([sum(s.inspections[k][0] + s.inspections[k][1] for k in range(4))
                                            for s in stats])),
+        "executed_inspections_mean": float(np.mean([s.work_inspections for s in stats])),
     }
     if rank == 0 and not args.no_cpu_baseline and not dist:
         line["cpu_baseline"] = cpu_baseline_same_graph(pg, roots, args, n, m)

@@ -84,7 +84,9 @@ typedef struct {
     int32_t parent_mode;        /* 0 none, 1 any valid tree (timed), 2 min-ID */
     int32_t engine;             /* 0 auto, 1 host-driven level loop, 2 persistent kernel */
     int32_t record_iterations;  /* keep per-iteration records for dbfs_bfs_iteration */
-    int32_t _pad;
+    int32_t exec_policy;        /* 1: on symmetric graphs in dobfs mode, execute a FORWARD-reported
+                                   kind as the equivalent pull when cheaper (reported directions and
+                                   counters unchanged); 0: execute exactly the reported directions */
 } dbfs_bfs_options;
 
 typedef struct {
@@ -99,6 +101,7 @@ typedef struct {
     int64_t d2h_bytes;          /* device->host bytes copied by this call */
     int64_t rows_touched;       /* CSR rows expanded (push) or scanned (pull), all levels */
     double init_us;             /* device time of state init + seeding */
+    int64_t work_inspections;   /* inspections actually executed (<= reported when pulls replace pushes) */
     int32_t per_iteration_truncated;
     int32_t engine_used;        /* 1 host loop, 2 persistent */
 } dbfs_run_stats;
@@ -114,6 +117,11 @@ typedef struct {
     int64_t pair_count;
     int64_t frontier_normals;   /* normals at this level (all workers) */
     int64_t frontier_delegates; /* delegates at this level */
+    int64_t work[4];            /* executed inspections per kind */
+    int32_t exec_dirs[4];       /* executed strategy per kind on worker 0 (0 push, 1 pull) */
+    double task_avg_us[8];      /* worker 0 per-task mean warp time (T1 normal push, T2 dn push, T2 dd push,
+                                   T4 dn pull, T5 nd pull, T6 dd pull, F delegates, F normals) */
+    double task_max_us[8];      /* worker 0 per-task max warp time */
     double visit_us;            /* device time of the visit phase (worker 0's clock) */
     double finish_us;           /* device time of the barrier/apply phase */
 } dbfs_iteration;
@@ -154,6 +162,9 @@ int32_t dbfs_graph_build_edges(dbfs_ctx *ctx, const int64_t *src, const int64_t 
                                int64_t n, int64_t theta, int32_t p_rank, int32_t p_gpu,
                                dbfs_graph **out);
 int32_t dbfs_graph_free(dbfs_graph *g);
+/* Declare the edge multiset symmetric (every (u,v) has its (v,u)); RMAT builds with
+ * symmetrize set are symmetric by construction. */
+int32_t dbfs_graph_set_symmetric(dbfs_graph *g, int32_t symmetric);
 int32_t dbfs_graph_info_get(const dbfs_graph *g, dbfs_graph_info *out);
 /* rows[4], nnz[4] of a local worker's nn/nd/dn/dd CSRs; n_nd_src = len(nd_source_list). */
 int32_t dbfs_graph_worker_info(const dbfs_graph *g, int32_t worker, int64_t *n_local, int64_t *rows,

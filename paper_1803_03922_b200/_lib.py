@@ -50,20 +50,21 @@ class BfsOptionsC(ctypes.Structure):
     _fields_ = [("mode", i32), ("allow_switch_back", i32), ("source", i64),
                 ("factor0", dbl * 4), ("factor1", dbl * 4),
                 ("local_all2all", i32), ("uniquify", i32), ("parent_mode", i32), ("engine", i32),
-                ("record_iterations", i32), ("_pad", i32)]
+                ("record_iterations", i32), ("exec_policy", i32)]
 
 
 class RunStatsC(ctypes.Structure):
     _fields_ = [("iterations", i64), ("inspections", (i64 * 2) * 4), ("b_measured", dbl),
                 ("device_ms", dbl), ("reached", i64), ("kernel_launches", i64), ("wire_bytes", i64),
-                ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64), ("init_us", dbl),
+                ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64), ("init_us", dbl), ("work_inspections", i64),
                 ("per_iteration_truncated", i32), ("engine_used", i32)]
 
 
 class IterationC(ctypes.Structure):
     _fields_ = [("iteration", i64), ("inspections", i64 * 4), ("fv", i64 * 4), ("mask_bytes", dbl),
                 ("normal_bytes", i64), ("message_count", i64), ("pair_count", i64),
-                ("frontier_normals", i64), ("frontier_delegates", i64), ("visit_us", dbl), ("finish_us", dbl)]
+                ("frontier_normals", i64), ("frontier_delegates", i64), ("work", i64 * 4), ("exec_dirs", i32 * 4),
+                ("task_avg_us", dbl * 8), ("task_max_us", dbl * 8), ("visit_us", dbl), ("finish_us", dbl)]
 
 
 P = ctypes.POINTER
@@ -89,6 +90,7 @@ SIGNATURES = {
     "dbfs_graph_build_rmat": (i32, [vp, P(RmatParamsC), i64, i32, i32, P(vp)]),
     "dbfs_graph_build_edges": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, P(vp)]),
     "dbfs_graph_free": (i32, [vp]),
+    "dbfs_graph_set_symmetric": (i32, [vp, i32]),
     "dbfs_graph_info_get": (i32, [vp, P(GraphInfoC)]),
     "dbfs_graph_worker_info": (i32, [vp, i32, P(i64), vp, vp, P(i64)]),
     "dbfs_graph_export_csr": (i32, [vp, i32, i32, vp, vp]),

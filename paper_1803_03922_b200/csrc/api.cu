@@ -205,6 +205,7 @@ int32_t dbfs_graph_build_rmat(dbfs_ctx *ctx, const dbfs_rmat_params *params, int
     int32_t rc = guard([&] {
         init_graph(g->g, ctx, theta, p_rank, p_gpu);
         build_graph_rmat(g->g, *params);
+        g->g.symmetric = params->symmetrize != 0;
     });
     if (rc) delete g;
     else *out = g;
@@ -231,6 +232,10 @@ int32_t dbfs_graph_free(dbfs_graph *g) {
         cudaSetDevice(g->g.ctx->device);
         delete g;
     });
+}
+
+int32_t dbfs_graph_set_symmetric(dbfs_graph *g, int32_t symmetric) {
+    return guard([&] { g->g.symmetric = symmetric != 0; });
 }
 
 int32_t dbfs_graph_info_get(const dbfs_graph *gg, dbfs_graph_info *out) {
@@ -341,7 +346,15 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
             }
             any_new |= x.new_del > 0;
             r.frontier_normals += (int64_t)x.nfront;
+            for (int k = 0; k < 4; k++) r.work[k] += (int64_t)x.work[k];
             if (i == 0) {
+                for (int k = 0; k < 4; k++) r.exec_dirs[k] = x.exec_dir[k];
+                double ghz = g.clock_ghz > 0 ? g.clock_ghz : 1.9;
+                double nwarps = g.warps_per_worker > 0 ? g.warps_per_worker : 1;
+                for (int k = 0; k < 8; k++) {
+                    r.task_avg_us[k] = (double)x.tsum[k] / nwarps / (ghz * 1e3);
+                    r.task_max_us[k] = (double)x.tmax[k] / (ghz * 1e3);
+                }
                 r.frontier_delegates = (int64_t)x.dfront;
                 if (x.t[1] > x.t[0]) r.visit_us = (double)(x.t[1] - x.t[0]) / 1e3;
                 if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;

@@ -100,7 +100,8 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
 __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
                                                        uint32_t src_del, GridBar *bar, int rec_cap,
                                                        AsmArgs asm_args, int do_assemble) {
-    __shared__ Smem sm;
+    extern __shared__ uint4 dsm[];
+    Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
     const View &V = views[wsel];
     const unsigned nblocks = gridDim.x;
@@ -139,12 +140,14 @@ __global__ void k_seed(const View *__restrict__ views, int W, int64_t source, ui
 }
 
 __global__ void __launch_bounds__(BT, DBFS_MINB) k_visit(const View *__restrict__ views, int W, int L) {
-    __shared__ Smem sm;
+    extern __shared__ uint4 dsm[];
+    Smem &sm = *reinterpret_cast<Smem *>(dsm);
     phase_visit(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W, sm);
 }
 
 __global__ void __launch_bounds__(BT) k_finish(const View *__restrict__ views, int W, int L, int parts) {
-    __shared__ Smem sm;
+    extern __shared__ uint4 dsm[];
+    Smem &sm = *reinterpret_cast<Smem *>(dsm);
     phase_finish(views[blockIdx.x % W], L, blockIdx.x / W, gridDim.x / W, sm, parts);
 }
 
@@ -160,8 +163,11 @@ Graph::~Graph() {}
 int32_t *Graph::levels_dev() { return (p == 1 && !dist) ? workers[0].nlevel.p : glevel.p; }
 int64_t *Graph::parents_dev() { return (p == 1 && !dist) ? workers[0].nparent.p : gparent.p; }
 
+void build_sorted_dd(Graph &g);
+
 static void ensure_resources(Graph &g) {
     if (g.bfs_ready) return;
+    if (g.symmetric) build_sorted_dd(g);
     Ctx &ctx = *g.ctx;
     const int W = (int)g.workers.size();
     g.W = W;
@@ -199,6 +205,7 @@ static void ensure_resources(Graph &g) {
         Wk.dfront.alloc(std::max<int64_t>(nw_d, 1));
         Wk.dnext0.alloc(std::max<int64_t>(nw_d, 1));
         Wk.dnext1.alloc(std::max<int64_t>(nw_d, 1));
+        Wk.coarse.alloc(4 * FW);
         for (int j = 0; j < 4; j++) {
             Wk.dlist[j].alloc(std::max<int64_t>(g.d, 1));
             Wk.dpre[j].alloc(g.d + 1);
@@ -247,9 +254,12 @@ static void ensure_resources(Graph &g) {
             V.off[k] = g.off_all.p + Wk.base[k];
             V.col[k] = g.col_all.p;
             V.src_bits[k] = Wk.src_bits[k].p;
+            V.deg[k] = Wk.deg[k].p;
             V.total_src[k] = (unsigned long long)Wk.n_src[k];
+            V.nnz[k] = (unsigned long long)Wk.nnz[k];
         }
         V.del_gid = g.del_gid.p;
+        V.col_sorted_dd = g.col_sorted.n ? g.col_sorted.p : nullptr;
         V.nlevel = Wk.nlevel.p;
         V.nparent = Wk.nparent.p;
         V.dlevel = Wk.dlevel.p;
@@ -262,6 +272,10 @@ static void ensure_resources(Graph &g) {
         V.dfront = Wk.dfront.p;
         V.dnext[0] = Wk.dnext0.p;
         V.dnext[1] = Wk.dnext1.p;
+        for (int par = 0; par < 2; par++) {
+            V.coarse_d[par] = Wk.coarse.p + par * FW;
+            V.coarse_n[par] = Wk.coarse.p + (2 + par) * FW;
+        }
         for (int kk = 0; kk < 2; kk++)
             for (int par = 0; par < 2; par++) {
                 V.dlist[kk][par] = Wk.dlist[kk * 2 + par].p;
@@ -305,9 +319,19 @@ static void ensure_resources(Graph &g) {
     (void)ctx;
 }
 
+static void set_smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    DBFS_CUDA(cudaFuncSetAttribute(k_bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
+    DBFS_CUDA(cudaFuncSetAttribute(k_visit, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
+    DBFS_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
+    done = true;
+}
+
 static int persistent_grid(Graph &g, int *blocks_per_sm) {
     int occ = 0;
-    DBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_persistent, BT, 0));
+    set_smem_attrs();
+    DBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_persistent, BT, sizeof(Smem)));
     DBFS_CHECK(occ >= 1, DBFS_EINTERNAL, "persistent kernel cannot be resident");
     *blocks_per_sm = occ;
     int grid = g.ctx->num_sms * occ;
@@ -392,6 +416,8 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         V.mode = o.mode;
         V.allow_back = o.allow_switch_back;
         V.parents = parents;
+        V.symmetric = g.symmetric;
+        V.exec_policy = o.exec_policy;
         for (int k = 0; k < 4; k++) {
             V.f0[k] = o.factor0[k];
             V.f1[k] = o.factor1[k];
@@ -414,17 +440,34 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
 
     GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
     if (engine == 2) DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
+    // everything host-side happens before ev0: the event pair brackets only device work
+    if (g.clock_ghz <= 0) {
+        int khz = 0;
+        cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx.device);
+        g.clock_ghz = khz / 1e6;
+    }
+    set_smem_attrs();
+    int pgrid = 0;
+    if (engine == 2) {
+        if (g.pgrid <= 0) {
+            int bps = 0;
+            g.pgrid = persistent_grid(g, &bps);
+        }
+        pgrid = g.pgrid;
+        g.warps_per_worker = (double)pgrid / W * WPB;
+    }
     DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
     if (engine == 2) {
-        int bps = 0;
-        int grid = persistent_grid(g, &bps);
+        int grid = pgrid;
         const View *vp = g.views.p;
         int64_t src = o.source;
         int rec_cap = g.rec_cap;
+        (void)grid;
         int do_asm = assemble ? 1 : 0;
         void *args[] = {(void *)&vp, (void *)&W, (void *)&src, (void *)&src_del, (void *)&bar,
                         (void *)&rec_cap, (void *)&aa, (void *)&do_asm};
-        DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, 0, ctx.stream));
+        DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, sizeof(Smem),
+                                              ctx.stream));
         DBFS_LAUNCHED();
         DBFS_CUDA(cudaEventRecord(ctx.ev1, ctx.stream));
         DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -436,6 +479,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         iterations = c0.last_level;
     } else {
         const int grid = std::max(W, (ctx.num_sms * 4 / W) * W);
+        g.warps_per_worker = (double)grid / W * WPB;
         k_init<<<grid, BT, 0, ctx.stream>>>(g.views.p, W);
         DBFS_LAUNCHED();
         k_seed<<<W, 32, 0, ctx.stream>>>(g.views.p, W, o.source, src_del);
@@ -444,16 +488,16 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         std::vector<Ctl> hc(W);
         int L = 0;
         for (;; L++) {
-            k_visit<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L);
+            k_visit<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L);
             DBFS_LAUNCHED();
             if (g.dist) dist_exchange(g, L, sc);
             if (g.dist) {
-                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_INGEST);
+                k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_INGEST);
                 DBFS_LAUNCHED();
-                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_NORMALS);
+                k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_NORMALS);
                 DBFS_LAUNCHED();
             } else {
-                k_finish<<<grid, BT, 0, ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_NORMALS);
+                k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_NORMALS);
                 DBFS_LAUNCHED();
             }
             for (int i = 0; i < W; i++)
@@ -559,10 +603,15 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
                 if (r.new_del && g.p > 1) wire += (int64_t)(g.p - 1) * nwords(g.d) * 4 / W;
             }
         st->wire_bytes = wire;
-        int64_t rows = 0;
+        int64_t rows = 0, work = 0;
         for (int L = 0; L < nrec; L++)
-            for (int i = 0; i < W; i++) rows += (int64_t)g.last_rec[(size_t)L * W + i].rows;
+            for (int i = 0; i < W; i++) {
+                const IterRec &r = g.last_rec[(size_t)L * W + i];
+                rows += (int64_t)r.rows;
+                for (int k = 0; k < 4; k++) work += (int64_t)r.work[k];
+            }
         st->rows_touched = rows;
+        st->work_inspections = work;
         // library-side copies of this call: views + options up, control block / records down
         st->h2d_bytes = (int64_t)(sizeof(View) * W);
         if (engine == 2) {

@@ -31,9 +31,26 @@ constexpr int BT = 256;        // threads per block
 constexpr int WPB = BT / 32;   // warps per block
 constexpr int LIST = 1024;     // per-warp compaction buffer (32 words x 32 bits)
 
+constexpr int FW = 8192;       // words of the coarse frontier filter (32 KB, 2^18 bits)
+#ifndef DBFS_FILTER
+#define DBFS_FILTER 0
+#endif
+
 struct Smem {
     uint32_t list[WPB][LIST];
+#if DBFS_FILTER
+    uint32_t filt[FW];         // coarse filter of the pull frontier (when sparse)
+#else
+    uint32_t filt[1];
+#endif
 };
+
+// Coarse filter: bit (x & 31) of word (x >> 10) & (FW-1) is the OR of the 32
+// frontier words of x's 1024-vertex group -- a warp folds its 32 words into one
+// coarse word with a shuffle OR and one atomic.
+__device__ __forceinline__ bool coarse_hit(const uint32_t *filt, uint32_t x) {
+    return (filt[(x >> 10) & (FW - 1)] >> (x & 31)) & 1u;
+}
 
 struct GridBar {
     unsigned int count;
@@ -136,6 +153,36 @@ __host__ __device__ inline void level_dirs(const View &V, const Ctl &c, int L, i
     }
 }
 
+// Executed strategy per kind.  The reported direction (and its counter) is the
+// reference rule's; when that rule says FORWARD on a symmetric graph, pushing
+// the frontier's k-rows and pulling over the reverse rows of the unvisited
+// k-candidates find the same vertex set, so the executor takes the cheaper one
+// (estimated L2 requests: push ~4 per edge with its atomics, pull ~1.5 per
+// scanned entry with hit probability FV_k / nnz_k).
+__host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, const unsigned long long *cum,
+                                          const int dirs[4], int ex[4]) {
+    for (int k = 0; k < 4; k++) ex[k] = dirs[k];
+    if (V.mode != 1 || !V.symmetric || !V.exec_policy) return;
+    const unsigned long long u_nd = V.total_src[KIND_ND] - cum[KIND_ND];
+    const unsigned long long u_dn = V.total_src[KIND_DN] - cum[KIND_DN];
+    const unsigned long long u_dd = V.total_src[KIND_DD] - cum[KIND_DD];
+    for (int k = 1; k < 4; k++) {
+        if (dirs[k] != FWD || S.fv[k] == 0) continue;
+        // reverse kind scanned by the equivalent pull, and its candidate count
+        int rev = k == KIND_ND ? KIND_DN : (k == KIND_DN ? KIND_ND : KIND_DD);
+        double U = (double)(k == KIND_ND ? u_dn : (k == KIND_DN ? u_nd : u_dd));
+        double rows = (double)(V.total_src[rev] ? V.total_src[rev] : 1);
+        double avg = (double)V.nnz[rev] / rows;
+        double scan = (double)V.nnz[k] / (double)S.fv[k];
+        if (k == KIND_DD && V.col_sorted_dd) scan = scan < 2.0 ? scan : 2.0;  // hubs first
+        if (scan > avg) scan = avg;
+        double words = (double)(rev == KIND_ND ? V.nw_n : V.nw_d);
+        double pull = 1.5 * U * scan + 0.25 * words;
+        double push = 4.0 * (double)S.fv[k];
+        if (pull < push) ex[k] = BWD;
+    }
+}
+
 // Per-iteration record of level L (engine.py:291-302, one worker).
 __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, IterRec &r) {
     const LevelSlot &S = c.s[L % 3];
@@ -151,6 +198,14 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         r.insp[k] = r.dir[k] == FWD ? S.fv[k] : S.insp_bwd[k];
     }
     r.records = S.records;
+    for (int k = 0; k < 4; k++) {
+        r.work[k] = S.work[k];
+        r.exec_dir[k] = S.exec_dir[k];
+    }
+    for (int k = 0; k < 8; k++) {
+        r.tsum[k] = S.tsum[k];
+        r.tmax[k] = S.tmax[k];
+    }
     r.nfront = S.nfront;
     r.dfront = S.dfront;
     r.rows = S.pull_rows;
@@ -172,8 +227,6 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
 #define DBFS_UNR 4
 #endif
 constexpr int UNR = DBFS_UNR;    // independent column loads in flight per lane (push)
-constexpr int PULL_LANE = 16;    // columns a lane loads at once in a pull scan
-constexpr int PULL_LANE_MAX = 32;  // entries a lane scans alone before the row goes warp-wide
 constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
 constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long M38 = (1ull << 38) - 1;
@@ -219,6 +272,25 @@ __device__ __forceinline__ int owner_search(T key, T x) {
     }
     return lo;
 }
+
+// Per-warp task timer (lane 0 accumulates clock64 spans into the level slot).
+#ifndef DBFS_TASK_TIMERS
+#define DBFS_TASK_TIMERS 0
+#endif
+struct TaskTimer {
+    long long t0;
+    __device__ __forceinline__ void start() {
+        if (DBFS_TASK_TIMERS) t0 = clock64();
+    }
+    __device__ __forceinline__ void stop(LevelSlot &A, int task) {
+        if (!DBFS_TASK_TIMERS) return;
+        long long dt = clock64() - t0;
+        if (lane_id() == 0 && dt > 0) {
+            atomicAdd(&A.tsum[task], (unsigned long long)dt);
+            atomicMax(&A.tmax[task], (unsigned long long)dt);
+        }
+    }
+};
 
 struct VisitCounters {
     unsigned long long fv_nn;       // FV_nn of this level's frontier (activity slot)
@@ -454,35 +526,47 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
 
 // ------------------------------------------------------------------- pulls
 // Early-exit scan (traversal.py:111-139): the first column of row [b, e) whose
-// bit is set in `front`.  A lane loads PULL_LANE columns at once (their bit
-// tests also in flight), and hands rows still unresolved after PULL_LANE_MAX
-// entries to the whole warp (32 * PULL_U columns per step, ballot for order).
+// bit is set in `front`.  A lane scans its row in geometric rounds (loads and
+// bit tests of a round in flight together) and hands rows still unresolved
+// after 30 entries to the whole warp (32 * PULL_U columns per step, ballot).
 
 struct PullRes {
     int64_t pos;  // absolute index of the first hit, or -1
     uint32_t col;
 };
 
+template <int W>
+__device__ __forceinline__ bool lane_round(const uint32_t *__restrict__ col, const uint32_t *__restrict__ front,
+                                           const uint32_t *filt, int64_t &j, int64_t e, PullRes &r) {
+    uint32_t c[W];
+    bool h[W];
+#pragma unroll
+    for (int u = 0; u < W; u++) c[u] = j + u < e ? __ldg(&col[j + u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < W; u++) h[u] = j + u < e && (!filt || coarse_hit(filt, c[u]));
+#pragma unroll
+    for (int u = 0; u < W; u++) h[u] = h[u] && tbit(front, c[u]);
+#pragma unroll
+    for (int u = 0; u < W; u++)
+        if (h[u]) {
+            r.pos = j + u;
+            r.col = c[u];
+            return true;
+        }
+    j += W;
+    return false;
+}
+
+// Geometric rounds (2, 4, 8, 16 entries): a hit near the row start costs two
+// tests, long scans still keep 16 loads in flight.  Returns true when resolved.
 __device__ __forceinline__ bool lane_scan(const uint32_t *__restrict__ col, const uint32_t *__restrict__ front,
-                                          int64_t b, int64_t e, int64_t &j, PullRes &r) {
+                                          const uint32_t *filt, int64_t b, int64_t e, int64_t &j, PullRes &r) {
     j = b;
-    const int64_t stop = b + PULL_LANE_MAX < e ? b + PULL_LANE_MAX : e;
-    while (j < stop) {
-        uint32_t c[PULL_LANE];
-        bool h[PULL_LANE];
-#pragma unroll
-        for (int u = 0; u < PULL_LANE; u++) c[u] = j + u < e ? __ldg(&col[j + u]) : 0u;
-#pragma unroll
-        for (int u = 0; u < PULL_LANE; u++) h[u] = j + u < e && tbit(front, c[u]);
-#pragma unroll
-        for (int u = 0; u < PULL_LANE; u++)
-            if (h[u]) {
-                r.pos = j + u;
-                r.col = c[u];
-                return true;
-            }
-        j += PULL_LANE;
-    }
+    r.pos = -1;
+    if (j < e && lane_round<2>(col, front, filt, j, e, r)) return true;
+    if (j < e && lane_round<4>(col, front, filt, j, e, r)) return true;
+    if (j < e && lane_round<8>(col, front, filt, j, e, r)) return true;
+    if (j < e && lane_round<16>(col, front, filt, j, e, r)) return true;
     if (j >= e) {
         r.pos = -1;
         return true;
@@ -491,7 +575,7 @@ __device__ __forceinline__ bool lane_scan(const uint32_t *__restrict__ col, cons
 }
 
 __device__ __forceinline__ PullRes warp_scan_row(const uint32_t *__restrict__ col, const uint32_t *__restrict__ front,
-                                                 int64_t j, int64_t e) {
+                                                 const uint32_t *filt, int64_t j, int64_t e) {
     const unsigned lane = lane_id();
     PullRes r;
     r.pos = -1;
@@ -505,7 +589,9 @@ __device__ __forceinline__ PullRes warp_scan_row(const uint32_t *__restrict__ co
             c[u] = x < e ? __ldg(&col[x]) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < PULL_U; u++) h[u] = (j + u * 32 + lane < e) && tbit(front, c[u]);
+        for (int u = 0; u < PULL_U; u++) h[u] = (j + u * 32 + lane < e) && (!filt || coarse_hit(filt, c[u]));
+#pragma unroll
+        for (int u = 0; u < PULL_U; u++) h[u] = h[u] && tbit(front, c[u]);
 #pragma unroll
         for (int u = 0; u < PULL_U; u++) {
             unsigned m = __ballot_sync(FULL, h[u]);
@@ -526,8 +612,9 @@ __device__ __forceinline__ PullRes warp_scan_row(const uint32_t *__restrict__ co
 template <class CandF, class HitF>
 __device__ __forceinline__ void pull_kind(int64_t nw, int64_t gw, int64_t TW, uint32_t *list,
                                           const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
-                                          const uint32_t *__restrict__ front, unsigned long long &insp,
-                                          unsigned long long &rows, CandF cand, HitF on_hit) {
+                                          const uint32_t *__restrict__ front, const uint32_t *filt,
+                                          unsigned long long &insp, unsigned long long &rows, CandF cand,
+                                          HitF on_hit) {
     const unsigned lane = lane_id();
     for (int64_t base = gw * 32; base < nw; base += TW * 32) {
         int64_t wi = base + lane;
@@ -543,13 +630,13 @@ __device__ __forceinline__ void pull_kind(int64_t nw, int64_t gw, int64_t TW, ui
             r.pos = -1;
             r.col = 0;
             int64_t j = e;
-            bool done = ok ? lane_scan(col, front, b, e, j, r) : true;
+            bool done = ok ? lane_scan(col, front, filt, b, e, j, r) : true;
             unsigned pend = __ballot_sync(FULL, !done);
             while (pend) {
                 int l = __ffs(pend) - 1;
                 pend &= pend - 1;
                 int64_t jl = __shfl_sync(FULL, j, l), el = __shfl_sync(FULL, e, l);
-                PullRes rr = warp_scan_row(col, front, jl, el);
+                PullRes rr = warp_scan_row(col, front, filt, jl, el);
                 if ((int)lane == l) r = rr;
             }
             if (ok) {
@@ -574,10 +661,14 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     double bv[4];
     unsigned long long cum[4];
     level_dirs(V, C, L, dirs, bv, cum);
+    int ex[4];
+    exec_dirs(V, S, cum, dirs, ex);
     if (wb == 0 && threadIdx.x == 0) {
         for (int k = 0; k < 4; k++) {
             C.dir[L & 1][k] = dirs[k];
             C.cumq[L & 1][k] = cum[k];
+            C.s[L % 3].exec_dir[k] = ex[k];
+            if (k > 0 && ex[k] == FWD) C.s[L % 3].work[k] = S.fv[k];
         }
     }
     VisitCounters vc = {};
@@ -587,12 +678,17 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     const int p = V.p, w = V.w;
     const uint32_t *nfront_cur = V.nfront[L & 1];
 
+    LevelSlot &AT = C.s[L % 3];
+    TaskTimer tt;
     // T1: normal frontier -- nn push (always, engine.py:207-222) + nd push.
+    tt.start();
     if (S.nfront > 0) {
-        const bool nd_fwd = dirs[KIND_ND] == FWD;
+        const bool nd_fwd = ex[KIND_ND] == FWD;
+        const uint32_t *has_nn = V.src_bits[KIND_NN], *has_nd = V.src_bits[KIND_ND];
         for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
             int64_t wi = base + lane;
-            uint32_t word = wi < V.nw_n ? nfront_cur[wi] : 0u;
+            // only frontier vertices with an nn row (or an nd row when nd pushes)
+            uint32_t word = wi < V.nw_n ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
             unsigned cnt = warp_compact(word, wi, list);
             for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
                 unsigned i = g0 + lane;
@@ -611,58 +707,98 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         }
     }
 
+    tt.stop(AT, 0);
     // T2: delegate frontier -- dn / dd push, load balanced over the level's
     // edge space (engine.py:238-263).
-    if (dirs[KIND_DN] == FWD && (S.dpack[0] & M38)) {
+    tt.start();
+    if (ex[KIND_DN] == FWD && (S.dpack[0] & M38)) {
         int64_t cnt = (int64_t)(S.dpack[0] >> 38), total = (int64_t)(S.dpack[0] & M38);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
         list_push<ACT_NORMAL>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1], cnt, total,
                               x0, x1, vc);
     }
-    if (dirs[KIND_DD] == FWD && (S.dpack[1] & M38)) {
+    tt.stop(AT, 1);
+    tt.start();
+    if (ex[KIND_DD] == FWD && (S.dpack[1] & M38)) {
         int64_t cnt = (int64_t)(S.dpack[1] >> 38), total = (int64_t)(S.dpack[1] & M38);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
         list_push<ACT_DELEG>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1], cnt, total,
                              x0, x1, vc);
     }
+    tt.stop(AT, 2);
+
+    // Pull frontiers that are sparse relative to the 2^18-bit coarse filter
+    // are tested in shared memory first (block-uniform decisions).
+    const bool dpull = ex[KIND_DN] == BWD || ex[KIND_DD] == BWD;
+    const bool dfilt = DBFS_FILTER && dpull && (double)S.dfront < 0.7 * FW * 32;
+    const bool nfilt = DBFS_FILTER && ex[KIND_ND] == BWD && (double)S.nfront < 0.7 * FW * 32;
+    if (dfilt) {
+        __syncthreads();
+        const uint32_t *src = V.coarse_d[L & 1];
+        for (int i = threadIdx.x; i < FW; i += BT) sm.filt[i] = __ldcg(&src[i]);
+        __syncthreads();
+    }
+    const uint32_t *filt = dfilt ? sm.filt : nullptr;
 
     // T4: dn pull -- unvisited nd-source normals scan nd rows for frontier
     // delegates (engine.py:242-248).
-    if (dirs[KIND_DN] == BWD) {
+    tt.start();
+    if (ex[KIND_DN] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_ND];
         const uint32_t *nvis = V.nvis;
-        pull_kind(V.nw_n, gw, TW, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, vc.insp_bwd[KIND_DN], vc.pull_rows,
+        pull_kind(V.nw_n, gw, TW, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](uint32_t c, uint32_t x) { claim_normal(V, L, c, __ldg(&V.del_gid[x]), false); });
     }
-    // T5: nd pull -- unvisited dn-source delegates scan dn rows for frontier
-    // normals (engine.py:229-233).
-    if (dirs[KIND_ND] == BWD) {
-        const uint32_t *srcb = V.src_bits[KIND_DN];
-        const uint32_t *dvis = V.dvis;
-        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, vc.insp_bwd[KIND_ND], vc.pull_rows,
-                  [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
-                  [&](uint32_t x, uint32_t c) { find_delegate(V, L, x, (int64_t)c * p + w, vc.dirty); });
-    }
+    tt.stop(AT, 3);
     // T6: dd pull -- unvisited dd-source delegates scan dd rows (engine.py:257-261).
-    if (dirs[KIND_DD] == BWD) {
+    tt.start();
+    if (ex[KIND_DD] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_DD];
         const uint32_t *dvis = V.dvis;
-        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DD], V.col[KIND_DD], V.dfront, vc.insp_bwd[KIND_DD], vc.pull_rows,
+        // reported FORWARD: any scan order finds the same set, so use the rows
+        // sorted by neighbour degree (hubs first); reported BACKWARD: the
+        // reference order, whose early-exit position is the counter.
+        const uint32_t *cdd = (dirs[KIND_DD] == FWD && V.col_sorted_dd) ? V.col_sorted_dd : V.col[KIND_DD];
+        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DD], cdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
                   [&](uint32_t x, uint32_t y) { find_delegate(V, L, x, __ldg(&V.del_gid[y]), vc.dirty); });
     }
-
+    tt.stop(AT, 5);
+    if (nfilt) {
+        __syncthreads();
+        const uint32_t *src = V.coarse_n[L & 1];
+        for (int i = threadIdx.x; i < FW; i += BT) sm.filt[i] = __ldcg(&src[i]);
+        __syncthreads();
+    }
+    // T5: nd pull -- unvisited dn-source delegates scan dn rows for frontier
+    // normals (engine.py:229-233).
+    tt.start();
+    if (ex[KIND_ND] == BWD) {
+        const uint32_t *srcb = V.src_bits[KIND_DN];
+        const uint32_t *dvis = V.dvis;
+        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
+                  vc.insp_bwd[KIND_ND], vc.pull_rows,
+                  [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
+                  [&](uint32_t x, uint32_t c) { find_delegate(V, L, x, (int64_t)c * p + w, vc.dirty); });
+    }
+    tt.stop(AT, 4);
     // flush: one atomic per warp per counter
     LevelSlot &A = C.s[L % 3];
     unsigned long long v;
     v = warp_sum(vc.fv_nn);
-    if (lane == 0) atomic_add_u64(&A.fv[KIND_NN], v);
+    if (lane == 0 && v) {
+        atomicAdd(&A.fv[KIND_NN], v);
+        atomicAdd(&A.work[KIND_NN], v);
+    }
     v = warp_sum(vc.records);
     if (lane == 0) atomic_add_u64(&A.records, v);
     for (int k = 1; k < 4; k++) {
         v = warp_sum(vc.insp_bwd[k]);
-        if (lane == 0) atomic_add_u64(&A.insp_bwd[k], v);
+        if (lane == 0 && v) {
+            if (dirs[k] == BWD) atomicAdd(&A.insp_bwd[k], v);
+            atomicAdd(&A.work[k], v);
+        }
     }
     v = warp_sum(vc.dirty);
     if (lane == 0 && v) atomicOr(&A.dirty, 1ull);
@@ -681,8 +817,8 @@ struct FinishCounters {
 // push-list row lengths.
 __device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, uint64_t &ldn, uint64_t &ldd) {
     const uint32_t xw = x >> 5, xb = x & 31;
-    ldn = (uint64_t)(__ldg(&V.off[KIND_DN][x + 1]) - __ldg(&V.off[KIND_DN][x]));
-    ldd = (uint64_t)(__ldg(&V.off[KIND_DD][x + 1]) - __ldg(&V.off[KIND_DD][x]));
+    ldn = __ldg(&V.deg[KIND_DN][x]);
+    ldd = __ldg(&V.deg[KIND_DD][x]);
     const int64_t gx = V.glevel ? __ldg(&V.del_gid[x]) : 0;
     V.dlevel[x] = L + 1;
     int64_t par = 0x7fffffffffffffffLL;
@@ -723,6 +859,12 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
             V.dfront[wi] = nw;
             if (nw) V.dvis[wi] = dv | nw;
         }
+        {
+            uint32_t fold = nw;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) fold |= __shfl_xor_sync(FULL, fold, o);
+            if (lane == 0 && fold) atomicOr(&V.coarse_d[(L + 1) & 1][(base >> 5) & (FW - 1)], fold);
+        }
         unsigned cnt = warp_compact(nw, wi, list);
         if (!cnt) continue;
         // pass A: state + totals
@@ -759,8 +901,8 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
             unsigned i = g0 + lane;
             uint32_t x = i < cnt ? list[i] : 0u;
-            uint64_t a = i < cnt ? (uint64_t)(__ldg(&V.off[KIND_DN][x + 1]) - __ldg(&V.off[KIND_DN][x])) : 0;
-            uint64_t b = i < cnt ? (uint64_t)(__ldg(&V.off[KIND_DD][x + 1]) - __ldg(&V.off[KIND_DD][x])) : 0;
+            uint64_t a = i < cnt ? (uint64_t)__ldg(&V.deg[KIND_DN][x]) : 0;
+            uint64_t b = i < cnt ? (uint64_t)__ldg(&V.deg[KIND_DD][x]) : 0;
             unsigned t1, t2;
             unsigned long long e1, e2;
             unsigned p1 = warp_excl_scan(a > 0 ? 1u : 0u, &t1);
@@ -809,12 +951,18 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
             if (nw) V.nvis[wi] |= nw;
         }
         if (!__any_sync(FULL, nw != 0u)) continue;
+        {
+            uint32_t fold = nw;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) fold |= __shfl_xor_sync(FULL, fold, o);
+            if (lane == 0) atomicOr(&V.coarse_n[(L + 1) & 1][(base >> 5) & (FW - 1)], fold);
+        }
         unsigned cnt = warp_compact(nw, wi, list);
         for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
             unsigned i = g0 + lane;
             if (i < cnt) {
                 uint32_t c = list[i];
-                int64_t dnd = __ldg(&V.off[KIND_ND][c + 1]) - __ldg(&V.off[KIND_ND][c]);
+                int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
                 fc.nfv_nd += (unsigned long long)dnd;
                 fc.nq_nd += dnd > 0;
                 fc.ncount++;
@@ -864,9 +1012,21 @@ __device__ void phase_finish(const View &V, int L, int wb, int nb, Smem &sm, int
     const int64_t gw = (int64_t)wb * WPB + warp_id(), TW = (int64_t)nb * WPB;
     const int64_t tid = (int64_t)wb * BT + threadIdx.x, nth = (int64_t)nb * BT;
     uint32_t *list = sm.list[warp_id()];
-    if (parts & F_DELEGATES) finish_delegates(V, L, gw, TW, list, fc);
+    TaskTimer tt;
+    if (parts & F_DELEGATES) {
+        for (int64_t i = tid; i < FW; i += nth) V.coarse_d[L & 1][i] = 0u;
+        tt.start();
+        finish_delegates(V, L, gw, TW, list, fc);
+        tt.stop(V.ctl->s[L % 3], 6);
+    }
+    if (parts & F_NORMALS)
+        for (int64_t i = tid; i < FW; i += nth) V.coarse_n[L & 1][i] = 0u;
     if (parts & F_INGEST) finish_ingest(V, L, tid, nth);
-    if (parts & F_NORMALS) finish_normals(V, L, gw, TW, list, fc);
+    if (parts & F_NORMALS) {
+        tt.start();
+        finish_normals(V, L, gw, TW, list, fc);
+        tt.stop(V.ctl->s[L % 3], 7);
+    }
     flush_finish(V, L, fc, wb, (parts & F_DELEGATES) != 0);
 }
 
@@ -883,6 +1043,12 @@ __device__ void phase_init(const View &V, int wb, int nb) {
         V.nvis[i] = 0u;
         V.nfront[0][i] = 0u;
         V.nfront[1][i] = 0u;
+    }
+    for (int64_t i = tid; i < FW; i += nth) {
+        V.coarse_d[0][i] = 0u;
+        V.coarse_d[1][i] = 0u;
+        V.coarse_n[0][i] = 0u;
+        V.coarse_n[1][i] = 0u;
     }
     for (int64_t i = tid; i < V.nw_d; i += nth) {
         V.dvis[i] = 0u;
@@ -901,6 +1067,7 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         V.dlevel[x] = 0;
         V.dvis[x >> 5] |= 1u << (x & 31);
         V.dfront[x >> 5] |= 1u << (x & 31);
+        V.coarse_d[0][(x >> 10) & (FW - 1)] |= 1u << (x & 31);
         if (V.parents) V.dparent[x] = source;
         if (V.glevel) {
             V.glevel[source] = 0;
@@ -929,6 +1096,7 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         if (V.parents) V.nparent[c] = source;
         V.nfront[0][c >> 5] |= 1u << (c & 31);
         V.nvis[c >> 5] |= 1u << (c & 31);
+        V.coarse_n[0][(c >> 10) & (FW - 1)] |= 1u << (c & 31);
         int64_t dnd = V.off[KIND_ND][c + 1] - V.off[KIND_ND][c];
         S.fv[KIND_ND] = dnd;
         S.q[KIND_ND] = dnd > 0;

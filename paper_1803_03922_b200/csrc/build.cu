@@ -316,6 +316,11 @@ __global__ void k_src_bits(const int64_t *__restrict__ off, int64_t rows, uint32
     if (lane_id() == 0 && c) atomicAdd(count, c);
 }
 
+__global__ void k_row_degrees(const int64_t *__restrict__ off, int64_t rows, uint32_t *__restrict__ deg) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+        deg[r] = (uint32_t)(off[r + 1] - off[r]);
+}
+
 __global__ void k_remote_caps_keys(const uint32_t *__restrict__ keys, const uint32_t *__restrict__ vals,
                                    int64_t m, int64_t nn_rows, PDiv pd, int w,
                                    unsigned long long *__restrict__ remote) {
@@ -354,7 +359,7 @@ static void finish_workers(Graph &g, int64_t nkeys, const std::vector<int64_t> &
         DBFS_CUDA(cudaMemcpy(&offs[4], g.off_all.p + W.base[3] + W.rows[3], 8, cudaMemcpyDeviceToHost));
         for (int k = 0; k < 4; k++) W.nnz[k] = offs[k + 1] - offs[k];
         DBFS_CUDA(cudaMemset(dcount, 0, sizeof(unsigned long long) * 4));
-        for (int k = 1; k < 4; k++) {
+        for (int k = 0; k < 4; k++) {
             W.src_bits[k].alloc(std::max<int64_t>(nwords(W.rows[k]), 1));
             DBFS_CUDA(cudaMemsetAsync(W.src_bits[k].p, 0, W.src_bits[k].bytes(), ctx.stream));
             if (W.rows[k] > 0) {
@@ -367,7 +372,18 @@ static void finish_workers(Graph &g, int64_t nkeys, const std::vector<int64_t> &
         unsigned long long hc[4];
         DBFS_CUDA(cudaMemcpyAsync(hc, dcount, sizeof(hc), cudaMemcpyDeviceToHost, ctx.stream));
         DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
-        for (int k = 1; k < 4; k++) W.n_src[k] = (int64_t)hc[k];
+        for (int k = 0; k < 4; k++) W.n_src[k] = (int64_t)hc[k];
+        // compact row lengths: nd per local normal, dn / dd per delegate
+        W.deg[KIND_ND].alloc(std::max<int64_t>(W.rows[KIND_ND], 1));
+        W.deg[KIND_DN].alloc(std::max<int64_t>(W.rows[KIND_DN], 1));
+        W.deg[KIND_DD].alloc(std::max<int64_t>(W.rows[KIND_DD], 1));
+        for (int k = 1; k < 4; k++)
+            if (W.rows[k] > 0) {
+                int blocks = (int)std::min<int64_t>(ceil_div(W.rows[k], 256), ctx.num_sms * 16);
+                k_row_degrees<<<blocks, 256, 0, ctx.stream>>>(g.off_all.p + W.base[k], W.rows[k], W.deg[k].p);
+                DBFS_LAUNCHED();
+            }
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     }
     cudaFree(dcount);
     (void)nkeys;
@@ -710,6 +726,82 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
         g.first_worker = r;
         g.W = 1;
         finish_workers(g, nkeys, wb);
+    }
+}
+
+// ------------------------------------------------- degree-ordered dd rows
+
+__global__ void k_deg_keys(const uint32_t *__restrict__ col, const int64_t *__restrict__ off0, int64_t nnz,
+                           const uint32_t *__restrict__ deg, const int64_t *__restrict__ del_gid,
+                           uint32_t *__restrict__ key, uint32_t *__restrict__ idx) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t dg = deg[del_gid[col[off0[0] + j]]];
+        key[j] = 0xffffffffu - dg;  // descending degree
+        idx[j] = (uint32_t)j;
+    }
+}
+
+__global__ void k_row_ids(const int64_t *__restrict__ off, int64_t rows, uint32_t *__restrict__ rowid) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t b0 = off[0];
+    for (int64_t r = gw; r < rows; r += TW)
+        for (int64_t j = off[r] - b0 + lane_id(); j < off[r + 1] - b0; j += 32) rowid[j] = (uint32_t)r;
+}
+
+__global__ void k_row_keys(const uint32_t *__restrict__ idx, const uint32_t *__restrict__ rowid, int64_t nnz,
+                           uint32_t *__restrict__ key) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+        key[j] = rowid[idx[j]];
+}
+
+__global__ void k_gather_cols(const uint32_t *__restrict__ idx, const uint32_t *__restrict__ col, int64_t base,
+                              int64_t nnz, uint32_t *__restrict__ out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+        out[base + j] = col[base + idx[j]];
+}
+
+// For every local worker: a copy of the dd rows with neighbours ordered by
+// descending degree (two stable radix passes: degree, then row).  Used only
+// by executor pulls of FORWARD-reported dd levels, where scan order is free.
+void build_sorted_dd(Graph &g) {
+    Ctx &ctx = *g.ctx;
+    if (g.col_sorted.n) return;
+    g.col_sorted.alloc(std::max<int64_t>(g.col_all.n, 1));
+    for (auto &W : g.workers) {
+        const int64_t nnz = W.nnz[KIND_DD], rows = W.rows[KIND_DD];
+        if (nnz == 0) continue;
+        DBFS_CHECK(nnz < ((int64_t)1 << 32), DBFS_ECAPACITY, "dd rows exceed 2^32 edges on one worker");
+        const int64_t *off = g.off_all.p + W.base[KIND_DD];
+        int64_t base = 0;
+        DBFS_CUDA(cudaMemcpy(&base, off, 8, cudaMemcpyDeviceToHost));
+        DArray<uint32_t> key, idx, key2, idx2, rowid;
+        key.alloc(nnz);
+        idx.alloc(nnz);
+        key2.alloc(nnz);
+        idx2.alloc(nnz);
+        rowid.alloc(nnz);
+        const int blocks = ctx.num_sms * 16;
+        k_deg_keys<<<blocks, 256, 0, ctx.stream>>>(g.col_all.p, off, nnz, g.degree.p, g.del_gid.p, key.p, idx.p);
+        DBFS_LAUNCHED();
+        bool alt = false;
+        radix_sort_pairs(ctx, key.p, idx.p, key2.p, idx2.p, nnz, 32, &alt);
+        uint32_t *sidx = alt ? idx2.p : idx.p;
+        k_row_ids<<<blocks, 256, 0, ctx.stream>>>(off, rows, rowid.p);
+        DBFS_LAUNCHED();
+        uint32_t *k2 = alt ? key.p : key2.p;   // free key buffer
+        k_row_keys<<<blocks, 256, 0, ctx.stream>>>(sidx, rowid.p, nnz, k2);
+        DBFS_LAUNCHED();
+        // k2 = row of each degree-ordered entry; sort (stable) by row
+        bool alt2 = false;
+        uint32_t *k3 = (k2 == key.p) ? key2.p : key.p;
+        uint32_t *i3 = (sidx == idx.p) ? idx2.p : idx.p;
+        int bits = 1;
+        while (bits < 32 && ((int64_t)1 << bits) < rows) bits++;
+        radix_sort_pairs(ctx, k2, sidx, k3, i3, nnz, bits, &alt2);
+        uint32_t *fidx = alt2 ? i3 : sidx;
+        k_gather_cols<<<blocks, 256, 0, ctx.stream>>>(fidx, g.col_all.p, base, nnz, g.col_sorted.p);
+        DBFS_LAUNCHED();
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     }
 }
 

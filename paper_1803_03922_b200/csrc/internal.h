@@ -32,6 +32,10 @@ struct LevelSlot {
     unsigned long long new_del;      // delegates discovered at the barrier
     unsigned long long inbox;        // records delivered to this worker
     unsigned long long pull_rows;    // reverse rows scanned by pulls at this level
+    unsigned long long work[4];      // inspections actually executed (push: FV, pull: scanned)
+    int exec_dir[4];                 // executed strategy per kind (may differ from the reported one)
+    unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
+    unsigned long long tmax[8];      // per-task warp cycles: max over warps
     unsigned long long send[MAXW];   // records per destination worker
 };
 
@@ -58,6 +62,9 @@ struct IterRec {
     unsigned long long messages;
     unsigned long long new_del;
     unsigned long long rows;         // rows expanded (push) + scanned (pull)
+    unsigned long long work[4];      // executed inspections
+    int exec_dir[4];
+    unsigned long long tsum[8], tmax[8];
     unsigned long long nfront, dfront;
     unsigned long long t[3];         // globaltimer at V start, V end, F end (persistent engine)
     unsigned long long send[MAXW];
@@ -67,6 +74,7 @@ struct IterRec {
 struct View {
     int w, W, p, p_rank, dist;       // global index, local worker count, shape
     int mode, allow_back, parents;
+    int symmetric, exec_policy;      // executor may pull a FORWARD-reported kind (dobfs, symmetric graphs)
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
     int rec_cap;
@@ -75,9 +83,12 @@ struct View {
     int64_t n, n_local, d, nw_n, nw_d;
     double f0[4], f1[4];
     unsigned long long total_src[4]; // |nd_src|, |dn_src|, |dd_src| (index by kind)
+    unsigned long long nnz[4];       // edges per kind on this worker
     const int64_t *off[4];
     const uint32_t *col[4];
-    const uint32_t *src_bits[4];     // [ND] nd sources (n_local bits), [DN] dn, [DD] dd (d bits)
+    const uint32_t *src_bits[4];     // rows present: [NN]/[ND] per local normal, [DN]/[DD] per delegate
+    const uint32_t *deg[4];          // row lengths ([ND], [DN], [DD])
+    const uint32_t *col_sorted_dd;   // dd rows reordered by neighbour degree (executor pulls only)
     const int64_t *del_gid;
     int32_t *nlevel;
     int64_t *nparent;
@@ -85,6 +96,7 @@ struct View {
     int64_t *dparent;
     int64_t *dcand;
     uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
+    uint32_t *coarse_d[2], *coarse_n[2];  // coarse frontier filters by level parity
     uint32_t *dlist[2][2];           // delegate frontier per push kind (0 dn, 1 dd) and parity
     int64_t *dpre[2][2];             // exclusive edge prefix of dlist rows
     uint2 *inbox[2];
@@ -161,10 +173,12 @@ struct WorkerHost {
     int64_t n_src[4] = {0, 0, 0, 0}; // |nd_src| at [ND], |dn_src| at [DN], |dd_src| at [DD]
     int64_t remote_cap[MAXW];        // nn edges on this worker whose column is owned by dest
     DArray<uint32_t> src_bits[4];
+    DArray<uint32_t> deg[4];         // row lengths: [ND] per local normal, [DN]/[DD] per delegate
     // BFS state
     DArray<int32_t> nlevel, dlevel;
     DArray<int64_t> nparent, dparent, dcand;
     DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
+    DArray<uint32_t> coarse;         // 4 x 8192 words: coarse_d[0..1], coarse_n[0..1]
     DArray<uint32_t> dlist[4];       // [kind*2 + parity]
     DArray<int64_t> dpre[4];
     DArray<uint2> inbox0, inbox1, sendbuf;
@@ -180,12 +194,14 @@ struct Graph {
     int p_rank = 1, p_gpu = 1, p = 1;
     int W = 1, first_worker = 0;
     bool dist = false;
+    bool symmetric = false;          // every edge's reverse is present (build_rmat_graph / symmetrize)
     int64_t kind_totals[4] = {0, 0, 0, 0};
     DArray<uint32_t> degree;         // out-degree per global vertex
     DArray<uint32_t> del_id;         // delegate id per global vertex, 0xffffffff for normals
     DArray<int64_t> del_gid;         // delegate global ids (ascending)
     DArray<int64_t> off_all;         // concatenated CSR offsets (absolute)
     DArray<uint32_t> col_all;        // concatenated CSR columns
+    DArray<uint32_t> col_sorted;     // same rows, neighbours by descending degree (dd rows used)
     std::vector<WorkerHost> workers; // local workers
     // BFS engine resources (allocated on first BFS)
     bool bfs_ready = false;
@@ -196,6 +212,9 @@ struct Graph {
     DArray<uint32_t> mask_gather;    // dist: allgather of dnext slices
     DArray<unsigned long long> dist_scratch;
     int rec_cap = 0;
+    double clock_ghz = 0;            // SM clock for cycle -> time conversion of task timers
+    int pgrid = 0;                   // cached cooperative grid of the persistent engine
+    double warps_per_worker = 0;
     // last run
     int64_t last_iterations = 0;
     int64_t last_source = -1;

@@ -51,6 +51,7 @@ class BfsOptions:
     seed: int = 0
     parents: str | None = "any"
     engine: str = "auto"
+    exec_policy: str = "cost"
 
     def __post_init__(self):
         if self.mode not in MODES:
@@ -59,6 +60,8 @@ class BfsOptions:
             raise ValueError(f"parents must be one of {list(PARENT_MODES)}")
         if self.engine not in ENGINES:
             raise ValueError(f"engine must be one of {list(ENGINES)}")
+        if self.exec_policy not in ("cost", "reported"):
+            raise ValueError("exec_policy must be 'cost' or 'reported'")
 
     def to_c(self) -> _lib.BfsOptionsC:
         o = _lib.BfsOptionsC()
@@ -73,6 +76,7 @@ class BfsOptions:
         o.parent_mode = PARENT_MODES[self.parents]
         o.engine = ENGINES[self.engine]
         o.record_iterations = 1
+        o.exec_policy = 1 if self.exec_policy == "cost" else 0
         return o
 
 
@@ -243,9 +247,10 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
     return (levels, par, st) if stats else (levels, par)
 
 
-def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any"):
+def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any",
+               exec_policy: str = "cost"):
     """One BFS leaving depth/parents in device memory (for timing); returns run stats."""
-    return _bfs_raw(pg, BfsOptions(mode=mode, source=int(root), parents=parents), None, None)
+    return _bfs_raw(pg, BfsOptions(mode=mode, source=int(root), parents=parents, exec_policy=exec_policy), None, None)
 
 
 def min_parents(pg: PartitionedGraph) -> np.ndarray:

@@ -241,6 +241,8 @@ def partition_graph(g: EdgeList, theta: int, shape: ClusterShape, verify: bool =
         _lib.check(L.dbfs_graph_build_edges(ctx.handle, src.ctypes.data_as(_lib.vp), dst.ctypes.data_as(_lib.vp),
                                             len(src), int(g.n), int(theta), shape.p_rank, shape.p_gpu,
                                             ctypes.byref(h)), "graph_build_edges")
+    if getattr(g, "symmetric", False):
+        _lib.check(L.dbfs_graph_set_symmetric(h, 1))
     pg = PartitionedGraph(h, ctx, shape)
     if verify and sum(pg.kind_totals.values()) != pg.m:
         raise BucketViolation("edge conservation violated")

@@ -213,3 +213,18 @@ def test_benchmark_api(api):
     pg2 = api.partition_graph(g, 1, api.ClusterShape(2, 1))
     with pytest.raises(api.EmptyReportError):
         api.benchmark(pg2, [4, 5, 6], api.BfsOptions())
+
+
+@pytest.mark.parametrize("scale,theta", [(14, 16), (16, 16), (15, 64)])
+def test_exec_policy_does_not_change_results(api, scale, theta):
+    """Pulling a FORWARD-reported kind (symmetric graphs) must leave every
+    reported output identical to executing the reported directions."""
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=1)), theta, api.ClusterShape(1, 1))
+    rng = np.random.default_rng(scale)
+    for root in rng.integers(0, 1 << scale, size=6):
+        a = api.run_bfs(pg, api.BfsOptions(source=int(root), exec_policy="cost"))
+        b = api.run_bfs(pg, api.BfsOptions(source=int(root), exec_policy="reported"))
+        da, db = a.to_dict(), b.to_dict()
+        for key in ("iterations", "per_iteration", "inspections", "comm", "levels_digest"):
+            assert da[key] == db[key], key
+        assert api.validate_bfs_tree(pg, int(root), a.levels, a.parents) == 0

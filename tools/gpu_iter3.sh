@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gpu_tests.log
+for lib in paper_1803_03922_b200/libdbfs*.so; do DBFS_LIB=$PWD/$lib timeout 300 python tools/sweep.py 24 2>&1 | tail -1; done
+DBFS_LIB=$PWD/paper_1803_03922_b200/libdbfs_timers.so timeout 300 python tools/level_profile.py 24 1 dobfs 2>&1 | head -20
