@@ -146,14 +146,13 @@ def run_ours(args, world, rank, local_rank):
 
         import torch.distributed as tdist
         tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=30))
+    from paper_1803_03922_b200.dist import init_nccl_context, weak_scale
     ctx = _lib.Context(local_rank if dist else args.device)
     _lib.set_default_context(ctx)
     if dist:
-        uid = [_lib.nccl_unique_id() if rank == 0 else None]
-        tdist.broadcast_object_list(uid, src=0)
-        ctx.init_dist(uid[0], world, rank)
+        init_nccl_context(ctx, tdist)
 
-    scale = args.scale + (int(round(math.log2(world))) if (dist and args.scaling == "weak") else 0)
+    scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
     params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40)
     t0 = time.perf_counter()
@@ -316,7 +315,8 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     import oracle as O
-    scale = args.scale + (int(round(math.log2(world))) if (world > 1 and args.scaling == "weak") else 0)
+    from paper_1803_03922_b200.dist import weak_scale
+    scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
     t0 = time.perf_counter()
     og = O.partition_rmat(scale, theta, 1, world, edge_factor=args.edge_factor, load_arrays=False)

@@ -572,6 +572,46 @@ void build_graph_edges(Graph &g, const int64_t *src, const int64_t *dst, int64_t
 // Distributed build: this rank routes its slice [begin,end) of the global edge
 // order, the (key, col) records travel to their owner rank (all-to-all, rank
 // order preserved => global edge order preserved), then a local stable sort.
+// Everything stays in device memory; only p-sized count vectors reach the host.
+__global__ void k_iota(uint32_t *__restrict__ a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
+__global__ void k_pack_records(const uint32_t *__restrict__ idx, const uint32_t *__restrict__ keys,
+                               const uint32_t *__restrict__ vals, int64_t n, uint2 *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t j = idx[i];
+        out[i] = make_uint2(keys[j], vals[j]);
+    }
+}
+
+__global__ void k_count_dest(const uint32_t *__restrict__ dest, int64_t n, unsigned long long *__restrict__ cnt) {
+    __shared__ unsigned long long s[MAXW];
+    for (int i = threadIdx.x; i < MAXW; i += blockDim.x) s[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&s[dest[i]], 1ull);
+    __syncthreads();
+    for (int i = threadIdx.x; i < MAXW; i += blockDim.x)
+        if (s[i]) atomicAdd(&cnt[i], s[i]);
+}
+
+__global__ void k_unpack_records(const uint2 *__restrict__ rec, int64_t n, uint32_t *__restrict__ keys,
+                                 uint32_t *__restrict__ vals, uint32_t *__restrict__ key_cnt, int64_t nn_rows,
+                                 PDiv pd, int self, unsigned long long *__restrict__ remote) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 r = rec[i];
+        keys[i] = r.x;
+        vals[i] = r.y;
+        atomicAdd(&key_cnt[r.x], 1u);
+        if ((int64_t)r.x < nn_rows) {  // nn edge: capacity of remote records to the column's owner
+            int o = pd.mod(r.y);
+            if (o != self) atomicAdd(&remote[o], 1ull);
+        }
+    }
+}
+
 static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) {
     Ctx &ctx = *g.ctx;
     const int p = g.p, r = ctx.rank;
@@ -593,17 +633,36 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
     dwbase.alloc((int64_t)p * 4);
     DBFS_CUDA(cudaMemcpy(dwbase.p, wbase.data(), 8 * p * 4, cudaMemcpyHostToDevice));
     const int64_t ml = end - begin;
-    DArray<uint32_t> dest, keys, vals, dest2, keys2, vals2;
-    dest.alloc(std::max<int64_t>(ml, 1));
-    keys.alloc(std::max<int64_t>(ml, 1));
-    vals.alloc(std::max<int64_t>(ml, 1));
-    DArray<unsigned long long> kt;
+    const int blocks = ctx.num_sms * 16;
+    DArray<unsigned long long> kt, dcnt;
     kt.alloc(4);
+    dcnt.alloc(MAXW);
     DBFS_CUDA(cudaMemsetAsync(kt.p, 0, kt.bytes(), ctx.stream));
-    if (ml > 0) {
-        k_route_dest<<<ctx.num_sms * 16, 256, 0, ctx.stream>>>(es, begin, end, g.degree.p, g.del_id.p, pd,
-                                                               dwbase.p, dest.p, keys.p, vals.p, kt.p);
-        DBFS_LAUNCHED();
+    DBFS_CUDA(cudaMemsetAsync(dcnt.p, 0, dcnt.bytes(), ctx.stream));
+    DArray<uint2> sbuf;
+    sbuf.alloc(std::max<int64_t>(ml, 1));
+    {
+        DArray<uint32_t> dest, keys, vals, idx, dest2, idx2;
+        dest.alloc(std::max<int64_t>(ml, 1));
+        keys.alloc(std::max<int64_t>(ml, 1));
+        vals.alloc(std::max<int64_t>(ml, 1));
+        idx.alloc(std::max<int64_t>(ml, 1));
+        dest2.alloc(std::max<int64_t>(ml, 1));
+        idx2.alloc(std::max<int64_t>(ml, 1));
+        if (ml > 0) {
+            k_route_dest<<<blocks, 256, 0, ctx.stream>>>(es, begin, end, g.degree.p, g.del_id.p, pd, dwbase.p, dest.p,
+                                                         keys.p, vals.p, kt.p);
+            DBFS_LAUNCHED();
+            k_count_dest<<<blocks, 256, 0, ctx.stream>>>(dest.p, ml, dcnt.p);
+            DBFS_LAUNCHED();
+            k_iota<<<blocks, 256, 0, ctx.stream>>>(idx.p, ml);
+            DBFS_LAUNCHED();
+            bool alt = false;  // stable bucket by destination (edge order kept inside a bucket)
+            radix_sort_pairs(ctx, dest.p, idx.p, dest2.p, idx2.p, ml, std::max(1, bits_for(p)), &alt);
+            k_pack_records<<<blocks, 256, 0, ctx.stream>>>(alt ? idx2.p : idx.p, keys.p, vals.p, ml, sbuf.p);
+            DBFS_LAUNCHED();
+        }
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     }
     // global kind totals
     {
@@ -617,116 +676,75 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
         DBFS_CUDA(cudaMemcpy(hv, t.p, sizeof(hv), cudaMemcpyDeviceToHost));
         for (int k = 0; k < 4; k++) g.kind_totals[k] = hv[k];
     }
-    // stable bucket by destination: pack (key, col) pairs as 64-bit values
-    dest2.alloc(std::max<int64_t>(ml, 1));
-    keys2.alloc(std::max<int64_t>(ml, 1));
-    vals2.alloc(std::max<int64_t>(ml, 1));
-    std::vector<int64_t> scount(p, 0);
+    // counts exchange, then the record all-to-all
+    std::vector<int64_t> scount(p);
     {
-        // two stable sorts carrying key and val each with dest as the sort key
-        DBFS_CUDA(cudaMemcpyAsync(dest2.p, dest.p, 4 * ml, cudaMemcpyDeviceToDevice, ctx.stream));
-        bool alt = false;
-        int bits = std::max(1, bits_for(p));
-        DArray<uint32_t> tmpk;
-        tmpk.alloc(std::max<int64_t>(ml, 1));
-        radix_sort_pairs(ctx, dest.p, keys.p, tmpk.p, keys2.p, ml, bits, &alt);
-        uint32_t *sk = alt ? keys2.p : keys.p;
-        bool alt2 = false;
-        radix_sort_pairs(ctx, dest2.p, vals.p, tmpk.p, vals2.p, ml, bits, &alt2);
-        uint32_t *sv = alt2 ? vals2.p : vals.p;
-        uint32_t *sd = alt2 ? tmpk.p : dest2.p;
-        // per-destination counts from the sorted destinations
-        std::vector<uint32_t> hd(ml);
-        if (ml) DBFS_CUDA(cudaMemcpy(hd.data(), sd, 4 * ml, cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < ml; i++) scount[hd[i]]++;
-        // interleave (key, col) into 8-byte records
-        std::vector<uint32_t> hk(ml), hv(ml);
-        if (ml) {
-            DBFS_CUDA(cudaMemcpy(hk.data(), sk, 4 * ml, cudaMemcpyDeviceToHost));
-            DBFS_CUDA(cudaMemcpy(hv.data(), sv, 4 * ml, cudaMemcpyDeviceToHost));
-        }
-        std::vector<uint2> rec(ml);
-        for (int64_t i = 0; i < ml; i++) rec[i] = make_uint2(hk[i], hv[i]);
-        dest.release();
-        dest2.release();
-        keys2.release();
-        vals2.release();
-        tmpk.release();
-        keys.alloc(1);
-        vals.alloc(1);
-        // counts exchange
-        DArray<int64_t> sc, rc;
-        sc.alloc((int64_t)p * p);
-        rc.alloc((int64_t)p * p);
-        DBFS_CUDA(cudaMemcpy(sc.p, scount.data(), 8 * p, cudaMemcpyHostToDevice));
-        nccl_allgather_bytes(ctx, sc.p, rc.p, 8 * p);
-        std::vector<int64_t> all((size_t)p * p);
-        DBFS_CUDA(cudaMemcpy(all.data(), rc.p, 8 * p * p, cudaMemcpyDeviceToHost));
-        std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
-        int64_t acc = 0, racc = 0;
-        for (int o = 0; o < p; o++) {
-            soff[o] = acc * 8;
-            sbytes[o] = scount[o] * 8;
-            acc += scount[o];
-            int64_t c = all[(size_t)o * p + r];  // records rank o sends to me
-            roff[o] = racc * 8;
-            rbytes[o] = c * 8;
-            racc += c;
-        }
-        DArray<uint2> sbuf, rbuf;
-        sbuf.alloc(std::max<int64_t>(ml, 1));
-        rbuf.alloc(std::max<int64_t>(racc, 1));
-        if (ml) DBFS_CUDA(cudaMemcpy(sbuf.p, rec.data(), 8 * ml, cudaMemcpyHostToDevice));
-        nccl_alltoallv_bytes(ctx, sbuf.p, soff.data(), sbytes.data(), rbuf.p, roff.data(), rbytes.data());
-        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
-        // unpack received (key, col) in source-rank order == global edge order
-        std::vector<uint2> rr(racc);
-        if (racc) DBFS_CUDA(cudaMemcpy(rr.data(), rbuf.p, 8 * racc, cudaMemcpyDeviceToHost));
-        std::vector<uint32_t> rk(racc), rv(racc);
-        for (int64_t i = 0; i < racc; i++) {
-            rk[i] = rr[i].x;
-            rv[i] = rr[i].y;
-        }
-        // local CSR
-        g.workers.clear();
-        g.workers.resize(1);
-        WorkerHost &me = g.workers[0];
-        me.w = r;
-        me.n_local = n_local_of(n, p, r);
-        int64_t nkeys = 2 * me.n_local + 2 * d;
-        DArray<uint32_t> kk, kk2, vv2, cnt;
-        kk.alloc(std::max<int64_t>(racc, 1));
-        g.col_all.alloc(std::max<int64_t>(racc, 1));
-        kk2.alloc(std::max<int64_t>(racc, 1));
-        vv2.alloc(std::max<int64_t>(racc, 1));
-        if (racc) {
-            DBFS_CUDA(cudaMemcpy(kk.p, rk.data(), 4 * racc, cudaMemcpyHostToDevice));
-            DBFS_CUDA(cudaMemcpy(g.col_all.p, rv.data(), 4 * racc, cudaMemcpyHostToDevice));
-        }
-        // histogram of keys -> offsets
-        std::vector<uint32_t> hist(std::max<int64_t>(nkeys, 1), 0);
-        for (int64_t i = 0; i < racc; i++) hist[rk[i]]++;
-        cnt.alloc(std::max<int64_t>(nkeys, 1));
-        DBFS_CUDA(cudaMemcpy(cnt.p, hist.data(), 4 * std::max<int64_t>(nkeys, 1), cudaMemcpyHostToDevice));
-        g.off_all.alloc(nkeys + 1);
-        exclusive_scan_u32_to_i64(ctx, cnt.p, g.off_all.p, nkeys);
-        // remote caps for nn records
-        for (int o = 0; o < MAXW; o++) me.remote_cap[o] = 0;
-        for (int64_t i = 0; i < racc; i++)
-            if ((int64_t)rk[i] < me.n_local) {
-                int o = (int)pd.mod(rv[i]);
-                if (o != r) me.remote_cap[o]++;
-            }
-        bool alt3 = false;
-        radix_sort_pairs(ctx, kk.p, g.col_all.p, kk2.p, vv2.p, racc, bits_for(nkeys), &alt3);
-        if (alt3 && racc)
-            DBFS_CUDA(cudaMemcpy(g.col_all.p, vv2.p, 4 * racc, cudaMemcpyDeviceToDevice));
-        std::vector<int64_t> wb = {wbase[(size_t)r * 4 + 0], wbase[(size_t)r * 4 + 1], wbase[(size_t)r * 4 + 2],
-                                   wbase[(size_t)r * 4 + 3]};
-        g.first_worker = r;
-        g.W = 1;
-        finish_workers(g, nkeys, wb);
+        std::vector<unsigned long long> h(MAXW);
+        DBFS_CUDA(cudaMemcpy(h.data(), dcnt.p, 8 * MAXW, cudaMemcpyDeviceToHost));
+        for (int o = 0; o < p; o++) scount[o] = (int64_t)h[o];
     }
+    DArray<int64_t> sc, rc;
+    sc.alloc(p);
+    rc.alloc((int64_t)p * p);
+    DBFS_CUDA(cudaMemcpy(sc.p, scount.data(), 8 * p, cudaMemcpyHostToDevice));
+    nccl_allgather_bytes(ctx, sc.p, rc.p, 8 * p);
+    std::vector<int64_t> all((size_t)p * p);
+    DBFS_CUDA(cudaMemcpy(all.data(), rc.p, 8 * p * p, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
+    int64_t acc = 0, racc = 0;
+    for (int o = 0; o < p; o++) {
+        soff[o] = acc * 8;
+        sbytes[o] = scount[o] * 8;
+        acc += scount[o];
+        int64_t c = all[(size_t)o * p + r];  // records rank o sends to me
+        roff[o] = racc * 8;
+        rbytes[o] = c * 8;
+        racc += c;
+    }
+    DArray<uint2> rbuf;
+    rbuf.alloc(std::max<int64_t>(racc, 1));
+    nccl_alltoallv_bytes(ctx, sbuf.p, soff.data(), sbytes.data(), rbuf.p, roff.data(), rbytes.data());
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    sbuf.release();
+    // local CSR from the received records (source-rank order == global edge order)
+    g.workers.clear();
+    g.workers.resize(1);
+    WorkerHost &me = g.workers[0];
+    me.w = r;
+    me.n_local = n_local_of(n, p, r);
+    const int64_t nkeys = 2 * me.n_local + 2 * d;
+    DBFS_CHECK(nkeys < ((int64_t)1 << 32), DBFS_ECAPACITY, "local row space exceeds 32 bits");
+    DArray<uint32_t> kk, kk2, vv2, cnt;
+    DArray<unsigned long long> remote;
+    kk.alloc(std::max<int64_t>(racc, 1));
+    kk2.alloc(std::max<int64_t>(racc, 1));
+    vv2.alloc(std::max<int64_t>(racc, 1));
+    cnt.alloc(std::max<int64_t>(nkeys, 1));
+    remote.alloc(MAXW);
+    g.col_all.alloc(std::max<int64_t>(racc, 1));
+    DBFS_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), ctx.stream));
+    DBFS_CUDA(cudaMemsetAsync(remote.p, 0, remote.bytes(), ctx.stream));
+    if (racc) {
+        k_unpack_records<<<blocks, 256, 0, ctx.stream>>>(rbuf.p, racc, kk.p, g.col_all.p, cnt.p, me.n_local, pd, r,
+                                                         remote.p);
+        DBFS_LAUNCHED();
+    }
+    rbuf.release();
+    g.off_all.alloc(nkeys + 1);
+    exclusive_scan_u32_to_i64(ctx, cnt.p, g.off_all.p, nkeys);
+    {
+        std::vector<unsigned long long> h(MAXW);
+        DBFS_CUDA(cudaMemcpy(h.data(), remote.p, 8 * MAXW, cudaMemcpyDeviceToHost));
+        for (int o = 0; o < MAXW; o++) me.remote_cap[o] = (int64_t)h[o];
+    }
+    bool alt3 = false;
+    radix_sort_pairs(ctx, kk.p, g.col_all.p, kk2.p, vv2.p, racc, bits_for(nkeys), &alt3);
+    if (alt3 && racc) DBFS_CUDA(cudaMemcpy(g.col_all.p, vv2.p, 4 * racc, cudaMemcpyDeviceToDevice));
+    std::vector<int64_t> wb = {wbase[(size_t)r * 4 + 0], wbase[(size_t)r * 4 + 1], wbase[(size_t)r * 4 + 2],
+                               wbase[(size_t)r * 4 + 3]};
+    g.first_worker = r;
+    g.W = 1;
+    finish_workers(g, nkeys, wb);
 }
 
 // ------------------------------------------------- degree-ordered dd rows

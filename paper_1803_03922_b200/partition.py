@@ -235,8 +235,8 @@ def partition_graph(g: EdgeList, theta: int, shape: ClusterShape, verify: bool =
         src = np.ascontiguousarray(g.src, dtype=np.int64)
         dst = np.ascontiguousarray(g.dst, dtype=np.int64)
         if ctx.nranks > 1:  # each rank passes its contiguous slice of the edge order
-            per = -(-len(src) // ctx.nranks)
-            lo, hi = min(len(src), per * ctx.rank), min(len(src), per * (ctx.rank + 1))
+            from .dist import edge_slice
+            lo, hi = edge_slice(len(src), ctx.nranks, ctx.rank)
             src, dst = src[lo:hi].copy(), dst[lo:hi].copy()
         _lib.check(L.dbfs_graph_build_edges(ctx.handle, src.ctypes.data_as(_lib.vp), dst.ctypes.data_as(_lib.vp),
                                             len(src), int(g.n), int(theta), shape.p_rank, shape.p_gpu,
