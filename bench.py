@@ -225,7 +225,8 @@ def run_ours(args, world, rank, local_rank):
     kernel_ms = float(np.mean(dev_ms))
     achieved = st_mean_bytes / (kernel_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _ncu_traffic(), "peak_source": peaks["source"],
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None if dist else _ncu_traffic(),
+            "peak_source": peaks["source"],
             "kernel": "k_bfs_persistent" if not dist else "k_visit+k_finish",
             "alg_bytes_per_launch": st_mean_bytes}
 

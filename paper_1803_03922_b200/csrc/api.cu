@@ -99,7 +99,7 @@ int32_t dbfs_ctx_create(int32_t device, dbfs_ctx **out) {
         DBFS_CUDA(cudaGetDeviceProperties(&prop, device));
         DBFS_CHECK(prop.major >= 10, DBFS_ECUDA, "libdbfs is built for sm_100a (B200)");
         c->c.num_sms = prop.multiProcessorCount;
-        DBFS_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        DBFS_CUDA(cudaStreamCreate(&c->c.stream));  // blocking: legacy-stream cudaMemcpy orders after it
         DBFS_CUDA(cudaEventCreate(&c->c.ev0));
         DBFS_CUDA(cudaEventCreate(&c->c.ev1));
         *out = c;

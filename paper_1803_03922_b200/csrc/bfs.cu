@@ -158,7 +158,10 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 // --------------------------------------------------------------- resources
 
 
-Graph::~Graph() {}
+Graph::~Graph() {
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_status) cudaFreeHost(h_status);
+}
 
 int32_t *Graph::levels_dev() { return (p == 1 && !dist) ? workers[0].nlevel.p : glevel.p; }
 int64_t *Graph::parents_dev() { return (p == 1 && !dist) ? workers[0].nparent.p : gparent.p; }
@@ -314,7 +317,11 @@ static void ensure_resources(Graph &g) {
     }
     g.views.alloc(W);
     DBFS_CUDA(cudaMemcpy(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice));
-    g.dist_scratch.alloc(64);
+    g.dist_scratch.alloc(2 * (int64_t)(g.p + 3) * (g.p + 1) + 64);
+    if (!g.h_ctl) {
+        DBFS_CUDA(cudaHostAlloc((void **)&g.h_ctl, sizeof(Ctl), cudaHostAllocDefault));
+        DBFS_CUDA(cudaHostAlloc((void **)&g.h_status, 8 * ((size_t)(g.p + 3) * g.p + 8), cudaHostAllocDefault));
+    }
     g.bfs_ready = true;
     (void)ctx;
 }
@@ -360,45 +367,68 @@ static AsmArgs make_asm(Graph &g, bool parents) {
 
 // --------------------------------------------------------------- dist glue
 
-// NCCL exchange between V(L) and F(L) for one rank: delegate masks
-// (all-gather of d/8 bytes, OR-folded in F) and the alltoallv of nn records.
-static void dist_exchange(Graph &g, int L, std::vector<unsigned long long> &send_counts) {
+// Status vector of one rank at level L: records per destination (level L),
+// then the termination inputs of level L-1: records(L-1), |frontier normals at
+// L| (counted in F(L-1)) and the delegates found at L-1.
+__global__ void k_pack_status(const Ctl *__restrict__ c, int L, int p, int64_t *__restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const LevelSlot &A = c->s[L % 3];
+    for (int o = 0; o < p; o++) out[o] = (int64_t)A.send[o];
+    const LevelSlot &P = c->s[(L + 2) % 3];  // level L-1
+    out[p] = L > 0 ? (int64_t)P.records : 0;
+    out[p + 1] = (int64_t)A.nfront;
+    out[p + 2] = L > 0 ? (int64_t)P.new_del : 0;
+}
+
+// One level of the one-worker-per-process engine: a single host sync per level.
+static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     Ctx &ctx = *g.ctx;
     WorkerHost &Wk = g.workers[0];
-    const int p = g.p;
+    const int p = g.p, me = ctx.rank;
     const int64_t nw_d = std::max<int64_t>(nwords(g.d), 1);
+    k_visit<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, 1, L);
+    DBFS_LAUNCHED();
+    const int S = p + 3;
+    int64_t *st_dev = (int64_t *)g.dist_scratch.p;
+    int64_t *st_all = st_dev + S;
+    k_pack_status<<<1, 32, 0, ctx.stream>>>(Wk.ctl.p, L, p, st_dev);
+    DBFS_LAUNCHED();
+    nccl_allgather_bytes(ctx, st_dev, st_all, 8 * S);
     uint32_t *own = (L & 1) ? Wk.dnext1.p : Wk.dnext0.p;
     nccl_allgather_bytes(ctx, own, g.mask_gather.p, nw_d * 4);
-    // send counts of this level (slot L%3)
-    Ctl hc;
-    DBFS_CUDA(cudaMemcpyAsync(&hc, Wk.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+    DBFS_CUDA(cudaMemcpyAsync(g.h_status, st_all, 8 * S * p, cudaMemcpyDeviceToHost, ctx.stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
-    const LevelSlot &A = hc.s[L % 3];
-    send_counts.assign(A.send, A.send + MAXW);
-    std::vector<int64_t> mine(p);
-    for (int o = 0; o < p; o++) mine[o] = (int64_t)A.send[o];
-    DArray<int64_t> s, r;
-    s.alloc(p);
-    r.alloc((int64_t)p * p);
-    DBFS_CUDA(cudaMemcpy(s.p, mine.data(), 8 * p, cudaMemcpyHostToDevice));
-    nccl_allgather_bytes(ctx, s.p, r.p, 8 * p);
-    std::vector<int64_t> all((size_t)p * p);
-    DBFS_CUDA(cudaMemcpy(all.data(), r.p, 8 * p * p, cudaMemcpyDeviceToHost));
+    const int64_t *all = g.h_status;
+    if (L > 0) {
+        // termination of level L-1 (engine.py:303-306), decided globally
+        int64_t act = all[0 * S + p + 2];  // new delegates (identical on every rank)
+        for (int r = 0; r < p; r++) act += all[r * S + p] + all[r * S + p + 1];
+        IterRec rr{};
+        make_record(g.views_h[0], *g.h_ctl, L - 1, rr);
+        if (L - 1 < g.rec_cap) recs.push_back(rr);
+        if (!act) return false;  // level L was speculative: nothing ran on an empty frontier
+    }
     std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
     int64_t racc = 0;
     for (int o = 0; o < p; o++) {
         soff[o] = Wk.send_off[o] * 8;
-        sbytes[o] = o == ctx.rank ? 0 : mine[o] * 8;
-        int64_t c = o == ctx.rank ? 0 : all[(size_t)o * p + ctx.rank];
+        sbytes[o] = o == me ? 0 : all[me * S + o] * 8;
+        int64_t c = o == me ? 0 : all[o * S + me];
         roff[o] = racc * 8;
         rbytes[o] = c * 8;
         racc += c;
     }
     uint2 *inbox = (L & 1) ? Wk.inbox1.p : Wk.inbox0.p;
     nccl_alltoallv_bytes(ctx, Wk.sendbuf.p, soff.data(), sbytes.data(), inbox, roff.data(), rbytes.data());
-    unsigned long long rin = (unsigned long long)racc;
-    DBFS_CUDA(cudaMemcpyAsync(&Wk.ctl.p->s[L % 3].inbox, &rin, 8, cudaMemcpyHostToDevice, ctx.stream));
-    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    g.h_status[S * p] = racc;
+    DBFS_CUDA(cudaMemcpyAsync(&Wk.ctl.p->s[L % 3].inbox, &g.h_status[S * p], 8, cudaMemcpyHostToDevice, ctx.stream));
+    k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, 1, L, F_DELEGATES | F_INGEST);
+    DBFS_LAUNCHED();
+    k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, 1, L, F_NORMALS);
+    DBFS_LAUNCHED();
+    // the control block after F(L) is what level L's record is made from
+    DBFS_CUDA(cudaMemcpyAsync(g.h_ctl, Wk.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+    return true;
 }
 
 // ------------------------------------------------------------------ driver
@@ -484,19 +514,21 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         DBFS_LAUNCHED();
         k_seed<<<W, 32, 0, ctx.stream>>>(g.views.p, W, o.source, src_del);
         DBFS_LAUNCHED();
-        std::vector<unsigned long long> sc;
         std::vector<Ctl> hc(W);
         int L = 0;
-        for (;; L++) {
+        if (g.dist) {
+            std::vector<IterRec> recs;
+            for (L = 0;; L++)
+                if (!dist_level(g, L, grid, recs)) break;
+            iterations = L;
+            for (size_t i = 0; i < recs.size(); i++)
+                DBFS_CUDA(cudaMemcpyAsync(g.workers[0].rec.p + i, &recs[i], sizeof(IterRec), cudaMemcpyHostToDevice,
+                                          ctx.stream));
+        }
+        for (; !g.dist; L++) {
             k_visit<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L);
             DBFS_LAUNCHED();
-            if (g.dist) dist_exchange(g, L, sc);
-            if (g.dist) {
-                k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_INGEST);
-                DBFS_LAUNCHED();
-                k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_NORMALS);
-                DBFS_LAUNCHED();
-            } else {
+            {
                 k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, W, L, F_DELEGATES | F_NORMALS);
                 DBFS_LAUNCHED();
             }
@@ -514,47 +546,13 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
             }
             unsigned long long act = hc[0].s[L % 3].new_del;
             for (int i = 0; i < W; i++) act += hc[i].s[(L + 1) % 3].nfront + hc[i].s[L % 3].records;
-            if (g.dist) {
-                int64_t *buf = (int64_t *)g.dist_scratch.p;
-                int64_t v = (int64_t)act;
-                DBFS_CUDA(cudaMemcpyAsync(buf, &v, 8, cudaMemcpyHostToDevice, ctx.stream));
-                nccl_allreduce_i64(ctx, buf, 1, 0);
-                DBFS_CUDA(cudaMemcpyAsync(&v, buf, 8, cudaMemcpyDeviceToHost, ctx.stream));
-                DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
-                act = (unsigned long long)v;
-            }
             if (!act) break;
         }
-        iterations = L + 1;
+        if (!g.dist) iterations = L + 1;
         if (g.dist) {
             // delegate parents: each rank holds its own candidates -> min over ranks
             if (parents && g.d) nccl_allreduce_i64(ctx, g.workers[0].dparent.p, g.d, 1);
-            // gather every rank's normal levels/parents, then assemble the global arrays
-            WorkerHost &Wk = g.workers[0];
-            int64_t stride = ceil_div(g.n, g.p);
-            DArray<int32_t> lv;
-            DArray<int64_t> pv;
-            lv.alloc(stride * g.p);
-            pv.alloc(stride * g.p);
-            DArray<int32_t> mylv;
-            DArray<int64_t> mypv;
-            mylv.alloc(stride);
-            mypv.alloc(stride);
-            DBFS_CUDA(cudaMemsetAsync(mylv.p, 0xff, 4 * stride, ctx.stream));
-            DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, 8 * stride, ctx.stream));
-            if (Wk.n_local) {
-                DBFS_CUDA(cudaMemcpyAsync(mylv.p, Wk.nlevel.p, 4 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
-                DBFS_CUDA(cudaMemcpyAsync(mypv.p, Wk.nparent.p, 8 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
-            }
-            nccl_allgather_bytes(ctx, mylv.p, lv.p, 4 * stride);
-            if (parents) nccl_allgather_bytes(ctx, mypv.p, pv.p, 8 * stride);
-            for (int w = 0; w < g.p; w++) {
-                aa.nlevel[w] = lv.p + (int64_t)w * stride;
-                aa.nparent[w] = pv.p + (int64_t)w * stride;
-            }
-            k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
-            DBFS_LAUNCHED();
-            DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+            g.assembled = false;  // outputs stay distributed until fetched (dist_assemble)
         } else if (assemble) {
             k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
             DBFS_LAUNCHED();
@@ -646,6 +644,39 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
 
 // ----------------------------------------------------------------- results
 
+// Distributed runs keep each rank's normals local (plus the replicated
+// delegates); the global depth/parent arrays are gathered only on demand.
+static void dist_assemble(Graph &g) {
+    if (!g.dist || g.assembled) return;
+    Ctx &ctx = *g.ctx;
+    const bool parents = g.last_parent_mode != 0;
+    AsmArgs aa = make_asm(g, parents);
+    WorkerHost &Wk = g.workers[0];
+    int64_t stride = ceil_div(g.n, g.p);
+    DArray<int32_t> lv, mylv;
+    DArray<int64_t> pv, mypv;
+    lv.alloc(stride * g.p);
+    pv.alloc(stride * g.p);
+    mylv.alloc(stride);
+    mypv.alloc(stride);
+    DBFS_CUDA(cudaMemsetAsync(mylv.p, 0xff, 4 * stride, ctx.stream));
+    DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, 8 * stride, ctx.stream));
+    if (Wk.n_local) {
+        DBFS_CUDA(cudaMemcpyAsync(mylv.p, Wk.nlevel.p, 4 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
+        DBFS_CUDA(cudaMemcpyAsync(mypv.p, Wk.nparent.p, 8 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    nccl_allgather_bytes(ctx, mylv.p, lv.p, 4 * stride);
+    if (parents) nccl_allgather_bytes(ctx, mypv.p, pv.p, 8 * stride);
+    for (int w = 0; w < g.p; w++) {
+        aa.nlevel[w] = lv.p + (int64_t)w * stride;
+        aa.nparent[w] = pv.p + (int64_t)w * stride;
+    }
+    k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
+    DBFS_LAUNCHED();
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    g.assembled = true;
+}
+
 __global__ void k_count_reached(const int32_t *__restrict__ lv, int64_t n, unsigned long long *out) {
     unsigned long long c = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -657,6 +688,7 @@ __global__ void k_count_reached(const int32_t *__restrict__ lv, int64_t n, unsig
 void fetch_result(Graph &g, int32_t *levels, int64_t *parents) {
     DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
     Ctx &ctx = *g.ctx;
+    dist_assemble(g);
     if (levels) DBFS_CUDA(cudaMemcpyAsync(levels, g.levels_dev(), 4 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
     if (parents) {
         DBFS_CHECK(g.last_parent_mode != 0, DBFS_EINVAL, "last BFS ran without parents");
@@ -720,6 +752,7 @@ static EdgeWalk walk_of(Graph &g, WorkerHost &Wk, int k) {
 void min_parents(Graph &g, int64_t *out) {
     DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
     Ctx &ctx = *g.ctx;
+    dist_assemble(g);
     DArray<unsigned long long> par;
     par.alloc(std::max<int64_t>(g.n, 1));
     const int32_t *lv = g.levels_dev();
@@ -800,6 +833,7 @@ int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *paren
         lv = lvh.p;
     } else {
         DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+        dist_assemble(g);
         lv = g.levels_dev();
     }
     if (parents) {
@@ -808,6 +842,7 @@ int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *paren
         pa = pah.p;
     } else {
         DBFS_CHECK(g.last_valid && g.last_parent_mode != 0, DBFS_EINVAL, "no parents on device");
+        dist_assemble(g);
         pa = g.parents_dev();
     }
     DArray<uint8_t> ok;

@@ -211,6 +211,8 @@ struct Graph {
     DArray<int64_t> gparent;
     DArray<uint32_t> mask_gather;    // dist: allgather of dnext slices
     DArray<unsigned long long> dist_scratch;
+    Ctl *h_ctl = nullptr;            // pinned host mirrors for the distributed level loop
+    int64_t *h_status = nullptr;
     int rec_cap = 0;
     double clock_ghz = 0;            // SM clock for cycle -> time conversion of task timers
     int pgrid = 0;                   // cached cooperative grid of the persistent engine
@@ -220,6 +222,7 @@ struct Graph {
     int64_t last_source = -1;
     int last_parent_mode = 0;
     bool last_valid = false;
+    bool assembled = true;           // dist: global outputs gathered for the last run
     bool last_truncated = false;
     std::vector<IterRec> last_rec;   // [iteration][local worker]
     std::vector<std::vector<unsigned long long>> last_send_matrix;

@@ -1,0 +1,52 @@
+"""torchrun check of the one-worker-per-GPU NCCL path against the oracle.
+
+  torchrun --nproc-per-node N tools/dist_check.py [scale]
+"""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datetime
+import numpy as np
+import torch.distributed as tdist
+
+import paper_1803_03922_b200 as api
+from paper_1803_03922_b200 import _lib
+from paper_1803_03922_b200.dist import env_world, init_nccl_context
+from paper_1803_03922_b200.engine import BfsOptions, _bfs_raw, levels_digest
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+world, rank, local = env_world()
+tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
+ctx = _lib.Context(local)
+_lib.set_default_context(ctx)
+init_nccl_context(ctx, tdist)
+t0 = time.time()
+pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40)), 16,
+                         api.ClusterShape(1, world), ctx=ctx)
+ctx.barrier()
+if rank == 0:
+    print(f"built s{scale} on {world} GPUs in {time.time()-t0:.2f}s kinds {pg.kind_totals} d {pg.classification.d}",
+          flush=True)
+roots = [1, 77, 4242 % (1 << scale), 9999 % (1 << scale)]
+res = []
+for mode in ("dobfs", "bfs"):
+    for r in roots:
+        lv = np.empty(pg.n, dtype=np.int32)
+        pa = np.empty(pg.n, dtype=np.int64)
+        st = _bfs_raw(pg, BfsOptions(mode=mode, source=r), lv, pa)
+        bad = api.validate_bfs_tree(pg, r)
+        res.append((mode, r, levels_digest(lv), st.iterations,
+                    [[int(st.inspections[k][0]), int(st.inspections[k][1])] for k in range(4)], bad, st.device_ms))
+ok = True
+if rank == 0:
+    import oracle as O
+    og = O.partition_rmat(scale, 16, 1, world)
+    for mode, r, dg, it, insp, bad, ms in res:
+        ref = O.run_bfs(og, r, mode=mode)
+        ri = [[ref["inspections"][k]["forward"], ref["inspections"][k]["backward"]] for k in ("nn", "nd", "dn", "dd")]
+        good = dg == ref["levels_digest"] and it == ref["iterations"] and insp == ri and bad == 0
+        ok &= good
+        print(f"{mode} root {r}: digest {'OK' if dg == ref['levels_digest'] else 'MISMATCH'} iters {it}/{ref['iterations']}"
+              f" insp {'OK' if insp == ri else (insp, ri)} certificate {bad} device {ms:.2f} ms", flush=True)
+    print("DIST CHECK", "PASS" if ok else "FAIL", flush=True)
+tdist.barrier()
+tdist.destroy_process_group()
