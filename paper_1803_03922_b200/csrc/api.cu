@@ -309,11 +309,6 @@ int32_t dbfs_bfs(dbfs_graph *gg, const dbfs_bfs_options *opts, int32_t *levels_o
         run_bfs(g, *opts, stats);
         if (levels_out || parents_out) fetch_result(g, levels_out, parents_out);
         if (stats) stats->d2h_bytes += (levels_out ? 4 * g.n : 0) + (parents_out ? 8 * g.n : 0);
-        if (stats && levels_out) {
-            int64_t r = 0;
-            for (int64_t i = 0; i < g.n; i++) r += levels_out[i] >= 0;
-            stats->reached = r;
-        }
     });
 }
 
@@ -335,7 +330,7 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
         memset(&r, 0, sizeof(r));
         r.iteration = it;
         bool any_new = false;
-        int64_t records = 0, msgs = 0;
+        int64_t records = 0, msgs = 0, uq_records = 0;
         // send matrix [sender][dest] for message accounting
         std::vector<int64_t> cnt((size_t)g.p * g.p, 0);
         for (int i = 0; i < W; i++) {
@@ -360,6 +355,7 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
                 if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;
             }
             records += (int64_t)x.records;
+            uq_records += (int64_t)x.uq_records;
             msgs += (int64_t)x.messages;
             int w = g.workers[i].w;
             for (int o = 0; o < g.p; o++) cnt[(size_t)w * g.p + o] = (int64_t)x.send[o];
@@ -370,7 +366,7 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
         }
         // comm.py:75-98 / 138-197 accounting
         r.mask_bytes = any_new ? 2.0 * (double)g.d * (double)g.p_rank / 8.0 : 0.0;
-        r.normal_bytes = 4 * records;
+        r.normal_bytes = 4 * (g.last_uq && g.p > 1 ? uq_records : records);
         if (g.last_la) {
             // local-all2all regroups (sender, dest) -> (r + p_rank * (dest / p_rank), dest)
             std::vector<int> seen((size_t)g.p * g.p, 0);

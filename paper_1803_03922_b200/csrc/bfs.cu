@@ -233,6 +233,7 @@ static void ensure_resources(Graph &g) {
         g.gparent.alloc(std::max<int64_t>(g.n, 1));
     }
     if (g.dist) g.mask_gather.alloc(std::max<int64_t>(nw_d, 1) * g.p);
+    g.recv_off.alloc(g.p + 1);
     // views
     g.views_h.assign(W, View{});
     for (int i = 0; i < W; i++) {
@@ -253,6 +254,8 @@ static void ensure_resources(Graph &g) {
         V.d = g.d;
         V.nw_n = nwords(Wk.n_local);
         V.nw_d = nw_d;
+        for (int o = 0; o < g.p && o < MAXW; o++) V.n_local_of_w[o] = g.n > o ? (g.n - o + g.p - 1) / g.p : 0;
+        V.recv_off = g.recv_off.p;
         for (int k = 0; k < 4; k++) {
             V.off[k] = g.off_all.p + Wk.base[k];
             V.col[k] = g.col_all.p;
@@ -320,7 +323,7 @@ static void ensure_resources(Graph &g) {
     g.dist_scratch.alloc(2 * (int64_t)(g.p + 3) * (g.p + 1) + 64);
     if (!g.h_ctl) {
         DBFS_CUDA(cudaHostAlloc((void **)&g.h_ctl, sizeof(Ctl), cudaHostAllocDefault));
-        DBFS_CUDA(cudaHostAlloc((void **)&g.h_status, 8 * ((size_t)(g.p + 3) * g.p + 8), cudaHostAllocDefault));
+        DBFS_CUDA(cudaHostAlloc((void **)&g.h_status, 8 * ((size_t)(g.p + 3) * g.p + g.p + 16), cudaHostAllocDefault));
     }
     g.bfs_ready = true;
     (void)ctx;
@@ -366,6 +369,8 @@ static AsmArgs make_asm(Graph &g, bool parents) {
 }
 
 // --------------------------------------------------------------- dist glue
+
+__global__ void k_count_reached(const int32_t *__restrict__ lv, int64_t n, unsigned long long *out);
 
 // Status vector of one rank at level L: records per destination (level L),
 // then the termination inputs of level L-1: records(L-1), |frontier normals at
@@ -422,6 +427,12 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     nccl_alltoallv_bytes(ctx, Wk.sendbuf.p, soff.data(), sbytes.data(), inbox, roff.data(), rbytes.data());
     g.h_status[S * p] = racc;
     DBFS_CUDA(cudaMemcpyAsync(&Wk.ctl.p->s[L % 3].inbox, &g.h_status[S * p], 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (g.views_h[0].uniquify) {
+        for (int o = 0; o < p; o++) g.h_status[S * p + 1 + o] = roff[o] / 8;
+        g.h_status[S * p + 1 + p] = racc;
+        DBFS_CUDA(cudaMemcpyAsync(g.recv_off.p, &g.h_status[S * p + 1], 8 * (p + 1), cudaMemcpyHostToDevice,
+                                  ctx.stream));
+    }
     k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, 1, L, F_DELEGATES | F_INGEST);
     DBFS_LAUNCHED();
     k_finish<<<grid, BT, sizeof(Smem), ctx.stream>>>(g.views.p, 1, L, F_NORMALS);
@@ -448,10 +459,28 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         V.parents = parents;
         V.symmetric = g.symmetric;
         V.exec_policy = o.exec_policy;
+        V.uniquify = o.uniquify;
+        V.local_all2all = o.local_all2all;
         for (int k = 0; k < 4; k++) {
             V.f0[k] = o.factor0[k];
             V.f1[k] = o.factor1[k];
         }
+    }
+    if (o.uniquify && g.p > 1) {  // seen-bits: [p groups][nw_n] per worker, zeroed once, then by F
+        bool fresh = false;
+        for (auto &Wk : g.workers)
+            if (!Wk.uq.p) {
+                Wk.uq.alloc((int64_t)g.p * std::max<int64_t>(nwords(Wk.n_local), 1));
+                DBFS_CUDA(cudaMemset(Wk.uq.p, 0, Wk.uq.bytes()));
+                fresh = true;
+            }
+        if (fresh)
+            for (int i = 0; i < W; i++) {
+                g.views_h[i].uq = g.workers[i].uq.p;
+                for (int j = 0; j < W; j++) g.views_h[i].uq_all[g.workers[j].w] = g.workers[j].uq.p;
+            }
+    } else {
+        for (auto &V : g.views_h) V.uniquify = 0;
     }
     DBFS_CUDA(cudaMemcpyAsync(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice, ctx.stream));
     uint32_t src_del = 0xffffffffu;
@@ -562,6 +591,17 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     }
     DBFS_CUDA(cudaGetLastError());
     DBFS_CHECK(!timeout, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
+    int64_t reached = -1;
+    if (!g.dist && st) {  // after ev1: not part of the timed traversal
+        unsigned long long *cnt = (unsigned long long *)g.dist_scratch.p + 2 * (g.p + 3) * (g.p + 1) + 8;
+        DBFS_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx.stream));
+        k_count_reached<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(g.levels_dev(), g.n, cnt);
+        DBFS_LAUNCHED();
+        unsigned long long h = 0;
+        DBFS_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, ctx.stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+        reached = (int64_t)h;
+    }
     float ms = 0.f;
     DBFS_CUDA(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1));
 
@@ -584,6 +624,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     if (st) {
         memset(st, 0, sizeof(*st));
         st->iterations = iterations;
+        st->reached = reached;
         for (int L = 0; L < nrec; L++)
             for (int i = 0; i < W; i++) {
                 const IterRec &r = g.last_rec[(size_t)L * W + i];

@@ -198,6 +198,7 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         r.insp[k] = r.dir[k] == FWD ? S.fv[k] : S.insp_bwd[k];
     }
     r.records = S.records;
+    r.uq_records = S.uq_records;
     for (int k = 0; k < 4; k++) {
         r.work[k] = S.work[k];
         r.exec_dir[k] = S.exec_dir[k];
@@ -228,6 +229,7 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
 #endif
 constexpr int UNR = DBFS_UNR;    // independent column loads in flight per lane (push)
 constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
+constexpr int PROBE = 4;         // candidate groups whose first entry is probed together
 constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long M38 = (1ull << 38) - 1;
 
@@ -295,6 +297,7 @@ struct TaskTimer {
 struct VisitCounters {
     unsigned long long fv_nn;       // FV_nn of this level's frontier (activity slot)
     unsigned long long records;     // remote normal records (comm accounting)
+    unsigned long long uq;          // records surviving uniquify
     unsigned long long insp_bwd[4];
     unsigned long long dirty;
     unsigned long long pull_rows;
@@ -350,6 +353,12 @@ __device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint3
     if (V.dist) {
         V.sendbin[o][base + rank] = make_uint2(c, (uint32_t)parent);
     } else {
+        if (V.uniquify) {  // staging group of (sender, dest): comm.py:165-171
+            int grp = V.local_all2all ? (V.w % V.p_rank) + V.p_rank * ((int)o / V.p_rank) : V.w;
+            const int64_t nwo = (V.n_local_of_w[o] + 31) >> 5;
+            uint32_t old = atomicOr(&V.uq_all[o][(int64_t)grp * nwo + (c >> 5)], 1u << (c & 31));
+            if (!(old & (1u << (c & 31)))) vc.uq++;
+        }
         claim_on(V.nvis_all[o], V.nfront_all[(L + 1) & 1][o], V.nlevel_all[o], V.nparent_all[o], V.parents, L, c,
                  parent, true);
     }
@@ -412,16 +421,13 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         if (ACT == ACT_DELEG && open) vc.dirty = 1;
         s[u] = open ? __ldcg(&nxt[tgt[u] >> 5]) : 0xffffffffu;
     }
-    // stage 3: independent atomics, all in flight; only the winner stores
-#pragma unroll
-    for (int u = 0; u < UNR; u++) {
-        const uint32_t bit = 1u << (tgt[u] & 31);
-        s[u] = (s[u] & bit) ? bit : atomicOr(&nxt[tgt[u] >> 5], bit);
-    }
+    // stage 3: fire-and-forget marks (RED.OR, no return value) and plain stores:
+    // concurrent writers of one vertex store the same level and a valid parent.
 #pragma unroll
     for (int u = 0; u < UNR; u++) {
         const uint32_t x = tgt[u];
         if ((s[u] >> (x & 31)) & 1u) continue;
+        atomicOr(&nxt[x >> 5], 1u << (x & 31));
         if (ACT == ACT_DELEG) {
             if (V.parents) V.dcand[x] = pp[u];
         } else {
@@ -621,35 +627,62 @@ __device__ __forceinline__ void pull_kind(int64_t nw, int64_t gw, int64_t TW, ui
         uint32_t word = wi < nw ? cand(wi) : 0u;
         unsigned cnt = warp_compact(word, wi, list);
         if (lane == 0) rows += cnt;
-        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
-            unsigned i = g0 + lane;
-            bool ok = i < cnt;
-            uint32_t v = ok ? list[i] : 0u;
-            int64_t b = ok ? __ldg(&off[v]) : 0, e = ok ? __ldg(&off[v + 1]) : 0;
-            PullRes r;
-            r.pos = -1;
-            r.col = 0;
-            int64_t j = e;
-            bool done = ok ? lane_scan(col, front, filt, b, e, j, r) : true;
-            unsigned pend = __ballot_sync(FULL, !done);
-            while (pend) {
-                int l = __ffs(pend) - 1;
-                pend &= pend - 1;
-                int64_t jl = __shfl_sync(FULL, j, l), el = __shfl_sync(FULL, e, l);
-                PullRes rr = warp_scan_row(col, front, filt, jl, el);
-                if ((int)lane == l) r = rr;
+        // First probe of 4 groups at once (4 independent chains per lane):
+        // offsets, first column, its status bit.  Most candidates resolve here
+        // at dense levels; the rest continue with the geometric lane scan.
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32 * PROBE) {
+            uint32_t v[PROBE], c0[PROBE];
+            int64_t b[PROBE], e[PROBE];
+            bool ok[PROBE], h0[PROBE];
+#pragma unroll
+            for (int q = 0; q < PROBE; q++) {
+                unsigned i = g0 + q * 32 + lane;
+                ok[q] = i < cnt;
+                v[q] = ok[q] ? list[i] : 0u;
             }
-            if (ok) {
-                if (r.pos >= 0) {
-                    insp += (unsigned long long)(r.pos - b + 1);
-                    on_hit(v, r.col);
-                } else {
-                    insp += (unsigned long long)(e - b);
+#pragma unroll
+            for (int q = 0; q < PROBE; q++) {
+                b[q] = ok[q] ? __ldg(&off[v[q]]) : 0;
+                e[q] = ok[q] ? __ldg(&off[v[q] + 1]) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < PROBE; q++) c0[q] = (ok[q] && b[q] < e[q]) ? __ldg(&col[b[q]]) : 0u;
+#pragma unroll
+            for (int q = 0; q < PROBE; q++)
+                h0[q] = ok[q] && b[q] < e[q] && (!filt || coarse_hit(filt, c0[q])) && tbit(front, c0[q]);
+#pragma unroll
+            for (int q = 0; q < PROBE; q++) {
+                PullRes r;
+                r.pos = h0[q] ? b[q] : -1;
+                r.col = c0[q];
+                int64_t j = e[q];
+                bool done = !ok[q] || h0[q] || b[q] + 1 >= e[q];
+                if (!done) done = lane_scan(col, front, filt, b[q] + 1, e[q], j, r);
+                unsigned pend = __ballot_sync(FULL, !done);
+                while (pend) {
+                    int l = __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    int64_t jl = __shfl_sync(FULL, j, l), el = __shfl_sync(FULL, e[q], l);
+                    PullRes rr = warp_scan_row(col, front, filt, jl, el);
+                    if ((int)lane == l) r = rr;
                 }
+                const bool hit = ok[q] && r.pos >= 0;
+                if (ok[q]) insp += (unsigned long long)(hit ? r.pos - b[q] + 1 : e[q] - b[q]);
+                on_hit(hit, v[q], r.col);  // warp-uniform call: marks are aggregated per word
             }
         }
         __syncwarp();
     }
+}
+
+// Warp-uniform mark of candidate v (lanes with hit): lanes of the warp hold
+// near-consecutive candidates, so bits of one word are OR-ed in registers and
+// the word gets one RED.OR.
+__device__ __forceinline__ void warp_mark(uint32_t *bm, bool hit, uint32_t v) {
+    const unsigned wkey = hit ? (v >> 5) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(FULL, wkey);
+    const unsigned bits = __reduce_or_sync(peers, hit ? (1u << (v & 31)) : 0u);
+    if (hit && (int)lane_id() == __ffs(peers) - 1) atomicOr(&bm[v >> 5], bits);
 }
 
 // -------------------------------------------------------------- phase V(L)
@@ -748,7 +781,13 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         const uint32_t *nvis = V.nvis;
         pull_kind(V.nw_n, gw, TW, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
-                  [&](uint32_t c, uint32_t x) { claim_normal(V, L, c, __ldg(&V.del_gid[x]), false); });
+                  [&](bool hit, uint32_t c, uint32_t x) {
+                      warp_mark(V.nfront[(L + 1) & 1], hit, c);
+                      if (hit) {
+                          V.nlevel[c] = L + 1;
+                          if (V.parents) V.nparent[c] = __ldg(&V.del_gid[x]);
+                      }
+                  });
     }
     tt.stop(AT, 3);
     // T6: dd pull -- unvisited dd-source delegates scan dd rows (engine.py:257-261).
@@ -762,7 +801,13 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         const uint32_t *cdd = (dirs[KIND_DD] == FWD && V.col_sorted_dd) ? V.col_sorted_dd : V.col[KIND_DD];
         pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DD], cdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
-                  [&](uint32_t x, uint32_t y) { find_delegate(V, L, x, __ldg(&V.del_gid[y]), vc.dirty); });
+                  [&](bool hit, uint32_t x, uint32_t y) {
+                      warp_mark(V.dnext[L & 1], hit, x);
+                      if (hit) {
+                          vc.dirty = 1;
+                          if (V.parents) V.dcand[x] = __ldg(&V.del_gid[y]);
+                      }
+                  });
     }
     tt.stop(AT, 5);
     if (nfilt) {
@@ -780,7 +825,13 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
                   vc.insp_bwd[KIND_ND], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
-                  [&](uint32_t x, uint32_t c) { find_delegate(V, L, x, (int64_t)c * p + w, vc.dirty); });
+                  [&](bool hit, uint32_t x, uint32_t c) {
+                      warp_mark(V.dnext[L & 1], hit, x);
+                      if (hit) {
+                          vc.dirty = 1;
+                          if (V.parents) V.dcand[x] = (int64_t)c * p + w;
+                      }
+                  });
     }
     tt.stop(AT, 4);
     // flush: one atomic per warp per counter
@@ -793,6 +844,8 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     }
     v = warp_sum(vc.records);
     if (lane == 0) atomic_add_u64(&A.records, v);
+    v = warp_sum(vc.uq);
+    if (lane == 0) atomic_add_u64(&A.uq_records, v);
     for (int k = 1; k < 4; k++) {
         v = warp_sum(vc.insp_bwd[k]);
         if (lane == 0 && v) {
@@ -930,10 +983,20 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
 __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
     const unsigned long long nin = V.ctl->s[L % 3].inbox;
     const uint2 *inbox = V.inbox[L & 1];
+    unsigned long long uq = 0;
     for (int64_t i = tid; i < (int64_t)nin; i += nth) {
         uint2 rec = inbox[i];
+        if (V.uniquify) {  // records arrive grouped by source rank: recover it
+            int s = 0;
+            while (s + 1 < V.p && V.recv_off[s + 1] <= i) s++;
+            int grp = V.local_all2all ? (s % V.p_rank) + V.p_rank * (V.w / V.p_rank) : s;
+            uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
+            if (!(old & (1u << (rec.x & 31)))) uq++;
+        }
         claim_normal(V, L, rec.x, (int64_t)rec.y, true);
     }
+    uq = warp_sum(uq);
+    if (lane_id() == 0 && uq) atomicAdd(&V.ctl->s[L % 3].uq_records, uq);
 }
 
 // F3: fold the new normal frontier into visited, clear the old one, and count
@@ -1022,6 +1085,8 @@ __device__ void phase_finish(const View &V, int L, int wb, int nb, Smem &sm, int
     if (parts & F_NORMALS)
         for (int64_t i = tid; i < FW; i += nth) V.coarse_n[L & 1][i] = 0u;
     if (parts & F_INGEST) finish_ingest(V, L, tid, nth);
+    if ((parts & F_NORMALS) && V.uniquify)
+        for (int64_t i = tid; i < (int64_t)V.p * V.nw_n; i += nth) V.uq[i] = 0u;
     if (parts & F_NORMALS) {
         tt.start();
         finish_normals(V, L, gw, TW, list, fc);

@@ -32,6 +32,7 @@ struct LevelSlot {
     unsigned long long new_del;      // delegates discovered at the barrier
     unsigned long long inbox;        // records delivered to this worker
     unsigned long long pull_rows;    // reverse rows scanned by pulls at this level
+    unsigned long long uq_records;   // records left after per-group uniquify (comm.py:122-127)
     unsigned long long work[4];      // inspections actually executed (push: FV, pull: scanned)
     int exec_dir[4];                 // executed strategy per kind (may differ from the reported one)
     unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
@@ -62,6 +63,7 @@ struct IterRec {
     unsigned long long messages;
     unsigned long long new_del;
     unsigned long long rows;         // rows expanded (push) + scanned (pull)
+    unsigned long long uq_records;
     unsigned long long work[4];      // executed inspections
     int exec_dir[4];
     unsigned long long tsum[8], tmax[8];
@@ -75,6 +77,11 @@ struct View {
     int w, W, p, p_rank, dist;       // global index, local worker count, shape
     int mode, allow_back, parents;
     int symmetric, exec_policy;      // executor may pull a FORWARD-reported kind (dobfs, symmetric graphs)
+    int uniquify, local_all2all;     // comm accounting options (comm.py:138-197)
+    uint32_t *uq_all[MAXW];          // per destination worker: [p staging groups][nw_n] seen-bits
+    uint32_t *uq;                    // this worker's seen-bits (cleared in F)
+    int64_t n_local_of_w[MAXW];      // local normal count of every worker
+    const int64_t *recv_off;         // dist: first inbox index of each source rank (p+1)
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
     int rec_cap;
@@ -182,6 +189,7 @@ struct WorkerHost {
     DArray<uint32_t> dlist[4];       // [kind*2 + parity]
     DArray<int64_t> dpre[4];
     DArray<uint2> inbox0, inbox1, sendbuf;
+    DArray<uint32_t> uq;             // uniquify seen-bits, allocated on first use
     DArray<Ctl> ctl;
     DArray<IterRec> rec;
     int64_t inbox_cap = 0;
@@ -210,6 +218,7 @@ struct Graph {
     DArray<int32_t> glevel;          // assembled outputs (p > 1)
     DArray<int64_t> gparent;
     DArray<uint32_t> mask_gather;    // dist: allgather of dnext slices
+    DArray<int64_t> recv_off;        // dist: per-source inbox offsets of the current level
     DArray<unsigned long long> dist_scratch;
     Ctl *h_ctl = nullptr;            // pinned host mirrors for the distributed level loop
     int64_t *h_status = nullptr;
