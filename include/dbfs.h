@@ -82,7 +82,7 @@ typedef struct {
     int32_t local_all2all;      /* accounting only (comm.py:138-197) */
     int32_t uniquify;           /* accounting only */
     int32_t parent_mode;        /* 0 none, 1 any valid tree (timed), 2 min-ID */
-    int32_t engine;             /* 0 auto, 1 host-driven level loop, 2 persistent kernel */
+    int32_t engine;             /* 0 auto, 1 host-driven level loop, 2 persistent kernel, 3 peer (multi-GPU persistent over CUDA IPC) */
     int32_t record_iterations;  /* keep per-iteration records for dbfs_bfs_iteration */
     int32_t exec_policy;        /* 1: on symmetric graphs in dobfs mode, execute a FORWARD-reported
                                    kind as the equivalent pull when cheaper (reported directions and
@@ -103,7 +103,7 @@ typedef struct {
     double init_us;             /* device time of state init + seeding */
     int64_t work_inspections;   /* inspections actually executed (<= reported when pulls replace pushes) */
     int32_t per_iteration_truncated;
-    int32_t engine_used;        /* 1 host loop, 2 persistent */
+    int32_t engine_used;        /* 1 host loop, 2 persistent, 3 peer */
 } dbfs_run_stats;
 
 /* One BfsRun.per_iteration entry summed over workers (engine.py:291-302). */

@@ -8,6 +8,7 @@
 //               used with one worker per process (torchrun, NCCL over NVLink).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "bfs_device.cuh"
@@ -32,16 +33,47 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Sense-counting grid barrier with a watchdog: a block that waits > 4 s sets
 // `abort`, every block then leaves the kernel (reported as DBFS_ETIMEOUT).
-__device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks) {
+// With `gbar` (peer engine) the last local arriver also meets the other GPUs
+// on a system-scope barrier in rank 0's memory before releasing its GPU, so
+// exactly one thread per GPU polls over NVLink.
+__device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBar *gbar = nullptr,
+                                          unsigned nranks = 1) {
     __shared__ int s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned gen = ld_acquire_u32(&bar->gen);
-        __threadfence();
+        if (gbar) __threadfence_system();
+        else __threadfence();
         unsigned arrived = atomicAdd(&bar->count, 1u);
         if (arrived == nblocks - 1) {
+            if (gbar) {
+                unsigned ggen = ld_acquire_sys_u32(&gbar->gen);
+                unsigned garr = atomicAdd_system(&gbar->count, 1u);
+                if (garr == nranks - 1) {
+                    atomicExch_system(&gbar->count, 0u);
+                    __threadfence_system();
+                    atomicAdd_system(&gbar->gen, 1u);
+                } else {
+                    unsigned long long t0 = globaltimer_ns();
+                    while (ld_acquire_sys_u32(&gbar->gen) == ggen) {
+                        if (ld_acquire_sys_u32(&gbar->abort)) break;
+                        if (globaltimer_ns() - t0 > 4000000000ull) {
+                            atomicExch_system(&gbar->abort, 1u);
+                            break;
+                        }
+                        __nanosleep(32);
+                    }
+                }
+                if (ld_acquire_sys_u32(&gbar->abort)) atomicExch(&bar->abort, 1u);
+            }
             atomicExch(&bar->count, 0u);
             __threadfence();
             atomicAdd(&bar->gen, 1u);
@@ -56,7 +88,8 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks) {
                 __nanosleep(64);
             }
         }
-        __threadfence();
+        if (gbar) __threadfence_system();
+        else __threadfence();
         s_ok = ld_acquire_u32(&bar->abort) == 0;
     }
     __syncthreads();
@@ -99,7 +132,8 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
 
 __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
                                                        uint32_t src_del, GridBar *bar, int rec_cap,
-                                                       AsmArgs asm_args, int do_assemble) {
+                                                       AsmArgs asm_args, int do_assemble, GridBar *gbar,
+                                                       int nranks) {
     extern __shared__ uint4 dsm[];
     Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
@@ -108,26 +142,35 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     const bool timer = wb == 0 && threadIdx.x == 0;
     if (timer) V.ctl->t_start = globaltimer_ns();
     phase_init(V, wb, nb);
-    if (!grid_sync(bar, nblocks)) return;
+    if (!grid_sync(bar, nblocks, gbar, nranks)) return;
     if (wb == 0 && threadIdx.x == 0) seed_worker(V, source, src_del);
-    if (!grid_sync(bar, nblocks)) return;
+    if (!grid_sync(bar, nblocks, gbar, nranks)) return;
     if (timer) V.ctl->t_seeded = globaltimer_ns();
     int L = 0;
     for (;; L++) {
         if (L > 0) {
-            bool cont = level_continue(views, W, L - 1);
+            bool cont = level_continue(V, L - 1);
             if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
             if (!cont) break;
         }
         if (timer && L < rec_cap) V.rec[L].t[0] = globaltimer_ns();
         phase_visit(V, L, wb, nb, sm);
-        if (!grid_sync(bar, nblocks)) return;
+        if (!grid_sync(bar, nblocks, gbar, nranks)) return;
         if (timer && L < rec_cap) V.rec[L].t[1] = globaltimer_ns();
-        phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
-        if (!grid_sync(bar, nblocks)) return;
+        if (V.peer) {  // peers' records are claimed before the frontier is folded
+            phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_INGEST);
+            if (!grid_sync(bar, nblocks)) return;
+            phase_finish(V, L, wb, nb, sm, F_NORMALS);
+        } else {
+            phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
+        }
+        if (!grid_sync(bar, nblocks, gbar, nranks)) return;
         if (timer && L < rec_cap) V.rec[L].t[2] = globaltimer_ns();
     }
     if (wb == 0 && threadIdx.x == 0) V.ctl->last_level = L;
+    // peers read this GPU's control block until they leave the loop: nobody may
+    // start the next BFS (host resets the block) before every GPU is past it
+    if (gbar && !grid_sync(bar, nblocks, gbar, nranks)) return;
     if (do_assemble) phase_assemble(asm_args, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
 }
 
@@ -161,6 +204,7 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 Graph::~Graph() {
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_status) cudaFreeHost(h_status);
+    for (void *q : peer_opened) cudaIpcCloseMemHandle(q);
 }
 
 int32_t *Graph::levels_dev() { return (p == 1 && !dist) ? workers[0].nlevel.p : glevel.p; }
@@ -193,6 +237,7 @@ static void ensure_resources(Graph &g) {
         std::vector<int64_t> all((size_t)g.p * g.p);
         DBFS_CUDA(cudaMemcpy(all.data(), r.p, 8 * g.p * g.p, cudaMemcpyDeviceToHost));
         for (int src = 0; src < g.p; src++) inbox_cap[ctx.rank] += all[(size_t)src * g.p + ctx.rank];
+        g.cap_all = all;
     }
     for (auto &Wk : g.workers) {
         const int64_t nl = Wk.n_local, nw_n = nwords(nl);
@@ -442,6 +487,98 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     return true;
 }
 
+// ------------------------------------------------------------- peer engine
+
+// Map the peers' control blocks, delegate masks/candidates and inboxes
+// through CUDA IPC (NVLink/NVSwitch), so the persistent kernel runs across all
+// ranks: delegate masks are OR-ed straight from peer memory, remote records are
+// stored into fixed per-sender segments of the owner's inbox, and levels are
+// separated by a system-scope barrier in rank 0's memory.  Collective; every
+// rank agrees on the outcome (the host-loop NCCL engine is the fallback).
+static void setup_peer(Graph &g) {
+    if (g.peer_state) return;
+    g.peer_state = -1;
+    Ctx &ctx = *g.ctx;
+    const int p = g.p, me = ctx.rank;
+    const char *env = getenv("DBFS_PEER");
+    int ok = (!env || env[0] != '0') && p <= MAXW && g.workers.size() == 1 && (int)g.cap_all.size() == p * p;
+    WorkerHost &Wk = g.workers[0];
+    g.gbar_mem.alloc(4);
+    DBFS_CUDA(cudaMemset(g.gbar_mem.p, 0, 16));
+    constexpr int NH = 6;
+    void *bases[NH] = {Wk.ctl.p, Wk.dnext0.p, Wk.dnext1.p, Wk.dcand.p, Wk.inbox0.p, g.gbar_mem.p};
+    std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * p);
+    for (int i = 0; i < NH && ok; i++)
+        if (cudaIpcGetMemHandle(&mine[i], bases[i]) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+        }
+    const int64_t HB = (int64_t)sizeof(cudaIpcMemHandle_t) * NH;
+    DArray<uint8_t> hs, hr;
+    hs.alloc(HB);
+    hr.alloc(HB * p);
+    DBFS_CUDA(cudaMemcpy(hs.p, mine.data(), HB, cudaMemcpyHostToDevice));
+    nccl_allgather_bytes(ctx, hs.p, hr.p, HB);
+    DBFS_CUDA(cudaMemcpy(all.data(), hr.p, HB * p, cudaMemcpyDeviceToHost));
+    auto agree = [&](int v) {
+        DArray<uint32_t> f;
+        f.alloc(1);
+        uint32_t h = v ? 1u : 0u;
+        DBFS_CUDA(cudaMemcpy(f.p, &h, 4, cudaMemcpyHostToDevice));
+        nccl_allreduce_u32_sum(ctx, f.p, 1);
+        DBFS_CUDA(cudaMemcpy(&h, f.p, 4, cudaMemcpyDeviceToHost));
+        return (int)h == p;
+    };
+    if (!agree(ok)) return;
+    std::vector<void *> ptr((size_t)NH * p, nullptr);
+    for (int j = 0; j < p; j++)
+        for (int i = 0; i < NH; i++) {
+            if (j == me) {
+                ptr[(size_t)j * NH + i] = bases[i];
+                continue;
+            }
+            if (i == NH - 1 && j != 0) continue;  // only rank 0's barrier is used
+            void *q = nullptr;
+            if (ok && cudaIpcOpenMemHandle(&q, all[(size_t)j * NH + i], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+                g.peer_opened.push_back(q);
+                ptr[(size_t)j * NH + i] = q;
+            } else {
+                cudaGetLastError();
+                ok = 0;
+            }
+        }
+    if (!agree(ok)) {
+        for (void *q : g.peer_opened) cudaIpcCloseMemHandle(q);
+        g.peer_opened.clear();
+        return;
+    }
+    View V = g.views_h[0];
+    V.peer = 1;
+    V.dist = 1;
+    V.cand_all = 1;
+    V.P_sources = p;
+    for (int j = 0; j < p; j++) {
+        V.ctl_all[j] = (Ctl *)ptr[(size_t)j * NH + 0];
+        V.mask_src[0][j] = (const uint32_t *)ptr[(size_t)j * NH + 1];
+        V.mask_src[1][j] = (const uint32_t *)ptr[(size_t)j * NH + 2];
+        V.cand_src[j] = (const int64_t *)ptr[(size_t)j * NH + 3];
+    }
+    // receiver r's inbox: segments by sender, sized by the senders' capacities towards r
+    auto seg = [&](int r, int s) {
+        int64_t o = 0;
+        for (int t = 0; t < s; t++) o += g.cap_all[(size_t)t * p + r];
+        return o;
+    };
+    for (int s = 0; s < p; s++) V.seg_off[s] = seg(me, s);
+    for (int o = 0; o < p; o++)
+        V.sendbin[o] = o == me ? nullptr : (uint2 *)ptr[(size_t)o * NH + 4] + seg(o, me);
+    V.inbox[0] = V.inbox[1] = Wk.inbox0.p;
+    g.gbar = ptr[NH - 1];  // rank 0's (its own on rank 0)
+    g.peer_view_h = V;
+    g.peer_view.alloc(1);
+    g.peer_state = 1;
+}
+
 // ------------------------------------------------------------------ driver
 
 void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
@@ -482,15 +619,37 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     } else {
         for (auto &V : g.views_h) V.uniquify = 0;
     }
+    int engine = o.engine;
+    if (g.dist) {
+        // auto / persistent: one kernel across all GPUs over peer memory when every rank can map its peers
+        if (engine != 1) setup_peer(g);
+        engine = (engine != 1 && g.peer_state == 1) ? 3 : 1;
+    } else {
+        if (engine == 0 || engine == 3) engine = 2;
+    }
+    if (engine == 3) {
+        View &P = g.peer_view_h;
+        const View &B = g.views_h[0];
+        P.mode = B.mode;
+        P.allow_back = B.allow_back;
+        P.parents = B.parents;
+        P.symmetric = B.symmetric;
+        P.exec_policy = B.exec_policy;
+        P.uniquify = B.uniquify;
+        P.uq = B.uq;
+        P.local_all2all = B.local_all2all;
+        for (int k = 0; k < 4; k++) {
+            P.f0[k] = B.f0[k];
+            P.f1[k] = B.f1[k];
+        }
+        DBFS_CUDA(cudaMemcpyAsync(g.peer_view.p, &P, sizeof(View), cudaMemcpyHostToDevice, ctx.stream));
+    }
     DBFS_CUDA(cudaMemcpyAsync(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice, ctx.stream));
     uint32_t src_del = 0xffffffffu;
     DBFS_CUDA(cudaMemcpyAsync(&src_del, g.del_id.p + o.source, 4, cudaMemcpyDeviceToHost, ctx.stream));
     for (auto &Wk : g.workers) DBFS_CUDA(cudaMemsetAsync(Wk.ctl.p, 0, sizeof(Ctl), ctx.stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
 
-    int engine = o.engine;
-    if (engine == 0) engine = g.dist ? 1 : 2;
-    DBFS_CHECK(!(g.dist && engine == 2), DBFS_EINVAL, "persistent engine needs all workers on one device");
     const int64_t launches0 = g_kernel_launches;
     const bool assemble = g.p > 1 && !g.dist;
     AsmArgs aa = make_asm(g, parents);
@@ -498,7 +657,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     bool timeout = false;
 
     GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
-    if (engine == 2) DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
+    if (engine >= 2) DBFS_CUDA(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx.stream));
     // everything host-side happens before ev0: the event pair brackets only device work
     if (g.clock_ghz <= 0) {
         int khz = 0;
@@ -507,7 +666,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     }
     set_smem_attrs();
     int pgrid = 0;
-    if (engine == 2) {
+    if (engine >= 2) {
         if (g.pgrid <= 0) {
             int bps = 0;
             g.pgrid = persistent_grid(g, &bps);
@@ -515,16 +674,18 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         pgrid = g.pgrid;
         g.warps_per_worker = (double)pgrid / W * WPB;
     }
+    if (engine == 3) DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
-    if (engine == 2) {
+    if (engine >= 2) {
         int grid = pgrid;
-        const View *vp = g.views.p;
+        const View *vp = engine == 3 ? g.peer_view.p : g.views.p;
         int64_t src = o.source;
         int rec_cap = g.rec_cap;
-        (void)grid;
         int do_asm = assemble ? 1 : 0;
-        void *args[] = {(void *)&vp, (void *)&W, (void *)&src, (void *)&src_del, (void *)&bar,
-                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm};
+        GridBar *gb = engine == 3 ? (GridBar *)g.gbar : nullptr;
+        int nr = engine == 3 ? g.p : 1;
+        void *args[] = {(void *)&vp,      (void *)&W,  (void *)&src,    (void *)&src_del, (void *)&bar,
+                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm, (void *)&gb,      (void *)&nr};
         DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, sizeof(Smem),
                                               ctx.stream));
         DBFS_LAUNCHED();
@@ -536,6 +697,10 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         Ctl c0;
         DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
         iterations = c0.last_level;
+        if (engine == 3) {
+            g.assembled = false;  // delegate parents are already the min over ranks (candidates read from peers)
+            if (timeout) g.peer_state = -1;  // barrier state unknown: later runs use the NCCL level loop
+        }
     } else {
         const int grid = std::max(W, (ctx.num_sms * 4 / W) * W);
         g.warps_per_worker = (double)grid / W * WPB;
@@ -653,7 +818,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         st->work_inspections = work;
         // library-side copies of this call: views + options up, control block / records down
         st->h2d_bytes = (int64_t)(sizeof(View) * W);
-        if (engine == 2) {
+        if (engine >= 2) {
             Ctl c0;
             DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
             st->init_us = (double)(c0.t_seeded - c0.t_start) / 1e3;

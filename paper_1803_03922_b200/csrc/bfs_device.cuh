@@ -878,8 +878,8 @@ __device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, u
     if (V.parents) {
         if (V.cand_all) {
             for (int s = 0; s < V.P_sources; s++)
-                if ((V.mask_src[L & 1][s][xw] >> xb) & 1u) {
-                    int64_t c = V.cand_src[s][x];
+                if ((__ldcg(&V.mask_src[L & 1][s][xw]) >> xb) & 1u) {
+                    int64_t c = __ldcg(&V.cand_src[s][x]);
                     par = c < par ? c : par;
                 }
         } else if ((V.dnext[L & 1][xw] >> xb) & 1u) {
@@ -905,7 +905,7 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         uint32_t nw = 0u;
         if (wi < V.nw_d) {
             uint32_t r = 0;
-            for (int s = 0; s < V.P_sources; s++) r |= V.mask_src[L & 1][s][wi];
+            for (int s = 0; s < V.P_sources; s++) r |= __ldcg(&V.mask_src[L & 1][s][wi]);
             uint32_t dv = V.dvis[wi];
             nw = r & ~dv;
             next_mask[wi] = 0u;
@@ -981,6 +981,26 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
 
 // F2 (distributed only): ingest remote records (engine.py:147-157).
 __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
+    if (V.peer) {  // senders stored into fixed segments of this inbox over NVLink
+        unsigned long long uq = 0;
+        for (int s = 0; s < V.p; s++) {
+            if (s == V.w) continue;
+            const unsigned long long cnt = __ldcg(&V.ctl_all[s]->s[L % 3].send[V.w]);
+            const uint2 *seg = V.inbox[0] + V.seg_off[s];
+            const int grp = V.local_all2all ? (s % V.p_rank) + V.p_rank * (V.w / V.p_rank) : s;
+            for (int64_t i = tid; i < (int64_t)cnt; i += nth) {
+                uint2 rec = __ldcg(&seg[i]);
+                if (V.uniquify) {
+                    uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
+                    if (!(old & (1u << (rec.x & 31)))) uq++;
+                }
+                claim_normal(V, L, rec.x, (int64_t)rec.y, true);
+            }
+        }
+        uq = warp_sum(uq);
+        if (lane_id() == 0 && uq) atomicAdd(&V.ctl->s[L % 3].uq_records, uq);
+        return;
+    }
     const unsigned long long nin = V.ctl->s[L % 3].inbox;
     const uint2 *inbox = V.inbox[L & 1];
     unsigned long long uq = 0;
@@ -1171,11 +1191,11 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
 
 // Continue after level L?  engine.py:303-306: new local normals, new
 // delegates, or any record in flight (over all in-process workers).
-__device__ __forceinline__ bool level_continue(const View *views, int W, int L) {
-    if (views[0].ctl->s[L % 3].new_del) return true;
-    for (int i = 0; i < W; i++) {
-        const Ctl &c = *views[i].ctl;
-        if (c.s[(L + 1) % 3].nfront || c.s[L % 3].records) return true;
+__device__ __forceinline__ bool level_continue(const View &V, int L) {
+    if (V.ctl->s[L % 3].new_del) return true;
+    for (int i = 0; i < V.P_sources; i++) {
+        const Ctl *c = V.ctl_all[i];  // a peer GPU's block in the peer engine: read at L2
+        if (__ldcg(&c->s[(L + 1) % 3].nfront) || __ldcg(&c->s[L % 3].records)) return true;
     }
     return false;
 }

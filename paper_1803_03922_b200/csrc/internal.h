@@ -82,6 +82,8 @@ struct View {
     uint32_t *uq;                    // this worker's seen-bits (cleared in F)
     int64_t n_local_of_w[MAXW];      // local normal count of every worker
     const int64_t *recv_off;         // dist: first inbox index of each source rank (p+1)
+    int peer;                        // dist over CUDA IPC: peers' arrays mapped, one persistent launch
+    int64_t seg_off[MAXW];           // peer: inbox segment of each source rank
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
     int rec_cap;
@@ -236,6 +238,14 @@ struct Graph {
     std::vector<IterRec> last_rec;   // [iteration][local worker]
     std::vector<std::vector<unsigned long long>> last_send_matrix;
     int last_mode = 1, last_la = 0, last_uq = 0;
+    // peer engine (dist): CUDA-IPC mapped peer arrays + a cross-GPU barrier
+    int peer_state = 0;              // 0 untried, 1 ready, -1 unavailable
+    std::vector<void *> peer_opened; // IPC mappings to close
+    DArray<uint32_t> gbar_mem;       // rank 0's copy is the cross-GPU barrier
+    void *gbar = nullptr;
+    View peer_view_h;
+    DArray<View> peer_view;
+    std::vector<int64_t> cap_all;    // dist: [src][dst] remote record capacities
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();

@@ -30,7 +30,7 @@ from .traversal import BACKWARD, DO_KINDS, FORWARD
 MODES = ("bfs", "dobfs")
 KINDS = ("nn", "nd", "dn", "dd")
 PARENT_MODES = {None: 0, "none": 0, "any": 1, "min": 2}
-ENGINES = {"auto": 0, "host": 1, "persistent": 2}
+ENGINES = {"auto": 0, "host": 1, "persistent": 2, "peer": 3}
 
 
 class EmptyReportError(RuntimeError):

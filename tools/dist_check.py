@@ -27,26 +27,39 @@ if rank == 0:
     print(f"built s{scale} on {world} GPUs in {time.time()-t0:.2f}s kinds {pg.kind_totals} d {pg.classification.d}",
           flush=True)
 roots = [1, 77, 4242 % (1 << scale), 9999 % (1 << scale)]
+engines = sys.argv[2].split(",") if len(sys.argv) > 2 else ["host", "peer"]
 res = []
-for mode in ("dobfs", "bfs"):
-    for r in roots:
-        lv = np.empty(pg.n, dtype=np.int32)
-        pa = np.empty(pg.n, dtype=np.int64)
-        st = _bfs_raw(pg, BfsOptions(mode=mode, source=r), lv, pa)
-        bad = api.validate_bfs_tree(pg, r)
-        res.append((mode, r, levels_digest(lv), st.iterations,
-                    [[int(st.inspections[k][0]), int(st.inspections[k][1])] for k in range(4)], bad, st.device_ms))
-ok = True
+local_ok = True
+for engine in engines:
+    for mode in ("dobfs", "bfs"):
+        for r in roots:
+            lv = np.empty(pg.n, dtype=np.int32)
+            pa = np.empty(pg.n, dtype=np.int64)
+            st = _bfs_raw(pg, BfsOptions(mode=mode, source=r, engine=engine), lv, pa)
+            bad = api.validate_bfs_tree(pg, r)
+            res.append((engine, st.engine_used, mode, r, levels_digest(lv), st.iterations,
+                        [[int(st.inspections[k][0]), int(st.inspections[k][1])] for k in range(4)], bad, st.device_ms))
+# per-rank records (directions, FV, comm accounting incl. uniquify) must not depend on the engine
+for opts in (dict(), dict(uniquify=True), dict(uniquify=True, local_all2all=True)):
+    runs = [api.run_bfs(pg, BfsOptions(source=roots[1], engine=e, **opts)).to_dict() for e in engines]
+    for key in ("iterations", "per_iteration", "comm", "levels_digest"):
+        if any(x[key] != runs[0][key] for x in runs[1:]):
+            local_ok = False
+            print(f"rank {rank}: engines disagree on {key} with {opts}", flush=True)
+flags = [None] * world
+tdist.all_gather_object(flags, local_ok)
+ok = all(flags)
 if rank == 0:
     import oracle as O
     og = O.partition_rmat(scale, 16, 1, world)
-    for mode, r, dg, it, insp, bad, ms in res:
+    for engine, used, mode, r, dg, it, insp, bad, ms in res:
         ref = O.run_bfs(og, r, mode=mode)
         ri = [[ref["inspections"][k]["forward"], ref["inspections"][k]["backward"]] for k in ("nn", "nd", "dn", "dd")]
         good = dg == ref["levels_digest"] and it == ref["iterations"] and insp == ri and bad == 0
         ok &= good
-        print(f"{mode} root {r}: digest {'OK' if dg == ref['levels_digest'] else 'MISMATCH'} iters {it}/{ref['iterations']}"
-              f" insp {'OK' if insp == ri else (insp, ri)} certificate {bad} device {ms:.2f} ms", flush=True)
+        print(f"{engine}({used}) {mode} root {r}: digest {'OK' if dg == ref['levels_digest'] else 'MISMATCH'} "
+              f"iters {it}/{ref['iterations']} insp {'OK' if insp == ri else (insp, ri)} certificate {bad} "
+              f"device {ms:.2f} ms", flush=True)
     print("DIST CHECK", "PASS" if ok else "FAIL", flush=True)
 tdist.barrier()
 tdist.destroy_process_group()
