@@ -15,7 +15,8 @@ A step is one BFS from one root; K steps cycle through the 64 roots.
   roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md §Measurement
 
 Multi-GPU (torchrun, one process per GPU): weak scaling, scale = 24 + log2(N),
-one worker per GPU over NCCL; step time = max over ranks.
+one worker per GPU; the BFS runs as one persistent kernel per GPU over
+CUDA-IPC peer memory (NVLink), NCCL only for setup/assembly; step time = max over ranks.
 ``--impl reference`` times the CPU restatement of the reference (oracle/) on
 this host on the same config (rank 0 only).
 """
@@ -40,6 +41,9 @@ sys.path.insert(0, ROOT)
 METRIC = "Graph500 harmonic-mean GTEPS, RMAT weak/strong scaling at 1/2/4/8 B200"
 UNIT = "GTEPS"
 L2_BYTES = 126 << 20
+
+
+ENGINE_NOTE = {1: " (NCCL level loop)", 3: " (one persistent kernel across GPUs over CUDA-IPC peer memory)"}
 
 
 def suggested_theta(scale: int) -> int:
@@ -188,6 +192,7 @@ def run_ours(args, world, rank, local_rank):
         ctx.barrier()
     wall = time.perf_counter() - wall0
     launches = _lib.kernel_launches() - launches0
+    engine_used = int(stats[-1].engine_used)
 
     # e2e through the public API: depth + parent to pinned host buffers every step
     lv_buf = _lib.pinned_empty(n, np.int32)
@@ -227,7 +232,7 @@ def run_ours(args, world, rank, local_rank):
     roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None if dist else _ncu_traffic(),
             "peak_source": peaks["source"],
-            "kernel": "k_bfs_persistent" if not dist else "k_visit+k_finish",
+            "kernel": "k_visit+k_finish" if engine_used == 1 else "k_bfs_persistent",
             "alg_bytes_per_launch": st_mean_bytes}
 
     line = {
@@ -240,7 +245,8 @@ def run_ours(args, world, rank, local_rank):
                    "scale": scale, "edge_factor": args.edge_factor, "theta": theta, "mode": args.mode,
                    "roots": args.roots, "parents": "valid parent tree written in the timed region",
                    "l2": "flushed between steps (256 MB write); graph also > L2",
-                   "parallelism": f"{world} worker(s), one per GPU" + (" (NCCL)" if dist else "")},
+                   "parallelism": f"{world} worker(s), one per GPU" + (ENGINE_NOTE.get(engine_used, "") if dist else ""),
+                   "engine": {1: "host level loop", 2: "persistent kernel", 3: "peer persistent kernel"}.get(engine_used)},
         "geomean_gteps": round(geomean, 4),
         "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h / args.steps)},

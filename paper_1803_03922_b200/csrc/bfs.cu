@@ -108,6 +108,8 @@ struct AsmArgs {
     int64_t stride;  // dist: gathered arrays are [p][stride]
     const int32_t *dlevel;
     const int64_t *dparent;
+    const int64_t *dpar_src[MAXW];  // peer-mapped: every rank's delegate candidates (min taken here)
+    int n_dpar;
     int32_t *glevel;
     int64_t *gparent;
     int parents;
@@ -119,7 +121,21 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
         uint32_t di = a.del_id[v];
         if (di != 0xffffffffu) {
             a.glevel[v] = a.dlevel[di];
-            if (a.parents) a.gparent[v] = a.dlevel[di] >= 0 ? a.dparent[di] : -1;
+            if (a.parents) {
+                int64_t par = -1;
+                if (a.dlevel[di] >= 0) {
+                    if (a.n_dpar) {
+                        par = 0x7fffffffffffffffLL;
+                        for (int s = 0; s < a.n_dpar; s++) {
+                            const int64_t c = a.dpar_src[s][di];
+                            par = c < par ? c : par;
+                        }
+                    } else {
+                        par = a.dparent[di];
+                    }
+                }
+                a.gparent[v] = par;
+            }
         } else {
             uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
             a.glevel[v] = a.nlevel[w][i];
@@ -135,6 +151,7 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
                                                        AsmArgs asm_args, int do_assemble, GridBar *gbar,
                                                        int nranks) {
     extern __shared__ uint4 dsm[];
+    __shared__ int s_cont;
     Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
     const View &V = views[wsel];
@@ -149,7 +166,10 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     int L = 0;
     for (;; L++) {
         if (L > 0) {
-            bool cont = level_continue(V, L - 1);
+            // one reader per block: in the peer engine these are NVLink loads of the peers' control blocks
+            if (threadIdx.x == 0) s_cont = level_continue(V, L - 1);
+            __syncthreads();
+            const bool cont = s_cont;
             if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
             if (!cont) break;
         }
@@ -505,8 +525,9 @@ static void setup_peer(Graph &g) {
     WorkerHost &Wk = g.workers[0];
     g.gbar_mem.alloc(4);
     DBFS_CUDA(cudaMemset(g.gbar_mem.p, 0, 16));
-    constexpr int NH = 6;
-    void *bases[NH] = {Wk.ctl.p, Wk.dnext0.p, Wk.dnext1.p, Wk.dcand.p, Wk.inbox0.p, g.gbar_mem.p};
+    constexpr int NH = 9;
+    void *bases[NH] = {Wk.ctl.p,    Wk.dnext0.p,  Wk.dnext1.p,  Wk.dcand.p,    Wk.inbox0.p,
+                       Wk.nlevel.p, Wk.nparent.p, Wk.dparent.p, g.gbar_mem.p};
     std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * p);
     for (int i = 0; i < NH && ok; i++)
         if (cudaIpcGetMemHandle(&mine[i], bases[i]) != cudaSuccess) {
@@ -555,7 +576,7 @@ static void setup_peer(Graph &g) {
     View V = g.views_h[0];
     V.peer = 1;
     V.dist = 1;
-    V.cand_all = 1;
+    V.cand_all = 0;  // own candidates only; the min over ranks is taken when outputs are gathered
     V.P_sources = p;
     for (int j = 0; j < p; j++) {
         V.ctl_all[j] = (Ctl *)ptr[(size_t)j * NH + 0];
@@ -573,6 +594,14 @@ static void setup_peer(Graph &g) {
     for (int o = 0; o < p; o++)
         V.sendbin[o] = o == me ? nullptr : (uint2 *)ptr[(size_t)o * NH + 4] + seg(o, me);
     V.inbox[0] = V.inbox[1] = Wk.inbox0.p;
+    g.peer_nlevel.assign(p, nullptr);
+    g.peer_nparent.assign(p, nullptr);
+    g.peer_dparent.assign(p, nullptr);
+    for (int j = 0; j < p; j++) {
+        g.peer_nlevel[j] = (int32_t *)ptr[(size_t)j * NH + 5];
+        g.peer_nparent[j] = (int64_t *)ptr[(size_t)j * NH + 6];
+        g.peer_dparent[j] = (int64_t *)ptr[(size_t)j * NH + 7];
+    }
     g.gbar = ptr[NH - 1];  // rank 0's (its own on rank 0)
     g.peer_view_h = V;
     g.peer_view.alloc(1);
@@ -698,7 +727,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
         iterations = c0.last_level;
         if (engine == 3) {
-            g.assembled = false;  // delegate parents are already the min over ranks (candidates read from peers)
+            g.assembled = false;  // outputs stay distributed until fetched (dist_assemble)
             if (timeout) g.peer_state = -1;  // barrier state unknown: later runs use the NCCL level loop
         }
     } else {
@@ -744,8 +773,6 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         }
         if (!g.dist) iterations = L + 1;
         if (g.dist) {
-            // delegate parents: each rank holds its own candidates -> min over ranks
-            if (parents && g.d) nccl_allreduce_i64(ctx, g.workers[0].dparent.p, g.d, 1);
             g.assembled = false;  // outputs stay distributed until fetched (dist_assemble)
         } else if (assemble) {
             k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
@@ -858,13 +885,33 @@ static void dist_assemble(Graph &g) {
     const bool parents = g.last_parent_mode != 0;
     AsmArgs aa = make_asm(g, parents);
     WorkerHost &Wk = g.workers[0];
+    if (g.peer_state == 1) {
+        // peer-mapped: read every rank's normals and delegate candidates over NVLink,
+        // then a barrier so nobody starts the next BFS while a peer still reads
+        for (int w = 0; w < g.p; w++) {
+            aa.nlevel[w] = g.peer_nlevel[w];
+            aa.nparent[w] = g.peer_nparent[w];
+            aa.dpar_src[w] = g.peer_dparent[w];
+        }
+        aa.n_dpar = g.p;
+        k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(aa);
+        DBFS_LAUNCHED();
+        nccl_barrier(ctx);
+        g.assembled = true;
+        return;
+    }
+    // delegate parents: each rank holds the candidate its own edges found (or
+    // INT64_MAX) -> the tree takes the minimum over ranks
+    if (parents && g.d) nccl_allreduce_i64(ctx, Wk.dparent.p, g.d, 1);
     int64_t stride = ceil_div(g.n, g.p);
-    DArray<int32_t> lv, mylv;
-    DArray<int64_t> pv, mypv;
-    lv.alloc(stride * g.p);
-    pv.alloc(stride * g.p);
-    mylv.alloc(stride);
-    mypv.alloc(stride);
+    DArray<int32_t> &lv = g.asm_lv, &mylv = g.asm_mylv;
+    DArray<int64_t> &pv = g.asm_pv, &mypv = g.asm_mypv;
+    if (lv.n != stride * g.p) {
+        lv.alloc(stride * g.p);
+        pv.alloc(stride * g.p);
+        mylv.alloc(stride);
+        mypv.alloc(stride);
+    }
     DBFS_CUDA(cudaMemsetAsync(mylv.p, 0xff, 4 * stride, ctx.stream));
     DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, 8 * stride, ctx.stream));
     if (Wk.n_local) {

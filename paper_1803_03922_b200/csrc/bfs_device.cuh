@@ -173,9 +173,11 @@ __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, con
         double U = (double)(k == KIND_ND ? u_dn : (k == KIND_DN ? u_nd : u_dd));
         double rows = (double)(V.total_src[rev] ? V.total_src[rev] : 1);
         double avg = (double)V.nnz[rev] / rows;
-        double scan = (double)V.nnz[k] / (double)S.fv[k];
-        if (k == KIND_DD && V.col_sorted_dd) scan = scan < 2.0 ? scan : 2.0;  // hubs first
+        double scan = (double)V.nnz[k] / (double)S.fv[k];  // entries per hit, uniform model
         if (scan > avg) scan = avg;
+        // hubs first: sorted rows reach a frontier hub sooner, but only when the
+        // frontier holds hubs -- a small frontier far from them scans whole rows
+        if (k == KIND_DD && V.col_sorted_dd) scan = scan * 0.5 > 1.0 ? scan * 0.5 : 1.0;
         double words = (double)(rev == KIND_ND ? V.nw_n : V.nw_d);
         double pull = 1.5 * U * scan + 0.25 * words;
         double push = 4.0 * (double)S.fv[k];
@@ -982,10 +984,13 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
 // F2 (distributed only): ingest remote records (engine.py:147-157).
 __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
     if (V.peer) {  // senders stored into fixed segments of this inbox over NVLink
+        __shared__ unsigned long long s_cnt[MAXW];
+        if (threadIdx.x < V.p) s_cnt[threadIdx.x] = __ldcg(&V.ctl_all[threadIdx.x]->s[L % 3].send[V.w]);
+        __syncthreads();
         unsigned long long uq = 0;
         for (int s = 0; s < V.p; s++) {
             if (s == V.w) continue;
-            const unsigned long long cnt = __ldcg(&V.ctl_all[s]->s[L % 3].send[V.w]);
+            const unsigned long long cnt = s_cnt[s];
             const uint2 *seg = V.inbox[0] + V.seg_off[s];
             const int grp = V.local_all2all ? (s % V.p_rank) + V.p_rank * (V.w / V.p_rank) : s;
             for (int64_t i = tid; i < (int64_t)cnt; i += nth) {

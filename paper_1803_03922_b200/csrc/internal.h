@@ -246,6 +246,10 @@ struct Graph {
     View peer_view_h;
     DArray<View> peer_view;
     std::vector<int64_t> cap_all;    // dist: [src][dst] remote record capacities
+    std::vector<int32_t *> peer_nlevel;  // peer-mapped outputs of every rank (assembly over NVLink)
+    std::vector<int64_t *> peer_nparent, peer_dparent;
+    DArray<int32_t> asm_lv, asm_mylv;    // NCCL assembly buffers (kept between runs)
+    DArray<int64_t> asm_pv, asm_mypv;
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();
