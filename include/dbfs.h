@@ -124,6 +124,8 @@ typedef struct {
     double task_max_us[8];      /* worker 0 per-task max warp time */
     double visit_us;            /* device time of the visit phase (worker 0's clock) */
     double finish_us;           /* device time of the barrier/apply phase */
+    double sync_us[4];          /* persistent engines: visit compute (to the last local block), visit cross-GPU
+                                   barrier wait, finish compute, finish cross-GPU wait */
 } dbfs_iteration;
 
 const char *dbfs_last_error(void);

@@ -353,6 +353,12 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
                 r.frontier_delegates = (int64_t)x.dfront;
                 if (x.t[1] > x.t[0]) r.visit_us = (double)(x.t[1] - x.t[0]) / 1e3;
                 if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;
+                if (x.tb[0] > x.t[0] && x.tb[1] >= x.tb[0] && x.tb[2] > x.t[1] && x.tb[3] >= x.tb[2]) {
+                    r.sync_us[0] = (double)(x.tb[0] - x.t[0]) / 1e3;
+                    r.sync_us[1] = (double)(x.tb[1] - x.tb[0]) / 1e3;
+                    r.sync_us[2] = (double)(x.tb[2] - x.t[1]) / 1e3;
+                    r.sync_us[3] = (double)(x.tb[3] - x.tb[2]) / 1e3;
+                }
             }
             records += (int64_t)x.records;
             uq_records += (int64_t)x.uq_records;

@@ -44,8 +44,13 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
 // With `gbar` (peer engine) the last local arriver also meets the other GPUs
 // on a system-scope barrier in rank 0's memory before releasing its GPU, so
 // exactly one thread per GPU polls over NVLink.
+// `cv`: the last arriver also evaluates the termination rule of level
+// `cont_level` (over every worker's / rank's control block) once for the grid
+// and publishes it in cv->ctl->cont before releasing; `ts` gets its
+// local-complete / global-complete timestamps.
 __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBar *gbar = nullptr,
-                                          unsigned nranks = 1) {
+                                          unsigned nranks = 1, const View *cv = nullptr, int cont_level = 0,
+                                          unsigned long long *ts = nullptr) {
     __shared__ int s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -54,6 +59,7 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBa
         else __threadfence();
         unsigned arrived = atomicAdd(&bar->count, 1u);
         if (arrived == nblocks - 1) {
+            if (ts) ts[0] = globaltimer_ns();
             if (gbar) {
                 unsigned ggen = ld_acquire_sys_u32(&gbar->gen);
                 unsigned garr = atomicAdd_system(&gbar->count, 1u);
@@ -74,6 +80,8 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBa
                 }
                 if (ld_acquire_sys_u32(&gbar->abort)) atomicExch(&bar->abort, 1u);
             }
+            if (ts) ts[1] = globaltimer_ns();
+            if (cv) cv->ctl->cont = level_continue(*cv, cont_level) ? 1 : 0;
             atomicExch(&bar->count, 0u);
             __threadfence();
             atomicAdd(&bar->gen, 1u);
@@ -151,7 +159,6 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
                                                        AsmArgs asm_args, int do_assemble, GridBar *gbar,
                                                        int nranks) {
     extern __shared__ uint4 dsm[];
-    __shared__ int s_cont;
     Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
     const View &V = views[wsel];
@@ -166,16 +173,15 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     int L = 0;
     for (;; L++) {
         if (L > 0) {
-            // one reader per block: in the peer engine these are NVLink loads of the peers' control blocks
-            if (threadIdx.x == 0) s_cont = level_continue(V, L - 1);
-            __syncthreads();
-            const bool cont = s_cont;
+            // evaluated once by the barrier's last arriver (NVLink loads in the peer engine)
+            const bool cont = __ldcg(&views[0].ctl->cont) != 0;
             if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
             if (!cont) break;
         }
         if (timer && L < rec_cap) V.rec[L].t[0] = globaltimer_ns();
+        unsigned long long *tb = L < rec_cap ? views[0].rec[L].tb : nullptr;
         phase_visit(V, L, wb, nb, sm);
-        if (!grid_sync(bar, nblocks, gbar, nranks)) return;
+        if (!grid_sync(bar, nblocks, gbar, nranks, nullptr, 0, tb)) return;
         if (timer && L < rec_cap) V.rec[L].t[1] = globaltimer_ns();
         if (V.peer) {  // peers' records are claimed before the frontier is folded
             phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_INGEST);
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
         } else {
             phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
         }
-        if (!grid_sync(bar, nblocks, gbar, nranks)) return;
+        if (!grid_sync(bar, nblocks, gbar, nranks, &views[0], L, tb ? tb + 2 : nullptr)) return;
         if (timer && L < rec_cap) V.rec[L].t[2] = globaltimer_ns();
     }
     if (wb == 0 && threadIdx.x == 0) V.ctl->last_level = L;

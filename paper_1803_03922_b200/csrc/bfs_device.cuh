@@ -617,16 +617,54 @@ __device__ __forceinline__ PullRes warp_scan_row(const uint32_t *__restrict__ co
 // One pull kind over its candidate words.  cand(wi) gives the candidate bits
 // of word wi; rows come from (off, col); `front` is the parent status bitmap;
 // on_hit(candidate, hit column) records the find.
+// Chunks [0, n) of 32 bitmap words over the warps of one worker: chunk gw
+// first, then chunks claimed from a per-level counter, prefetched one chunk
+// ahead so the atomic's latency hides behind the current chunk.  Degree skew
+// makes chunk costs uneven; claiming on demand keeps warps finishing together.
+#ifndef DBFS_DYN
+#define DBFS_DYN 1
+#endif
+#ifndef DBFS_CWD
+#define DBFS_CWD 8   // bitmap words per chunk over delegates (d/32 words: few, heavy)
+#endif
+#ifndef DBFS_CWN
+#define DBFS_CWN 32  // bitmap words per chunk over normals
+#endif
+struct WarpChunks {
+    unsigned *ctr;  // nullptr: static stride (light levels, where a claim costs more than a chunk)
+    int n, TW, cur, cw;
+    unsigned pend;
+    __device__ __forceinline__ WarpChunks(unsigned *c, int64_t nwords, int cw_, int64_t gw, int64_t tw)
+        : ctr(DBFS_DYN ? c : nullptr), n((int)((nwords + cw_ - 1) / cw_)), TW((int)tw), cur((int)gw), cw(cw_) {
+        pend = (ctr && lane_id() == 0 && cur < n) ? atomicAdd(ctr, 1u) : 0u;
+    }
+    __device__ __forceinline__ bool valid() const { return cur < n; }
+    __device__ __forceinline__ int64_t base() const { return (int64_t)cur * cw; }
+    // lane's word of the chunk, or -1
+    __device__ __forceinline__ int64_t word(int64_t nwords) const {
+        const int64_t wi = base() + lane_id();
+        return ((int)lane_id() < cw && wi < nwords) ? wi : -1;
+    }
+    __device__ __forceinline__ void next() {
+        if (!ctr) {
+            cur += TW;
+            return;
+        }
+        cur = TW + (int)__shfl_sync(FULL, pend, 0);
+        pend = (lane_id() == 0 && cur < n) ? atomicAdd(ctr, 1u) : 0u;
+    }
+};
+
 template <class CandF, class HitF>
-__device__ __forceinline__ void pull_kind(int64_t nw, int64_t gw, int64_t TW, uint32_t *list,
+__device__ __forceinline__ void pull_kind(int64_t nw, int cw, int64_t gw, int64_t TW, unsigned *sched, uint32_t *list,
                                           const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
                                           const uint32_t *__restrict__ front, const uint32_t *filt,
                                           unsigned long long &insp, unsigned long long &rows, CandF cand,
                                           HitF on_hit) {
     const unsigned lane = lane_id();
-    for (int64_t base = gw * 32; base < nw; base += TW * 32) {
-        int64_t wi = base + lane;
-        uint32_t word = wi < nw ? cand(wi) : 0u;
+    for (WarpChunks ch(sched, nw, cw, gw, TW); ch.valid(); ch.next()) {
+        const int64_t wi = ch.word(nw);
+        uint32_t word = wi >= 0 ? cand(wi) : 0u;
         unsigned cnt = warp_compact(word, wi, list);
         if (lane == 0) rows += cnt;
         // First probe of 4 groups at once (4 independent chains per lane):
@@ -687,6 +725,15 @@ __device__ __forceinline__ void warp_mark(uint32_t *bm, bool hit, uint32_t v) {
     if (hit && (int)lane_id() == __ffs(peers) - 1) atomicOr(&bm[v >> 5], bits);
 }
 
+// Pulls of kind k are balanced dynamically when many candidates remain (the
+// unvisited sources of the reverse kind), statically on light tail levels.
+__device__ __forceinline__ bool dyn_pull(const View &V, const unsigned long long *cum, int k, int64_t TW) {
+    unsigned long long U, Q, Sx;
+    const unsigned long long q0[4] = {0, 0, 0, 0};
+    level_inputs(V.total_src, cum, q0, k, U, Q, Sx);
+    return U > 32ull * (unsigned long long)TW;
+}
+
 // -------------------------------------------------------------- phase V(L)
 
 __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
@@ -720,10 +767,11 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (S.nfront > 0) {
         const bool nd_fwd = ex[KIND_ND] == FWD;
         const uint32_t *has_nn = V.src_bits[KIND_NN], *has_nd = V.src_bits[KIND_ND];
-        for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
-            int64_t wi = base + lane;
+        for (WarpChunks ch(S.nfront > (unsigned long long)TW ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW);
+             ch.valid(); ch.next()) {
+            const int64_t wi = ch.word(V.nw_n);
             // only frontier vertices with an nn row (or an nd row when nd pushes)
-            uint32_t word = wi < V.nw_n ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
+            uint32_t word = wi >= 0 ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
             unsigned cnt = warp_compact(word, wi, list);
             for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
                 unsigned i = g0 + lane;
@@ -781,7 +829,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (ex[KIND_DN] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_ND];
         const uint32_t *nvis = V.nvis;
-        pull_kind(V.nw_n, gw, TW, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
+        pull_kind(V.nw_n, DBFS_CWN, gw, TW, dyn_pull(V, cum, KIND_DN, TW) ? &AT.sched[1] : nullptr, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](bool hit, uint32_t c, uint32_t x) {
                       warp_mark(V.nfront[(L + 1) & 1], hit, c);
@@ -801,7 +849,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         // sorted by neighbour degree (hubs first); reported BACKWARD: the
         // reference order, whose early-exit position is the counter.
         const uint32_t *cdd = (dirs[KIND_DD] == FWD && V.col_sorted_dd) ? V.col_sorted_dd : V.col[KIND_DD];
-        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DD], cdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
+        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_DD, TW) ? &AT.sched[2] : nullptr, list, V.off[KIND_DD], cdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
                   [&](bool hit, uint32_t x, uint32_t y) {
                       warp_mark(V.dnext[L & 1], hit, x);
@@ -824,7 +872,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (ex[KIND_ND] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_DN];
         const uint32_t *dvis = V.dvis;
-        pull_kind(V.nw_d, gw, TW, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
+        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_ND, TW) ? &AT.sched[3] : nullptr, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
                   vc.insp_bwd[KIND_ND], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
                   [&](bool hit, uint32_t x, uint32_t c) {
@@ -902,10 +950,12 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     const unsigned lane = lane_id();
     uint32_t *next_mask = V.dnext[(L + 1) & 1];
     LevelSlot &N = V.ctl->s[(L + 1) % 3];
-    for (int64_t base = gw * 32; base < V.nw_d; base += TW * 32) {
-        int64_t wi = base + lane;
+    const bool dyn = V.ctl->s[L % 3].dirty != 0;  // delegates were found: new-delegate work to balance
+    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, DBFS_CWD, gw, TW); ch.valid(); ch.next()) {
+        const int64_t base = ch.base();
+        const int64_t wi = ch.word(V.nw_d);
         uint32_t nw = 0u;
-        if (wi < V.nw_d) {
+        if (wi >= 0) {
             uint32_t r = 0;
             for (int s = 0; s < V.P_sources; s++) r |= __ldcg(&V.mask_src[L & 1][s][wi]);
             uint32_t dv = V.dvis[wi];
@@ -1030,10 +1080,13 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
     const unsigned lane = lane_id();
     uint32_t *cur = V.nfront[L & 1];
     const uint32_t *nxt = V.nfront[(L + 1) & 1];
-    for (int64_t base = gw * 32; base < V.nw_n; base += TW * 32) {
-        int64_t wi = base + lane;
+    const LevelSlot &A = V.ctl->s[L % 3];
+    const bool dyn = A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
+    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[5] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
+        const int64_t base = ch.base();
+        const int64_t wi = ch.word(V.nw_n);
         uint32_t nw = 0u;
-        if (wi < V.nw_n) {
+        if (wi >= 0) {
             if (cur[wi]) cur[wi] = 0u;
             nw = nxt[wi];
             if (nw) V.nvis[wi] |= nw;

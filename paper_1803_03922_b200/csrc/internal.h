@@ -37,6 +37,7 @@ struct LevelSlot {
     int exec_dir[4];                 // executed strategy per kind (may differ from the reported one)
     unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
     unsigned long long tmax[8];      // per-task warp cycles: max over warps
+    unsigned int sched[8];           // dynamic chunk counters: T1, T4, T6, T5, F1, F3
     unsigned long long send[MAXW];   // records per destination worker
 };
 
@@ -48,7 +49,7 @@ struct Ctl {
     unsigned int abort;              // watchdog / error flag
     int last_level;                  // iterations when the loop ended
     unsigned long long t_start, t_seeded;  // globaltimer: kernel start, after init+seed
-    int cont;                        // host-loop: continue flag
+    int cont;                        // persistent engine: termination rule of the last level (1 = go on)
     int pad;
 };
 
@@ -69,6 +70,7 @@ struct IterRec {
     unsigned long long tsum[8], tmax[8];
     unsigned long long nfront, dfront;
     unsigned long long t[3];         // globaltimer at V start, V end, F end (persistent engine)
+    unsigned long long tb[4];        // last arriver at the V / F barriers: all local blocks in, all GPUs in
     unsigned long long send[MAXW];
 };
 
