@@ -158,7 +158,8 @@ def run_ours(args, world, rank, local_rank):
 
     scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
-    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40)
+    scrambled = args.labeling == "scrambled"
+    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, scramble=scrambled)
     t0 = time.perf_counter()
     pg = api.partition_graph(api.build_rmat_graph(params), theta,
                              api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
@@ -224,6 +225,7 @@ def run_ours(args, world, rank, local_rank):
         if api.validate_bfs_tree(pg, r) != 0:
             raise SystemExit(f"Graph500 certificate failed for root {r}")
         validated += 1
+    imbalance = _load_imbalance(ctx, pg, dist)
 
     peaks = measured_peaks()
     st_mean_bytes = float(np.mean([alg_bytes(s, n) for s in stats]))
@@ -259,13 +261,54 @@ def run_ours(args, world, rank, local_rank):
                                            for s in stats])),
         "executed_inspections_mean": float(np.mean([s.work_inspections for s in stats])),
     }
+    line["config"]["labeling"] = ("reference hash_randomize_vertices + Feistel relabeling (balanced v mod p owners)"
+                                  if scrambled else "reference hash_randomize_vertices")
+    line["worker_edges_max_over_mean"] = imbalance
     if rank == 0 and not args.no_cpu_baseline and not dist:
         line["cpu_baseline"] = cpu_baseline_same_graph(pg, roots, args, n, m)
+    if scrambled and not args.no_alt_labeling:
+        # the same workload on the reference's own labeling, device time only
+        pg.close()
+        del pg
+        line["reference_labeling"] = _device_series(api, ctx, args, scale, theta, world, dist)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         tdist.barrier()
         tdist.destroy_process_group()
+
+
+def _load_imbalance(ctx, pg, dist):
+    """max over workers of the worker's edge count / mean edge count."""
+    loads = np.array([[float(sum(w.sizes()[1])) for w in pg.workers]], dtype=np.float64).ravel()
+    mx = float(loads.max())
+    if dist:
+        mx = float(_allreduce_max(ctx, np.array([mx]))[0])
+    return round(mx / (pg.m / pg.shape.p), 3) if pg.m else 1.0
+
+
+def _device_series(api, ctx, args, scale, theta, world, dist):
+    from paper_1803_03922_b200.engine import bfs_device
+    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40)
+    pg = api.partition_graph(api.build_rmat_graph(params), theta,
+                             api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
+    roots = graph500_roots(pg.classification.out_degree, args.roots)
+    for i in range(args.warmup):
+        bfs_device(pg, roots[i % len(roots)], mode=args.mode)
+    if dist:
+        ctx.barrier()
+    dev_ms = []
+    for i in range(args.steps):
+        ctx.flush_l2()
+        dev_ms.append(bfs_device(pg, roots[i % len(roots)], mode=args.mode).device_ms)
+    if dist:
+        dev_ms = list(_allreduce_max(ctx, np.array(dev_ms, dtype=np.float64)))
+    out = {"value": round(args.steps * (pg.m / 2) / (sum(dev_ms) / 1e3) / 1e9, 4), "unit": UNIT,
+           "ms_per_step": round(float(np.mean(dev_ms)), 4),
+           "worker_edges_max_over_mean": _load_imbalance(ctx, pg, dist),
+           "note": "reference labeling: owners v mod p inherit the hash's low-bit degree skew"}
+    pg.close()
+    return out
 
 
 def _allreduce_max(ctx, arr):
@@ -316,6 +359,9 @@ def cpu_baseline_same_graph(pg, roots, args, n, m):
 
 # ------------------------------------------------------------- reference arm
 
+REF_SCALE_CAP = 24
+
+
 def run_reference(args, world, rank):
     """The reference's CPU path on this host: the oracle port (oracle/, a C
     restatement of delegate_bfs run_bfs), rank 0 only."""
@@ -325,8 +371,13 @@ def run_reference(args, world, rank):
     from paper_1803_03922_b200.dist import weak_scale
     scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
+    # host memory/time bound: graphs above scale 24 are sampled at scale 24
+    # (GTEPS of this traversal is nearly scale-independent), same labeling
+    cpu_scale = min(scale, REF_SCALE_CAP)
+    cpu_theta = args.theta if args.theta is not None else suggested_theta(cpu_scale)
     t0 = time.perf_counter()
-    og = O.partition_rmat(scale, theta, 1, world, edge_factor=args.edge_factor, load_arrays=False)
+    og = O.partition_rmat(cpu_scale, cpu_theta, 1, world, edge_factor=args.edge_factor, load_arrays=False,
+                          scramble=args.labeling == "scrambled")
     deg = _oracle_degrees(og, O)
     build_s = time.perf_counter() - t0
     roots = graph500_roots(deg, args.roots)
@@ -346,9 +397,10 @@ def run_reference(args, world, rank):
         "data": "synthetic RMAT (Graph500 quadrants, seed 0), generated on the host",
         "config": {"workload": f"RMAT scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
                                f"{args.roots} Graph500 roots, CPU", "scale": scale, "theta": theta,
-                   "mode": args.mode, "roots": args.roots, "shape": f"1x1x{world}"},
+                   "mode": args.mode, "roots": args.roots, "shape": f"1x1x{world}", "labeling": args.labeling},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} BFS runs over the {args.roots} roots, "
+                         "sample": f"{args.steps} BFS runs over the {args.roots} roots of the scale-{cpu_scale} "
+                                   f"graph (theta {cpu_theta}, {world} simulated workers), "
                                    "oracle/dbfs_oracle.c (C restatement of engine.run_bfs), single thread"},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build_s": round(build_s, 2),
@@ -376,16 +428,31 @@ def main():
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--labeling", choices=["scrambled", "reference"], default="scrambled",
+                    help="vertex labels: the reference hash, plus (default) this build's Feistel relabeling")
+    ap.add_argument("--no-alt-labeling", action="store_true",
+                    help="skip the extra device-time series on the reference labeling")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         ap.error("need steps >= 1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-    else:
-        run_ours(args, world, rank, local_rank)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local_rank)
+    except BaseException:
+        if world > 1:
+            # one failed rank must not leave the others blocked in a collective:
+            # exit hard so the launcher tears the job down
+            import traceback
+            traceback.print_exc()
+            sys.stderr.flush()
+            sys.stdout.flush()
+            os._exit(1)
+        raise
 
 
 if __name__ == "__main__":

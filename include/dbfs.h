@@ -55,7 +55,7 @@ typedef struct {
     int32_t scale;
     int32_t randomize;   /* hash_randomize_vertices(g, seed) */
     int32_t symmetrize;  /* symmetrize(g) */
-    int32_t _pad;
+    int32_t scramble;    /* this build: Feistel relabeling after the hash (balanced v mod p owners) */
     int64_t edge_factor;
     double a, b, c;      /* d = 1 - a - b - c */
     uint64_t seed;

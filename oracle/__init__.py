@@ -59,6 +59,8 @@ def lib():
         "orc_hash_vertices": (c_int, [i64, u64, vp, vp, i64]),
         "orc_partition": (c_int, [vp, vp, i64, i64, i64, c_int, c_int, ctypes.POINTER(vp)]),
         "orc_partition_rmat": (c_int, [c_int, i64, c_double, c_double, c_double, u64, i64, c_int, c_int, ctypes.POINTER(vp)]),
+        "orc_partition_rmat_flags": (c_int, [c_int, i64, c_double, c_double, c_double, u64, c_int, i64, c_int, c_int,
+                                             ctypes.POINTER(vp)]),
         "orc_graph_free": (None, [vp]),
         "orc_graph_new": (vp, [i64, i64, i64, c_int, c_int, i64, vp]),
         "orc_graph_set_csr": (c_int, [vp, c_int, c_int, i64, vp, vp]),
@@ -118,14 +120,16 @@ def _view(ptr, count, dtype):
 # ---------------------------------------------------------------- generation
 
 def rmat_edges(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=0, randomize=True,
-               symmetrize=True, begin=0, end=None):
-    """Edges [begin, end) of build_rmat_graph (rmat.py:125-208)."""
+               symmetrize=True, begin=0, end=None, scramble=False):
+    """Edges [begin, end) of build_rmat_graph (rmat.py:125-208); ``scramble``
+    adds this build's Feistel relabeling after the reference hash."""
     m0 = (1 << scale) * edge_factor
     m = 2 * m0 if symmetrize else m0
     end = m if end is None else end
     src = np.empty(end - begin, dtype=np.int64)
     dst = np.empty(end - begin, dtype=np.int64)
-    _check(lib().orc_rmat_edges(scale, edge_factor, a, b, c, seed & (2**64 - 1), int(randomize),
+    _check(lib().orc_rmat_edges(scale, edge_factor, a, b, c, seed & (2**64 - 1),
+                                int(bool(randomize)) | (2 if scramble else 0),
                                 int(symmetrize), begin, end, _ptr(src), _ptr(dst)), "rmat")
     return src, dst
 
@@ -196,9 +200,9 @@ def partition(src, dst, n, theta, p_rank=1, p_gpu=1) -> OracleGraph:
 
 
 def partition_rmat(scale, theta, p_rank=1, p_gpu=1, edge_factor=16, a=0.57, b=0.19, c=0.19,
-                   seed=0, load_arrays=True) -> OracleGraph:
+                   seed=0, load_arrays=True, scramble=False) -> OracleGraph:
     h = vp()
-    _check(lib().orc_partition_rmat(scale, edge_factor, a, b, c, seed & (2**64 - 1), theta,
+    _check(lib().orc_partition_rmat_flags(scale, edge_factor, a, b, c, seed & (2**64 - 1), 3 if scramble else 1, theta,
                                     p_rank, p_gpu, ctypes.byref(h)), "partition_rmat")
     return OracleGraph(h, load_arrays=load_arrays)
 

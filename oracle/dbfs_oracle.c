@@ -72,9 +72,10 @@ typedef struct {
     int64_t n, m0;
     uint64_t key;
     uint64_t ta, tab, tabc;
-    int randomize;
+    int randomize;               /* bit 0: reference hash; bit 1: Feistel scramble (this build) */
     uint64_t mask, c1, m1, m2;
     int s1, s2;
+    uint64_t skey;
 } rmat_gen;
 
 static void rmat_gen_init(rmat_gen *g, int scale, int64_t ef, double a, double b,
@@ -96,6 +97,7 @@ static void rmat_gen_init(rmat_gen *g, int scale, int64_t ef, double a, double b
     g->c1 = mix64(seed) & g->mask;
     g->m1 = (0x9E3779B97F4A7C15ULL & 0x7FFFFFFFFFFFFFFFULL) | 1ULL;
     g->m2 = (0xBF58476D1CE4E5B9ULL & 0x7FFFFFFFFFFFFFFFULL) | 1ULL;
+    g->skey = mix64(seed ^ 0x5CA3B1E5D00DF00DULL);
 }
 
 static inline uint64_t hash_perm(const rmat_gen *g, uint64_t v) { /* rmat.py:173-180 */
@@ -105,6 +107,23 @@ static inline uint64_t hash_perm(const rmat_gen *g, uint64_t v) { /* rmat.py:173
     v = (v * g->m2) & g->mask;
     v ^= (v << g->s2) & g->mask;
     return v;
+}
+
+/* Optional relabeling of this build (not in the reference): a 3-round Feistel
+ * bijection on the scale bits, applied after the reference hash.  The
+ * reference hash keeps low id bits a function of low bits only, so owners
+ * v mod p inherit RMAT's bit-pattern degree skew; the scramble makes every id
+ * bit depend on all of them.  Same function as csrc/build.cu scramble(). */
+static inline uint64_t scramble(const rmat_gen *g, uint64_t v) {
+    int k = g->scale;
+    if (k < 2) return v;
+    int j = k / 2;
+    uint64_t lm = (1ULL << j) - 1, hm = (1ULL << (k - j)) - 1;
+    uint64_t lo = v & lm, hi = v >> j;
+    lo ^= mix64(hi ^ g->skey) & lm;
+    hi ^= mix64(lo ^ (g->skey + 1)) & hm;
+    lo ^= mix64(hi ^ (g->skey + 2)) & lm;
+    return (hi << j) | lo;
 }
 
 /* One original (undoubled) RMAT edge, rmat.py:139-148. */
@@ -118,9 +137,13 @@ static inline void rmat_edge(const rmat_gen *g, uint64_t e, uint64_t *u, uint64_
         su |= ub << (g->scale - 1 - l);
         sv |= vb << (g->scale - 1 - l);
     }
-    if (g->randomize) {
+    if (g->randomize & 1) {
         su = hash_perm(g, su);
         sv = hash_perm(g, sv);
+    }
+    if (g->randomize & 2) {
+        su = scramble(g, su);
+        sv = scramble(g, sv);
     }
     *u = su;
     *v = sv;
@@ -371,9 +394,20 @@ int orc_partition(const int64_t *src, const int64_t *dst, int64_t m, int64_t n,
 
 /* Build the partition straight from RMAT parameters (same result as
  * partition_graph(build_rmat_graph(params), ...)). */
+int orc_partition_rmat_flags(int scale, int64_t edge_factor, double a, double b, double c,
+                             uint64_t seed, int gen_flags, int64_t theta, int p_rank, int p_gpu,
+                             orc_graph **out);
+
 int orc_partition_rmat(int scale, int64_t edge_factor, double a, double b, double c,
                        uint64_t seed, int64_t theta, int p_rank, int p_gpu,
                        orc_graph **out) {
+    return orc_partition_rmat_flags(scale, edge_factor, a, b, c, seed, 1, theta, p_rank, p_gpu, out);
+}
+
+/* gen_flags: the `randomize` bits of orc_rmat_edges (1 = reference hash, 3 = + scramble). */
+int orc_partition_rmat_flags(int scale, int64_t edge_factor, double a, double b, double c,
+                             uint64_t seed, int gen_flags, int64_t theta, int p_rank, int p_gpu,
+                             orc_graph **out) {
     *out = NULL;
     if (scale < 0 || scale > 36 || edge_factor < 1) return ORC_EINVAL;
     int64_t n = (int64_t)1 << scale;
@@ -381,7 +415,7 @@ int orc_partition_rmat(int scale, int64_t edge_factor, double a, double b, doubl
     int64_t *src = malloc(m * sizeof(int64_t));
     int64_t *dst = malloc(m * sizeof(int64_t));
     if (!src || !dst) { free(src); free(dst); return ORC_ENOMEM; }
-    int rc = orc_rmat_edges(scale, edge_factor, a, b, c, seed, 1, 1, 0, m, src, dst);
+    int rc = orc_rmat_edges(scale, edge_factor, a, b, c, seed, gen_flags, 1, 0, m, src, dst);
     if (rc == ORC_OK) rc = orc_partition(src, dst, m, n, theta, p_rank, p_gpu, out);
     free(src);
     free(dst);

@@ -35,7 +35,7 @@ class DbfsError(RuntimeError):
 
 
 class RmatParamsC(ctypes.Structure):
-    _fields_ = [("scale", i32), ("randomize", i32), ("symmetrize", i32), ("_pad", i32),
+    _fields_ = [("scale", i32), ("randomize", i32), ("symmetrize", i32), ("scramble", i32),
                 ("edge_factor", i64), ("a", dbl), ("b", dbl), ("c", dbl), ("seed", u64)]
 
 

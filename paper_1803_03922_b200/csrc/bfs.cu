@@ -336,7 +336,8 @@ static void ensure_resources(Graph &g) {
             V.nnz[k] = (unsigned long long)Wk.nnz[k];
         }
         V.del_gid = g.del_gid.p;
-        V.col_sorted_dd = g.col_sorted.n ? g.col_sorted.p : nullptr;
+        // indexed with absolute dd offsets (the worker's copy starts at dd_base)
+        V.col_sorted_dd = Wk.col_sorted.n ? Wk.col_sorted.p - Wk.dd_base : nullptr;
         V.nlevel = Wk.nlevel.p;
         V.nparent = Wk.nparent.p;
         V.dlevel = Wk.dlevel.p;

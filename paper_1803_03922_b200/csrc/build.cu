@@ -13,6 +13,8 @@
 //   k_src_bits    nd_source_list / dn_source_mask / dd_source_mask
 //                 (partition.py:330-332) as bitmaps
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -24,8 +26,9 @@ namespace dbfs {
 struct RmatGen {
     int scale;
     int randomize;
+    int scramble;     // Feistel relabeling after the reference hash (this build's option)
     int64_t m0;       // undoubled edges
-    uint64_t key, ta, tab, tabc, mask, c1, m1, m2;
+    uint64_t key, ta, tab, tabc, mask, c1, m1, m2, skey;
     int s1, s2;
 };
 
@@ -67,7 +70,24 @@ static RmatGen make_gen(const dbfs_rmat_params &p) {
     g.c1 = mix64(p.seed) & g.mask;
     g.m1 = (0x9E3779B97F4A7C15ULL & 0x7FFFFFFFFFFFFFFFULL) | 1ULL;
     g.m2 = (0xBF58476D1CE4E5B9ULL & 0x7FFFFFFFFFFFFFFFULL) | 1ULL;
+    g.scramble = p.scramble;
+    g.skey = mix64(p.seed ^ 0x5CA3B1E5D00DF00DULL);
     return g;
+}
+
+// 3-round Feistel bijection on the scale bits (oracle/dbfs_oracle.c scramble()):
+// the reference hash keeps low id bits a function of low bits only, so owners
+// v mod p inherit RMAT's bit-pattern degree skew; this mixes all bits.
+__host__ __device__ __forceinline__ uint64_t scramble(const RmatGen &g, uint64_t v) {
+    const int k = g.scale;
+    if (k < 2) return v;
+    const int j = k / 2;
+    const uint64_t lm = (1ULL << j) - 1, hm = (1ULL << (k - j)) - 1;
+    uint64_t lo = v & lm, hi = v >> j;
+    lo ^= mix64(hi ^ g.skey) & lm;
+    hi ^= mix64(lo ^ (g.skey + 1)) & hm;
+    lo ^= mix64(hi ^ (g.skey + 2)) & lm;
+    return (hi << j) | lo;
 }
 
 __device__ __forceinline__ uint64_t hash_perm(const RmatGen &g, uint64_t v) {  // rmat.py:173-180
@@ -93,6 +113,10 @@ __device__ __forceinline__ void rmat_edge(const RmatGen &g, uint64_t e, uint32_t
     if (g.randomize) {
         su = (uint32_t)hash_perm(g, su);
         sv = (uint32_t)hash_perm(g, sv);
+    }
+    if (g.scramble) {
+        su = (uint32_t)scramble(g, su);
+        sv = (uint32_t)scramble(g, sv);
     }
     u = su;
     v = sv;
@@ -489,6 +513,14 @@ static void classify(Graph &g) {
 
 static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end);
 
+void mem_note(const Ctx &ctx, const char *what) {
+    static const bool on = getenv("DBFS_VERBOSE") && getenv("DBFS_VERBOSE")[0] == '1';
+    if (!on) return;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    fprintf(stderr, "[dbfs rank %d dev %d] %s: %zu MiB free of %zu\n", ctx.rank, ctx.device, what, fr >> 20, tot >> 20);
+}
+
 void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm) {
     Ctx &ctx = *g.ctx;
     DBFS_CHECK(prm.scale >= 0 && prm.scale <= 32 && prm.edge_factor >= 1, DBFS_EINVAL, "bad RMAT params");
@@ -514,7 +546,9 @@ void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm) {
     }
     if (g.dist) nccl_allreduce_u32_sum(ctx, g.degree.p, g.n);
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    mem_note(ctx, "degrees");
     classify(g);
+    mem_note(ctx, "classified");
     if (g.dist) {
         int64_t per = ceil_div(g.m, ctx.nranks);
         int64_t b = std::min(g.m, per * ctx.rank), e = std::min(g.m, b + per);
@@ -634,35 +668,51 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
     DBFS_CUDA(cudaMemcpy(dwbase.p, wbase.data(), 8 * p * 4, cudaMemcpyHostToDevice));
     const int64_t ml = end - begin;
     const int blocks = ctx.num_sms * 16;
-    DArray<unsigned long long> kt, dcnt;
+    // The slice is routed in chunks of <= 2^29 edges (bounded temporaries,
+    // 32-bit indices at any scale).  A counting pass sizes every (source rank,
+    // chunk) segment first, so each chunk's all-to-all lands at its place in
+    // global edge order on the receiver.
+    const int64_t CH = (int64_t)1 << 29;
+    int64_t nch = std::max<int64_t>(1, ceil_div(ml, CH));
+    {
+        DArray<int64_t> t;
+        t.alloc(1);
+        DBFS_CUDA(cudaMemcpy(t.p, &nch, 8, cudaMemcpyHostToDevice));
+        nccl_allreduce_i64(ctx, t.p, 1, 2);  // max over ranks: the chunk loop is collective
+        DBFS_CUDA(cudaMemcpy(&nch, t.p, 8, cudaMemcpyDeviceToHost));
+    }
+    const int64_t cap = std::max<int64_t>(1, std::min(ml, CH));
+    auto chunk = [&](int64_t c, int64_t &c0, int64_t &c1) {
+        c0 = std::min(end, begin + c * CH);
+        c1 = std::min(end, c0 + CH);
+    };
+    DArray<unsigned long long> kt, dcnt, kt_dummy;
     kt.alloc(4);
+    kt_dummy.alloc(4);
     dcnt.alloc(MAXW);
     DBFS_CUDA(cudaMemsetAsync(kt.p, 0, kt.bytes(), ctx.stream));
-    DBFS_CUDA(cudaMemsetAsync(dcnt.p, 0, dcnt.bytes(), ctx.stream));
-    DArray<uint2> sbuf;
-    sbuf.alloc(std::max<int64_t>(ml, 1));
-    {
-        DArray<uint32_t> dest, keys, vals, idx, dest2, idx2;
-        dest.alloc(std::max<int64_t>(ml, 1));
-        keys.alloc(std::max<int64_t>(ml, 1));
-        vals.alloc(std::max<int64_t>(ml, 1));
-        idx.alloc(std::max<int64_t>(ml, 1));
-        dest2.alloc(std::max<int64_t>(ml, 1));
-        idx2.alloc(std::max<int64_t>(ml, 1));
-        if (ml > 0) {
-            k_route_dest<<<blocks, 256, 0, ctx.stream>>>(es, begin, end, g.degree.p, g.del_id.p, pd, dwbase.p, dest.p,
-                                                         keys.p, vals.p, kt.p);
-            DBFS_LAUNCHED();
-            k_count_dest<<<blocks, 256, 0, ctx.stream>>>(dest.p, ml, dcnt.p);
-            DBFS_LAUNCHED();
-            k_iota<<<blocks, 256, 0, ctx.stream>>>(idx.p, ml);
-            DBFS_LAUNCHED();
-            bool alt = false;  // stable bucket by destination (edge order kept inside a bucket)
-            radix_sort_pairs(ctx, dest.p, idx.p, dest2.p, idx2.p, ml, std::max(1, bits_for(p)), &alt);
-            k_pack_records<<<blocks, 256, 0, ctx.stream>>>(alt ? idx2.p : idx.p, keys.p, vals.p, ml, sbuf.p);
-            DBFS_LAUNCHED();
-        }
-        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    DArray<uint32_t> dest, keys, vals, idx, dest2, idx2;
+    dest.alloc(cap);
+    keys.alloc(cap);
+    vals.alloc(cap);
+    idx.alloc(cap);
+    dest2.alloc(cap);
+    idx2.alloc(cap);
+    // pass 1: records per (chunk, destination)
+    std::vector<int64_t> cnt_local((size_t)nch * p, 0);
+    for (int64_t c = 0; c < nch; c++) {
+        int64_t c0, c1;
+        chunk(c, c0, c1);
+        if (c1 <= c0) continue;
+        DBFS_CUDA(cudaMemsetAsync(dcnt.p, 0, dcnt.bytes(), ctx.stream));
+        k_route_dest<<<blocks, 256, 0, ctx.stream>>>(es, c0, c1, g.degree.p, g.del_id.p, pd, dwbase.p, dest.p, keys.p,
+                                                     vals.p, kt.p);
+        DBFS_LAUNCHED();
+        k_count_dest<<<blocks, 256, 0, ctx.stream>>>(dest.p, c1 - c0, dcnt.p);
+        DBFS_LAUNCHED();
+        std::vector<unsigned long long> h(MAXW);
+        DBFS_CUDA(cudaMemcpy(h.data(), dcnt.p, 8 * MAXW, cudaMemcpyDeviceToHost));
+        for (int o = 0; o < p; o++) cnt_local[(size_t)c * p + o] = (int64_t)h[o];
     }
     // global kind totals
     {
@@ -676,36 +726,67 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
         DBFS_CUDA(cudaMemcpy(hv, t.p, sizeof(hv), cudaMemcpyDeviceToHost));
         for (int k = 0; k < 4; k++) g.kind_totals[k] = hv[k];
     }
-    // counts exchange, then the record all-to-all
-    std::vector<int64_t> scount(p);
+    // every rank's counts [source][chunk][dest]
+    const int64_t CPS = nch * p;
+    std::vector<int64_t> all((size_t)p * CPS);
     {
-        std::vector<unsigned long long> h(MAXW);
-        DBFS_CUDA(cudaMemcpy(h.data(), dcnt.p, 8 * MAXW, cudaMemcpyDeviceToHost));
-        for (int o = 0; o < p; o++) scount[o] = (int64_t)h[o];
+        DArray<int64_t> sc, rc;
+        sc.alloc(CPS);
+        rc.alloc((int64_t)p * CPS);
+        DBFS_CUDA(cudaMemcpy(sc.p, cnt_local.data(), 8 * CPS, cudaMemcpyHostToDevice));
+        nccl_allgather_bytes(ctx, sc.p, rc.p, 8 * CPS);
+        DBFS_CUDA(cudaMemcpy(all.data(), rc.p, 8 * p * CPS, cudaMemcpyDeviceToHost));
     }
-    DArray<int64_t> sc, rc;
-    sc.alloc(p);
-    rc.alloc((int64_t)p * p);
-    DBFS_CUDA(cudaMemcpy(sc.p, scount.data(), 8 * p, cudaMemcpyHostToDevice));
-    nccl_allgather_bytes(ctx, sc.p, rc.p, 8 * p);
-    std::vector<int64_t> all((size_t)p * p);
-    DBFS_CUDA(cudaMemcpy(all.data(), rc.p, 8 * p * p, cudaMemcpyDeviceToHost));
-    std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
-    int64_t acc = 0, racc = 0;
-    for (int o = 0; o < p; o++) {
-        soff[o] = acc * 8;
-        sbytes[o] = scount[o] * 8;
-        acc += scount[o];
-        int64_t c = all[(size_t)o * p + r];  // records rank o sends to me
-        roff[o] = racc * 8;
-        rbytes[o] = c * 8;
-        racc += c;
-    }
-    DArray<uint2> rbuf;
+    auto count = [&](int s, int64_t c, int o) { return all[(size_t)s * CPS + (size_t)c * p + o]; };
+    // receive layout: source-major, then chunk (== global edge order)
+    std::vector<int64_t> rseg((size_t)p * nch);
+    int64_t racc = 0;
+    for (int s = 0; s < p; s++)
+        for (int64_t c = 0; c < nch; c++) {
+            rseg[(size_t)s * nch + c] = racc;
+            racc += count(s, c, r);
+        }
+    DArray<uint2> rbuf, sbuf;
+    mem_note(ctx, "counted");
     rbuf.alloc(std::max<int64_t>(racc, 1));
-    nccl_alltoallv_bytes(ctx, sbuf.p, soff.data(), sbytes.data(), rbuf.p, roff.data(), rbytes.data());
-    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    sbuf.alloc(cap);
+    mem_note(ctx, "exchange buffers");
+    // pass 2: route, bucket by destination (stable), exchange
+    for (int64_t c = 0; c < nch; c++) {
+        int64_t c0, c1;
+        chunk(c, c0, c1);
+        const int64_t cm = std::max<int64_t>(c1 - c0, 0);
+        if (cm > 0) {
+            k_route_dest<<<blocks, 256, 0, ctx.stream>>>(es, c0, c1, g.degree.p, g.del_id.p, pd, dwbase.p, dest.p,
+                                                         keys.p, vals.p, kt_dummy.p);
+            DBFS_LAUNCHED();
+            k_iota<<<blocks, 256, 0, ctx.stream>>>(idx.p, cm);
+            DBFS_LAUNCHED();
+            bool alt = false;  // stable bucket by destination (edge order kept inside a bucket)
+            radix_sort_pairs(ctx, dest.p, idx.p, dest2.p, idx2.p, cm, std::max(1, bits_for(p)), &alt);
+            k_pack_records<<<blocks, 256, 0, ctx.stream>>>(alt ? idx2.p : idx.p, keys.p, vals.p, cm, sbuf.p);
+            DBFS_LAUNCHED();
+        }
+        std::vector<int64_t> soff(p), sbytes(p), roff(p), rbytes(p);
+        int64_t acc = 0;
+        for (int o = 0; o < p; o++) {
+            soff[o] = acc * 8;
+            sbytes[o] = count(r, c, o) * 8;
+            acc += count(r, c, o);
+            roff[o] = rseg[(size_t)o * nch + c] * 8;
+            rbytes[o] = count(o, c, r) * 8;
+        }
+        nccl_alltoallv_bytes(ctx, sbuf.p, soff.data(), sbytes.data(), rbuf.p, roff.data(), rbytes.data());
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+        mem_note(ctx, "chunk exchanged");
+    }
     sbuf.release();
+    dest.release();
+    keys.release();
+    vals.release();
+    idx.release();
+    dest2.release();
+    idx2.release();
     // local CSR from the received records (source-rank order == global edge order)
     g.workers.clear();
     g.workers.resize(1);
@@ -722,6 +803,7 @@ static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end) 
     cnt.alloc(std::max<int64_t>(nkeys, 1));
     remote.alloc(MAXW);
     g.col_all.alloc(std::max<int64_t>(racc, 1));
+    mem_note(ctx, "local sort buffers");
     DBFS_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), ctx.stream));
     DBFS_CUDA(cudaMemsetAsync(remote.p, 0, remote.bytes(), ctx.stream));
     if (racc) {
@@ -783,42 +865,59 @@ __global__ void k_gather_cols(const uint32_t *__restrict__ idx, const uint32_t *
 // by executor pulls of FORWARD-reported dd levels, where scan order is free.
 void build_sorted_dd(Graph &g) {
     Ctx &ctx = *g.ctx;
-    if (g.col_sorted.n) return;
-    g.col_sorted.alloc(std::max<int64_t>(g.col_all.n, 1));
     for (auto &W : g.workers) {
         const int64_t nnz = W.nnz[KIND_DD], rows = W.rows[KIND_DD];
-        if (nnz == 0) continue;
-        DBFS_CHECK(nnz < ((int64_t)1 << 32), DBFS_ECAPACITY, "dd rows exceed 2^32 edges on one worker");
+        if (nnz == 0 || W.col_sorted.n) continue;
         const int64_t *off = g.off_all.p + W.base[KIND_DD];
-        int64_t base = 0;
-        DBFS_CUDA(cudaMemcpy(&base, off, 8, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> h(rows + 1);
+        DBFS_CUDA(cudaMemcpy(h.data(), off, 8 * (rows + 1), cudaMemcpyDeviceToHost));
+        W.dd_base = h[0];
+        W.col_sorted.alloc(nnz);
+        // row batches of <= 2^29 entries (a longer row is a batch of its own):
+        // 32-bit entry indices and bounded sort temporaries at any scale
+        const int64_t B = (int64_t)1 << 29;
+        int64_t cap = 0;
+        for (int64_t r0 = 0, r1; r0 < rows; r0 = r1) {
+            r1 = r0 + 1;
+            while (r1 < rows && h[r1 + 1] - h[r0] <= B) r1++;
+            cap = std::max(cap, h[r1] - h[r0]);
+        }
+        DBFS_CHECK(cap < ((int64_t)1 << 32), DBFS_ECAPACITY, "a dd row exceeds 2^32 edges");
         DArray<uint32_t> key, idx, key2, idx2, rowid;
-        key.alloc(nnz);
-        idx.alloc(nnz);
-        key2.alloc(nnz);
-        idx2.alloc(nnz);
-        rowid.alloc(nnz);
+        key.alloc(cap);
+        idx.alloc(cap);
+        key2.alloc(cap);
+        idx2.alloc(cap);
+        rowid.alloc(cap);
         const int blocks = ctx.num_sms * 16;
-        k_deg_keys<<<blocks, 256, 0, ctx.stream>>>(g.col_all.p, off, nnz, g.degree.p, g.del_gid.p, key.p, idx.p);
-        DBFS_LAUNCHED();
-        bool alt = false;
-        radix_sort_pairs(ctx, key.p, idx.p, key2.p, idx2.p, nnz, 32, &alt);
-        uint32_t *sidx = alt ? idx2.p : idx.p;
-        k_row_ids<<<blocks, 256, 0, ctx.stream>>>(off, rows, rowid.p);
-        DBFS_LAUNCHED();
-        uint32_t *k2 = alt ? key.p : key2.p;   // free key buffer
-        k_row_keys<<<blocks, 256, 0, ctx.stream>>>(sidx, rowid.p, nnz, k2);
-        DBFS_LAUNCHED();
-        // k2 = row of each degree-ordered entry; sort (stable) by row
-        bool alt2 = false;
-        uint32_t *k3 = (k2 == key.p) ? key2.p : key.p;
-        uint32_t *i3 = (sidx == idx.p) ? idx2.p : idx.p;
-        int bits = 1;
-        while (bits < 32 && ((int64_t)1 << bits) < rows) bits++;
-        radix_sort_pairs(ctx, k2, sidx, k3, i3, nnz, bits, &alt2);
-        uint32_t *fidx = alt2 ? i3 : sidx;
-        k_gather_cols<<<blocks, 256, 0, ctx.stream>>>(fidx, g.col_all.p, base, nnz, g.col_sorted.p);
-        DBFS_LAUNCHED();
+        for (int64_t r0 = 0, r1; r0 < rows; r0 = r1) {
+            r1 = r0 + 1;
+            while (r1 < rows && h[r1 + 1] - h[r0] <= B) r1++;
+            const int64_t bn = h[r1] - h[r0], brows = r1 - r0;
+            if (bn == 0) continue;
+            k_deg_keys<<<blocks, 256, 0, ctx.stream>>>(g.col_all.p, off + r0, bn, g.degree.p, g.del_gid.p, key.p,
+                                                       idx.p);
+            DBFS_LAUNCHED();
+            bool alt = false;
+            radix_sort_pairs(ctx, key.p, idx.p, key2.p, idx2.p, bn, 32, &alt);
+            uint32_t *sidx = alt ? idx2.p : idx.p;
+            k_row_ids<<<blocks, 256, 0, ctx.stream>>>(off + r0, brows, rowid.p);
+            DBFS_LAUNCHED();
+            uint32_t *k2 = alt ? key.p : key2.p;  // free key buffer
+            k_row_keys<<<blocks, 256, 0, ctx.stream>>>(sidx, rowid.p, bn, k2);
+            DBFS_LAUNCHED();
+            // k2 = row of each degree-ordered entry; sort (stable) by row
+            bool alt2 = false;
+            uint32_t *k3 = (k2 == key.p) ? key2.p : key.p;
+            uint32_t *i3 = (sidx == idx.p) ? idx2.p : idx.p;
+            int bits = 1;
+            while (bits < 32 && ((int64_t)1 << bits) < brows) bits++;
+            radix_sort_pairs(ctx, k2, sidx, k3, i3, bn, bits, &alt2);
+            uint32_t *fidx = alt2 ? i3 : sidx;
+            k_gather_cols<<<blocks, 256, 0, ctx.stream>>>(fidx, g.col_all.p + h[r0], 0, bn,
+                                                          W.col_sorted.p + (h[r0] - h[0]));
+            DBFS_LAUNCHED();
+        }
         DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     }
 }

@@ -152,7 +152,19 @@ struct DArray {
     void alloc(int64_t count) {
         release();
         n = count;
-        if (count > 0) DBFS_CUDA(cudaMalloc(&p, sizeof(T) * (size_t)count));
+        if (count <= 0) return;
+        cudaError_t e = cudaMalloc(&p, sizeof(T) * (size_t)count);
+        if (e != cudaSuccess) {
+            size_t fr = 0, tot = 0;
+            cudaGetLastError();
+            cudaMemGetInfo(&fr, &tot);
+            p = nullptr;
+            n = 0;
+            throw Error(e == cudaErrorMemoryAllocation ? DBFS_ERESOURCE : DBFS_ECUDA,
+                        std::string("device allocation of ") + std::to_string(sizeof(T) * (size_t)count) +
+                            " bytes failed (" + cudaGetErrorString(e) + "; " + std::to_string(fr >> 20) +
+                            " MiB free of " + std::to_string(tot >> 20) + ")");
+        }
     }
     void release() {
         if (p) cudaFree(p);
@@ -185,6 +197,8 @@ struct WorkerHost {
     int64_t remote_cap[MAXW];        // nn edges on this worker whose column is owned by dest
     DArray<uint32_t> src_bits[4];
     DArray<uint32_t> deg[4];         // row lengths: [ND] per local normal, [DN]/[DD] per delegate
+    DArray<uint32_t> col_sorted;     // dd rows with neighbours by descending degree (executor pulls)
+    int64_t dd_base = 0;             // absolute offset of this worker's first dd entry
     // BFS state
     DArray<int32_t> nlevel, dlevel;
     DArray<int64_t> nparent, dparent, dcand;
@@ -213,7 +227,6 @@ struct Graph {
     DArray<int64_t> del_gid;         // delegate global ids (ascending)
     DArray<int64_t> off_all;         // concatenated CSR offsets (absolute)
     DArray<uint32_t> col_all;        // concatenated CSR columns
-    DArray<uint32_t> col_sorted;     // same rows, neighbours by descending degree (dd rows used)
     std::vector<WorkerHost> workers; // local workers
     // BFS engine resources (allocated on first BFS)
     bool bfs_ready = false;
@@ -258,6 +271,7 @@ struct Graph {
 };
 
 // build.cu
+void mem_note(const Ctx &ctx, const char *what);  // DBFS_VERBOSE=1: free device memory at build stages
 void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm);
 void build_graph_edges(Graph &g, const int64_t *src, const int64_t *dst, int64_t m_local);
 void export_csr(const Graph &g, int worker, int kind, int64_t *off, void *cols);
@@ -278,7 +292,7 @@ void nccl_unique_id(uint8_t *out);
 void nccl_init(Ctx &ctx, const uint8_t *uid, int nranks, int rank);
 void nccl_destroy(Ctx &ctx);
 void nccl_allreduce_u32_sum(Ctx &ctx, uint32_t *dbuf, int64_t count);
-void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op_min);
+void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op);  // 0 sum, 1 min, 2 max
 void nccl_allreduce_f64_max(Ctx &ctx, double *dbuf, int64_t count);
 void nccl_allgather_bytes(Ctx &ctx, const void *send, void *recv, int64_t bytes);
 void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, const int64_t *send_bytes,

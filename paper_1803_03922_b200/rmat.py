@@ -43,6 +43,11 @@ class RmatParams:
     d_quad: float = DEFAULT_QUADS[3]
     seed: int = 0
     scale_cap: int = DESK_SCALE_CAP
+    # This build only: Feistel relabeling after hash_randomize_vertices.  The
+    # reference hash keeps an id's low bits a function of its low bits, so the
+    # owners v mod p inherit RMAT's degree skew (p=8: heaviest worker 2.75x the
+    # mean edges); scrambled ids balance workers.  Off = the reference graph.
+    scramble: bool = False
 
     def __post_init__(self):
         if self.scale < 0:
@@ -68,6 +73,7 @@ class RmatParams:
         p.scale = self.scale
         p.randomize = int(randomize)
         p.symmetrize = int(symmetrize)
+        p.scramble = int(bool(self.scramble))
         p.edge_factor = self.edge_factor
         p.a, p.b, p.c = self.a, self.b, self.c
         p.seed = self.seed & 0xFFFFFFFFFFFFFFFF
