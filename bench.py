@@ -43,6 +43,16 @@ UNIT = "GTEPS"
 L2_BYTES = 126 << 20
 
 
+GRAPH_NAME = {"rmat": "RMAT", "er": "Uniform random (Erdos-Renyi, RMAT with uniform quadrants)"}
+
+
+def graph_quads(args, oracle=False):
+    """RMAT quadrants: Graph500 (0.57, 0.19, 0.19, 0.05), or uniform = Erdos-Renyi G(n, m)."""
+    if args.graph == "er":
+        return {"a": 0.25, "b": 0.25, "c": 0.25} if oracle else {"a": 0.25, "b": 0.25, "c": 0.25, "d_quad": 0.25}
+    return {}
+
+
 ENGINE_NOTE = {1: " (NCCL level loop)", 3: " (one persistent kernel across GPUs over CUDA-IPC peer memory)"}
 
 
@@ -159,7 +169,8 @@ def run_ours(args, world, rank, local_rank):
     scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
     scrambled = args.labeling == "scrambled"
-    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, scramble=scrambled)
+    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, scramble=scrambled,
+                            **graph_quads(args))
     t0 = time.perf_counter()
     pg = api.partition_graph(api.build_rmat_graph(params), theta,
                              api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
@@ -241,8 +252,9 @@ def run_ours(args, world, rank, local_rank):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic RMAT (Graph500 quadrants, seed 0), generated on device",
-        "config": {"workload": f"RMAT scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
+        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, seed 0), "
+                "generated on device",
+        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
                                f"{args.roots} Graph500 roots, {world}xB200",
                    "scale": scale, "edge_factor": args.edge_factor, "theta": theta, "mode": args.mode,
                    "roots": args.roots, "parents": "valid parent tree written in the timed region",
@@ -291,7 +303,7 @@ def _load_imbalance(ctx, pg, dist):
 
 def _device_series(api, ctx, args, scale, theta, world, dist):
     from paper_1803_03922_b200.engine import bfs_device
-    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40)
+    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, **graph_quads(args))
     pg = api.partition_graph(api.build_rmat_graph(params), theta,
                              api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
     roots = graph500_roots(pg.classification.out_degree, args.roots)
@@ -379,6 +391,7 @@ def run_reference(args, world, rank):
     cpu_theta = args.theta if args.theta is not None else suggested_theta(cpu_scale)
     t0 = time.perf_counter()
     og = O.partition_rmat(cpu_scale, cpu_theta, 1, world, edge_factor=args.edge_factor, load_arrays=False,
+                          **graph_quads(args, oracle=True),
                           scramble=args.labeling == "scrambled")
     deg = _oracle_degrees(og, O)
     build_s = time.perf_counter() - t0
@@ -396,8 +409,9 @@ def run_reference(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 3),
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic RMAT (Graph500 quadrants, seed 0), generated on the host",
-        "config": {"workload": f"RMAT scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
+        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, seed 0), "
+                "generated on the host",
+        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
                                f"{args.roots} Graph500 roots, CPU", "scale": scale, "theta": theta,
                    "mode": args.mode, "roots": args.roots, "shape": f"1x1x{world}", "labeling": args.labeling},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "port",
@@ -430,6 +444,8 @@ def main():
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--graph", choices=["rmat", "er"], default="rmat",
+                    help="rmat: Graph500 quadrants; er: uniform quadrants (Erdos-Renyi, configs[4])")
     ap.add_argument("--labeling", choices=["scrambled", "reference"], default="scrambled",
                     help="vertex labels: the reference hash, plus (default) this build's Feistel relabeling")
     ap.add_argument("--no-alt-labeling", action="store_true",
