@@ -319,6 +319,17 @@ static void ensure_resources(Graph &g) {
         V.cand_all = !g.dist;
         V.P_sources = g.dist ? g.p : W;
         V.rec_cap = g.rec_cap;
+        {
+            // one 64-bit atomic reserves list slots and edge prefixes together:
+            // edge bits for this worker's dn/dd totals, count bits for d
+            int cbits = 1, ebits = 1;
+            while (((int64_t)1 << cbits) <= g.d) cbits++;
+            const int64_t emax = std::max(Wk.nnz[KIND_DN], Wk.nnz[KIND_DD]);
+            while (ebits < 63 && ((int64_t)1 << ebits) <= emax) ebits++;
+            DBFS_CHECK(cbits + ebits <= 64, DBFS_ECAPACITY,
+                       "delegate frontier lists: d and the dn/dd edge totals need more than 64 bits");
+            V.dshift = 64 - cbits;
+        }
         V.pd.init((uint32_t)g.p);
         V.n = g.n;
         V.n_local = Wk.n_local;

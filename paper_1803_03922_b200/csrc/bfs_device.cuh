@@ -233,7 +233,6 @@ constexpr int UNR = DBFS_UNR;    // independent column loads in flight per lane 
 constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
 constexpr int PROBE = 4;         // candidate groups whose first entry is probed together
 constexpr unsigned FULL = 0xffffffffu;
-constexpr unsigned long long M38 = (1ull << 38) - 1;
 
 __device__ __forceinline__ bool tbit(const uint32_t *b, uint32_t i) { return (b[i >> 5] >> (i & 31)) & 1u; }
 
@@ -794,16 +793,17 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     // T2: delegate frontier -- dn / dd push, load balanced over the level's
     // edge space (engine.py:238-263).
     tt.start();
-    if (ex[KIND_DN] == FWD && (S.dpack[0] & M38)) {
-        int64_t cnt = (int64_t)(S.dpack[0] >> 38), total = (int64_t)(S.dpack[0] & M38);
+    const unsigned long long EM = (1ull << V.dshift) - 1;  // packed list: count << dshift | edges
+    if (ex[KIND_DN] == FWD && (S.dpack[0] & EM)) {
+        int64_t cnt = (int64_t)(S.dpack[0] >> V.dshift), total = (int64_t)(S.dpack[0] & EM);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
         list_push<ACT_NORMAL>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1], cnt, total,
                               x0, x1, vc);
     }
     tt.stop(AT, 1);
     tt.start();
-    if (ex[KIND_DD] == FWD && (S.dpack[1] & M38)) {
-        int64_t cnt = (int64_t)(S.dpack[1] >> 38), total = (int64_t)(S.dpack[1] & M38);
+    if (ex[KIND_DD] == FWD && (S.dpack[1] & EM)) {
+        int64_t cnt = (int64_t)(S.dpack[1] >> V.dshift), total = (int64_t)(S.dpack[1] & EM);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
         list_push<ACT_DELEG>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1], cnt, total,
                              x0, x1, vc);
@@ -994,13 +994,14 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         unsigned long long tdn = warp_sum(cdn), tedn = warp_sum(edn), tdd = warp_sum(cdd), tedd = warp_sum(edd);
         unsigned long long bdn = 0, bdd = 0;
         if (lane == 0) {
-            if (tdn) bdn = atomicAdd(&N.dpack[0], (tdn << 38) + tedn);
-            if (tdd) bdd = atomicAdd(&N.dpack[1], (tdd << 38) + tedd);
+            if (tdn) bdn = atomicAdd(&N.dpack[0], (tdn << V.dshift) + tedn);
+            if (tdd) bdd = atomicAdd(&N.dpack[1], (tdd << V.dshift) + tedd);
         }
         bdn = __shfl_sync(FULL, bdn, 0);
         bdd = __shfl_sync(FULL, bdd, 0);
         // pass B: list entries in batch order
-        unsigned long long pdn = bdn >> 38, qdn = bdn & M38, pdd = bdd >> 38, qdd = bdd & M38;
+        const unsigned long long EM = (1ull << V.dshift) - 1;
+        unsigned long long pdn = bdn >> V.dshift, qdn = bdn & EM, pdd = bdd >> V.dshift, qdd = bdd & EM;
         uint32_t *ldn_list = V.dlist[0][(L + 1) & 1], *ldd_list = V.dlist[1][(L + 1) & 1];
         int64_t *ldn_pre = V.dpre[0][(L + 1) & 1], *ldd_pre = V.dpre[1][(L + 1) & 1];
         for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
@@ -1226,12 +1227,12 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         if (ddn > 0) {
             V.dlist[0][0][0] = x;
             V.dpre[0][0][0] = 0;
-            S.dpack[0] = (1ull << 38) | (unsigned long long)ddn;
+            S.dpack[0] = (1ull << V.dshift) | (unsigned long long)ddn;
         }
         if (ddd > 0) {
             V.dlist[1][0][0] = x;
             V.dpre[1][0][0] = 0;
-            S.dpack[1] = (1ull << 38) | (unsigned long long)ddd;
+            S.dpack[1] = (1ull << V.dshift) | (unsigned long long)ddd;
         }
     } else if ((int)(source % V.p) == V.w) {
         uint32_t c = (uint32_t)(source / V.p);

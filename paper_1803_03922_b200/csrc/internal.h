@@ -25,7 +25,7 @@ struct LevelSlot {
     unsigned long long q[4];         // |queue| per kind (previsit queue sizes)
     unsigned long long nfront;       // normals in the frontier
     unsigned long long dfront;       // delegates in the frontier
-    unsigned long long dpack[2];     // delegate frontier lists (dn, dd): count << 38 | edges
+    unsigned long long dpack[2];     // delegate frontier lists (dn, dd): count << View::dshift | edges
     unsigned long long insp_bwd[4];  // backward inspections at this level
     unsigned long long records;      // remote normal records sent at this level
     unsigned long long dirty;        // this worker found >= 1 new delegate (comm.py:33-36)
@@ -85,6 +85,7 @@ struct View {
     int64_t n_local_of_w[MAXW];      // local normal count of every worker
     const int64_t *recv_off;         // dist: first inbox index of each source rank (p+1)
     int peer;                        // dist over CUDA IPC: peers' arrays mapped, one persistent launch
+    int dshift;                      // packed delegate lists: edge-count bits (count above them)
     int64_t seg_off[MAXW];           // peer: inbox segment of each source rank
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR

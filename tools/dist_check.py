@@ -14,20 +14,22 @@ from paper_1803_03922_b200.dist import env_world, init_nccl_context
 from paper_1803_03922_b200.engine import BfsOptions, _bfs_raw, levels_digest
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+er = "er" in sys.argv[3:]
+Q = dict(a=0.25, b=0.25, c=0.25) if er else {}
 world, rank, local = env_world()
 tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
 ctx = _lib.Context(local)
 _lib.set_default_context(ctx)
 init_nccl_context(ctx, tdist)
 t0 = time.time()
-pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40)), 16,
+pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40, **Q, **({"d_quad": 0.25} if er else {}))), 16,
                          api.ClusterShape(1, world), ctx=ctx)
 ctx.barrier()
 if rank == 0:
     print(f"built s{scale} on {world} GPUs in {time.time()-t0:.2f}s kinds {pg.kind_totals} d {pg.classification.d}",
           flush=True)
 roots = [1, 77, 4242 % (1 << scale), 9999 % (1 << scale)]
-engines = sys.argv[2].split(",") if len(sys.argv) > 2 else ["host", "peer"]
+engines = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] != "-" else ["host", "peer"]
 res = []
 local_ok = True
 for engine in engines:
@@ -51,7 +53,7 @@ tdist.all_gather_object(flags, local_ok)
 ok = all(flags)
 if rank == 0:
     import oracle as O
-    og = O.partition_rmat(scale, 16, 1, world)
+    og = O.partition_rmat(scale, 16, 1, world, **Q)
     for engine, used, mode, r, dg, it, insp, bad, ms in res:
         ref = O.run_bfs(og, r, mode=mode)
         ri = [[ref["inspections"][k]["forward"], ref["inspections"][k]["backward"]] for k in ("nn", "nd", "dn", "dd")]
