@@ -14,7 +14,7 @@
 #include "bfs_device.cuh"
 
 #ifndef DBFS_MINB
-#define DBFS_MINB 3
+#define DBFS_MINB 1
 #endif
 
 namespace dbfs {

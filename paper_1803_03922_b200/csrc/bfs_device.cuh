@@ -27,7 +27,10 @@
 
 namespace dbfs {
 
-constexpr int BT = 256;        // threads per block
+#ifndef DBFS_BT
+#define DBFS_BT 768
+#endif
+constexpr int BT = DBFS_BT;    // threads per block
 constexpr int WPB = BT / 32;   // warps per block
 constexpr int LIST = 1024;     // per-warp compaction buffer (32 words x 32 bits)
 
