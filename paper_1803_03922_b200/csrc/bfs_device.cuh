@@ -953,14 +953,27 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     const unsigned lane = lane_id();
     uint32_t *next_mask = V.dnext[(L + 1) & 1];
     LevelSlot &N = V.ctl->s[(L + 1) % 3];
-    const bool dyn = V.ctl->s[L % 3].dirty != 0;  // delegates were found: new-delegate work to balance
+    // sources that found delegates this level (a clean source's mask is all
+    // zero): the others' masks -- NVLink reads in the peer engine -- are skipped
+    __shared__ unsigned long long s_src;
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        const bool flags = V.peer || !V.dist;  // control blocks of every source are mapped
+        for (int s = 0; s < V.P_sources; s++)
+            if (!flags || __ldcg(&V.ctl_all[s]->s[L % 3].dirty)) m |= 1ull << s;
+        s_src = m;
+    }
+    __syncthreads();
+    const unsigned long long src = s_src;
+    const bool dyn = src != 0;  // delegates were found: new-delegate work to balance
     for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, DBFS_CWD, gw, TW); ch.valid(); ch.next()) {
         const int64_t base = ch.base();
         const int64_t wi = ch.word(V.nw_d);
         uint32_t nw = 0u;
         if (wi >= 0) {
             uint32_t r = 0;
-            for (int s = 0; s < V.P_sources; s++) r |= __ldcg(&V.mask_src[L & 1][s][wi]);
+            for (int s = 0; s < V.P_sources; s++)
+                if ((src >> s) & 1) r |= __ldcg(&V.mask_src[L & 1][s][wi]);
             uint32_t dv = V.dvis[wi];
             nw = r & ~dv;
             next_mask[wi] = 0u;
