@@ -771,6 +771,8 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         const uint32_t *has_nn = V.src_bits[KIND_NN], *has_nd = V.src_bits[KIND_ND];
         for (WarpChunks ch(S.nfront > (unsigned long long)TW ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW);
              ch.valid(); ch.next()) {
+            // groups of 1024 normals without frontier bits (coarse fold of F(L-1)) are skipped
+            if (DBFS_CWN == 32 && !__ldcg(&V.coarse_n[L & 1][ch.cur & (FW - 1)])) continue;
             const int64_t wi = ch.word(V.nw_n);
             // only frontier vertices with an nn row (or an nd row when nd pushes)
             uint32_t word = wi >= 0 ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
