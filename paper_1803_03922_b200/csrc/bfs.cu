@@ -288,6 +288,7 @@ static void ensure_resources(Graph &g) {
         Wk.inbox0.alloc(Wk.inbox_cap);
         Wk.inbox1.alloc(Wk.inbox_cap);
         if (g.dist) {
+            Wk.sentbits.alloc(std::max<int64_t>(nwords(g.n), 1));
             int64_t acc = 0;
             for (int o = 0; o < g.p; o++) {
                 Wk.send_off[o] = acc;
@@ -461,7 +462,7 @@ __global__ void k_count_reached(const int32_t *__restrict__ lv, int64_t n, unsig
 __global__ void k_pack_status(const Ctl *__restrict__ c, int L, int p, int64_t *__restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const LevelSlot &A = c->s[L % 3];
-    for (int o = 0; o < p; o++) out[o] = (int64_t)A.send[o];
+    for (int o = 0; o < p; o++) out[o] = (int64_t)A.sent[o];  // shipped records size the exchange
     const LevelSlot &P = c->s[(L + 2) % 3];  // level L-1
     out[p] = L > 0 ? (int64_t)P.records : 0;
     out[p + 1] = (int64_t)A.nfront;
@@ -666,6 +667,11 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     } else {
         for (auto &V : g.views_h) V.uniquify = 0;
     }
+    for (int i = 0; i < W; i++) {  // the sender-side filter hides records the uniquify accounting must see
+        WorkerHost &Wk = g.workers[i];
+        g.views_h[i].sent = (g.dist && !g.views_h[i].uniquify && !getenv("DBFS_NO_SEND_FILTER")) ? Wk.sentbits.p : nullptr;
+        g.views_h[i].nw_g = nwords(g.n);
+    }
     int engine = o.engine;
     if (g.dist) {
         // auto / persistent: one kernel across all GPUs over peer memory when every rank can map its peers
@@ -684,6 +690,8 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         P.exec_policy = B.exec_policy;
         P.uniquify = B.uniquify;
         P.uq = B.uq;
+        P.sent = B.sent;
+        P.nw_g = B.nw_g;
         P.local_all2all = B.local_all2all;
         for (int k = 0; k < 4; k++) {
             P.f0[k] = B.f0[k];

@@ -339,6 +339,14 @@ __device__ __forceinline__ void find_delegate(const View &V, int L, uint32_t x, 
 // lanes with `need` send (owner o, local c, parent).  In-process peers are
 // claimed directly in their device arrays; distributed peers get an 8-byte
 // record in the per-destination send bin.  One atomic per destination per warp.
+// Per-block record counts per destination (reference accounting), flushed
+// once per block at the end of V: one shared atomic per destination group
+// per warp step instead of a global atomic on one hot address.
+__device__ __forceinline__ unsigned long long *block_sendc() {
+    __shared__ unsigned long long s_sendc[MAXW];
+    return s_sendc;
+}
+
 __device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint32_t o, uint32_t c, uint32_t parent,
                                           VisitCounters &vc) {
     unsigned m = __ballot_sync(FULL, need);
@@ -347,16 +355,40 @@ __device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint3
     unsigned peers = __match_any_sync(FULL, key);
     int leader = __ffs(peers) - 1;
     unsigned rank = __popc(peers & ((1u << lane_id()) - 1));
-    unsigned long long base = 0;
-    if (need && (int)lane_id() == leader) {
-        base = atomicAdd(&V.ctl->s[L % 3].send[o], (unsigned long long)__popc(peers));
-    }
-    base = __shfl_sync(FULL, base, leader);
-    if (!need) return;
-    vc.records++;
+    if (need && (int)lane_id() == leader) atomicAdd(&block_sendc()[o], (unsigned long long)__popc(peers));
+    if (need) vc.records++;
     if (V.dist) {
-        V.sendbin[o][base + rank] = make_uint2(c, (uint32_t)parent);
+        // A target shipped once this BFS was claimed by its owner at that
+        // level (or already visited), so later records for it are redundant:
+        // one bit per global id, test-then-set, keeps each remote target to a
+        // single record per sender.  The reference counters above still see
+        // every record (comm.py:138-197 accounting).
+        bool ship = need;
+        if (need && V.sent) {
+            const uint32_t gv = c * (uint32_t)V.p + o;
+            const uint32_t bit = 1u << (gv & 31);
+            uint32_t *wp = &V.sent[gv >> 5];
+            ship = !(__ldcg(wp) & bit) && !(atomicOr(wp, bit) & bit);
+        }
+        if (!V.sent) {
+            unsigned long long base = 0;
+            if (need && (int)lane_id() == leader)
+                base = atomicAdd(&V.ctl->s[L % 3].sent[o], (unsigned long long)__popc(peers));
+            base = __shfl_sync(FULL, base, leader);
+            if (need) V.sendbin[o][base + rank] = make_uint2(c, (uint32_t)parent);
+            return;
+        }
+        const unsigned ms = __ballot_sync(FULL, ship);
+        if (!ms) return;
+        const unsigned speers = __match_any_sync(FULL, ship ? o : 0xffffffffu);
+        const int sl = __ffs(speers) - 1;
+        const unsigned srank = __popc(speers & ((1u << lane_id()) - 1));
+        unsigned long long sbase = 0;
+        if (ship && (int)lane_id() == sl) sbase = atomicAdd(&V.ctl->s[L % 3].sent[o], (unsigned long long)__popc(speers));
+        sbase = __shfl_sync(FULL, sbase, sl);
+        if (ship) V.sendbin[o][sbase + srank] = make_uint2(c, (uint32_t)parent);
     } else {
+        if (!need) return;
         if (V.uniquify) {  // staging group of (sender, dest): comm.py:165-171
             int grp = V.local_all2all ? (V.w % V.p_rank) + V.p_rank * ((int)o / V.p_rank) : V.w;
             const int64_t nwo = (V.n_local_of_w[o] + 31) >> 5;
@@ -759,6 +791,10 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     const unsigned lane = lane_id(), warp = warp_id();
     const int64_t gw = (int64_t)wb * WPB + warp, TW = (int64_t)nb * WPB;
     uint32_t *list = sm.list[warp];
+    if (V.p > 1) {
+        for (int i = threadIdx.x; i < V.p; i += BT) block_sendc()[i] = 0ull;
+        __syncthreads();
+    }
     const int p = V.p, w = V.w;
     const uint32_t *nfront_cur = V.nfront[L & 1];
 
@@ -912,6 +948,13 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (lane == 0 && v) atomicOr(&A.dirty, 1ull);
     v = warp_sum(vc.pull_rows);
     if (lane == 0) atomic_add_u64(&A.pull_rows, v);
+    if (V.p > 1) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < V.p; i += BT) {
+            const unsigned long long cnt = block_sendc()[i];
+            if (cnt) atomicAdd(&A.send[i], cnt);
+        }
+    }
 }
 
 // ------------------------------------------------------------ phase F(L)
@@ -1054,7 +1097,7 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
 __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
     if (V.peer) {  // senders stored into fixed segments of this inbox over NVLink
         __shared__ unsigned long long s_cnt[MAXW];
-        if (threadIdx.x < V.p) s_cnt[threadIdx.x] = __ldcg(&V.ctl_all[threadIdx.x]->s[L % 3].send[V.w]);
+        if (threadIdx.x < V.p) s_cnt[threadIdx.x] = __ldcg(&V.ctl_all[threadIdx.x]->s[L % 3].sent[V.w]);
         __syncthreads();
         unsigned long long uq = 0;
         for (int s = 0; s < V.p; s++) {
@@ -1212,6 +1255,8 @@ __device__ void phase_init(const View &V, int wb, int nb) {
         V.coarse_n[0][i] = 0u;
         V.coarse_n[1][i] = 0u;
     }
+    if (V.sent)
+        for (int64_t i = tid; i < V.nw_g; i += nth) V.sent[i] = 0u;
     for (int64_t i = tid; i < V.nw_d; i += nth) {
         V.dvis[i] = 0u;
         V.dfront[i] = 0u;

@@ -38,7 +38,8 @@ struct LevelSlot {
     unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
     unsigned long long tmax[8];      // per-task warp cycles: max over warps
     unsigned int sched[8];           // dynamic chunk counters: T1, T4, T6, T5, F1, F3
-    unsigned long long send[MAXW];   // records per destination worker
+    unsigned long long send[MAXW];   // records per destination worker (reference accounting)
+    unsigned long long sent[MAXW];   // records actually shipped (after the sender's once-per-BFS filter)
 };
 
 struct Ctl {
@@ -86,6 +87,8 @@ struct View {
     const int64_t *recv_off;         // dist: first inbox index of each source rank (p+1)
     int peer;                        // dist over CUDA IPC: peers' arrays mapped, one persistent launch
     int dshift;                      // packed delegate lists: edge-count bits (count above them)
+    uint32_t *sent;                  // dist: global ids already shipped to their owner this BFS (nullptr = off)
+    int64_t nw_g;                    // words of `sent`
     int64_t seg_off[MAXW];           // peer: inbox segment of each source rank
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
@@ -199,6 +202,7 @@ struct WorkerHost {
     DArray<uint32_t> src_bits[4];
     DArray<uint32_t> deg[4];         // row lengths: [ND] per local normal, [DN]/[DD] per delegate
     DArray<uint32_t> col_sorted;     // dd rows with neighbours by descending degree (executor pulls)
+    DArray<uint32_t> sentbits;       // dist: remote targets already shipped this BFS (bit per global id)
     int64_t dd_base = 0;             // absolute offset of this worker's first dd entry
     // BFS state
     DArray<int32_t> nlevel, dlevel;

@@ -16,13 +16,16 @@ from bench import graph500_roots
 base = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 nroots = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 engines = sys.argv[3].split(",") if len(sys.argv) > 3 else ["peer", "host"]
+er = "er" in sys.argv[4:]
+theta = int(sys.argv[5]) if len(sys.argv) > 5 else 16
 world, rank, local = env_world()
 tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
 ctx = _lib.Context(local)
 _lib.set_default_context(ctx)
 init_nccl_context(ctx, tdist)
 scale = weak_scale(base, world)
-pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40)), 16,
+Q = dict(a=0.25, b=0.25, c=0.25, d_quad=0.25) if er else {}
+pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40, scramble=True, **Q)), theta,
                          api.ClusterShape(1, world), ctx=ctx)
 roots = graph500_roots(pg.classification.out_degree, 64)[:nroots]
 L = _lib.load()
