@@ -339,44 +339,36 @@ __device__ __forceinline__ void find_delegate(const View &V, int L, uint32_t x, 
 // lanes with `need` send (owner o, local c, parent).  In-process peers are
 // claimed directly in their device arrays; distributed peers get an 8-byte
 // record in the per-destination send bin.  One atomic per destination per warp.
-// Per-block record counts per destination (reference accounting), flushed
-// once per block at the end of V: one shared atomic per destination group
-// per warp step instead of a global atomic on one hot address.
-__device__ __forceinline__ unsigned long long *block_sendc() {
-    __shared__ unsigned long long s_sendc[MAXW];
-    return s_sendc;
+// Destinations that received >= 1 record this level, per block (the
+// reference's message count is the number of non-empty (sender, dest)
+// pairs, comm.py:138-197); flushed once per block at the end of V.
+__device__ __forceinline__ unsigned long long *block_sendmask() {
+    __shared__ unsigned long long s_mask;
+    return &s_mask;
 }
 
 __device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint32_t o, uint32_t c, uint32_t parent,
                                           VisitCounters &vc) {
     unsigned m = __ballot_sync(FULL, need);
     if (!m) return;
-    unsigned key = need ? o : 0xffffffffu;
-    unsigned peers = __match_any_sync(FULL, key);
-    int leader = __ffs(peers) - 1;
-    unsigned rank = __popc(peers & ((1u << lane_id()) - 1));
-    if (need && (int)lane_id() == leader) atomicAdd(&block_sendc()[o], (unsigned long long)__popc(peers));
+    {
+        const unsigned lo = __reduce_or_sync(FULL, (need && o < 32) ? 1u << o : 0u);
+        const unsigned hi = V.p > 32 ? __reduce_or_sync(FULL, (need && o >= 32) ? 1u << (o - 32) : 0u) : 0u;
+        if (lane_id() == 0) atomicOr(block_sendmask(), ((unsigned long long)hi << 32) | lo);
+    }
     if (need) vc.records++;
     if (V.dist) {
         // A target shipped once this BFS was claimed by its owner at that
         // level (or already visited), so later records for it are redundant:
         // one bit per global id, test-then-set, keeps each remote target to a
-        // single record per sender.  The reference counters above still see
-        // every record (comm.py:138-197 accounting).
+        // single record per sender.  The reference counters still see every
+        // record (vc.records, the destination mask above).
         bool ship = need;
         if (need && V.sent) {
             const uint32_t gv = c * (uint32_t)V.p + o;
             const uint32_t bit = 1u << (gv & 31);
             uint32_t *wp = &V.sent[gv >> 5];
             ship = !(__ldcg(wp) & bit) && !(atomicOr(wp, bit) & bit);
-        }
-        if (!V.sent) {
-            unsigned long long base = 0;
-            if (need && (int)lane_id() == leader)
-                base = atomicAdd(&V.ctl->s[L % 3].sent[o], (unsigned long long)__popc(peers));
-            base = __shfl_sync(FULL, base, leader);
-            if (need) V.sendbin[o][base + rank] = make_uint2(c, (uint32_t)parent);
-            return;
         }
         const unsigned ms = __ballot_sync(FULL, ship);
         if (!ms) return;
@@ -792,7 +784,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     const int64_t gw = (int64_t)wb * WPB + warp, TW = (int64_t)nb * WPB;
     uint32_t *list = sm.list[warp];
     if (V.p > 1) {
-        for (int i = threadIdx.x; i < V.p; i += BT) block_sendc()[i] = 0ull;
+        if (threadIdx.x == 0) *block_sendmask() = 0ull;
         __syncthreads();
     }
     const int p = V.p, w = V.w;
@@ -950,10 +942,9 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (lane == 0) atomic_add_u64(&A.pull_rows, v);
     if (V.p > 1) {
         __syncthreads();
-        for (int i = threadIdx.x; i < V.p; i += BT) {
-            const unsigned long long cnt = block_sendc()[i];
-            if (cnt) atomicAdd(&A.send[i], cnt);
-        }
+        const unsigned long long dm = *block_sendmask();
+        for (int i = threadIdx.x; i < V.p; i += BT)
+            if ((dm >> i) & 1) atomicOr(&A.send[i], 1ull);
     }
 }
 

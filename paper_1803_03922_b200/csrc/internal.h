@@ -38,7 +38,7 @@ struct LevelSlot {
     unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
     unsigned long long tmax[8];      // per-task warp cycles: max over warps
     unsigned int sched[8];           // dynamic chunk counters: T1, T4, T6, T5, F1, F3
-    unsigned long long send[MAXW];   // records per destination worker (reference accounting)
+    unsigned long long send[MAXW];   // 1 if >= 1 record went to this destination (reference message count)
     unsigned long long sent[MAXW];   // records actually shipped (after the sender's once-per-BFS filter)
 };
 
