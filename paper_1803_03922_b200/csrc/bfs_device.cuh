@@ -347,48 +347,102 @@ __device__ __forceinline__ unsigned long long *block_sendmask() {
     return &s_mask;
 }
 
-__device__ __forceinline__ void warp_send(const View &V, int L, bool need, uint32_t o, uint32_t c, uint32_t parent,
-                                          VisitCounters &vc) {
-    unsigned m = __ballot_sync(FULL, need);
-    if (!m) return;
+// Remote nn targets of one warp step (UNR slots, engine.py:207-222 ->
+// comm.py:138-197), handled as one batch so the slots' memory round trips
+// overlap.  In-process peers are claimed directly in their bitmaps; a
+// distributed peer gets an 8-byte record in its inbox segment, unless this
+// sender already shipped that target during this BFS: a target shipped once
+// was claimed by its owner at that level (or was already visited), so one
+// bit per global id (test, then set) keeps each remote target to a single
+// record per sender.  The reference counters see every record
+// (vc.records, the destination mask).
+__device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool (&need)[UNR], const uint32_t (&o)[UNR],
+                                                const uint32_t (&c)[UNR], const uint32_t (&parent)[UNR],
+                                                VisitCounters &vc) {
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < UNR; u++) any |= need[u];
+    if (!__any_sync(FULL, any)) return;
     {
-        const unsigned lo = __reduce_or_sync(FULL, (need && o < 32) ? 1u << o : 0u);
-        const unsigned hi = V.p > 32 ? __reduce_or_sync(FULL, (need && o >= 32) ? 1u << (o - 32) : 0u) : 0u;
+        unsigned lo = 0, hi = 0;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            if (need[u]) {
+                vc.records++;
+                if (o[u] < 32) lo |= 1u << o[u];
+                else hi |= 1u << (o[u] - 32);
+            }
+        }
+        lo = __reduce_or_sync(FULL, lo);
+        if (V.p > 32) hi = __reduce_or_sync(FULL, hi);
         if (lane_id() == 0) atomicOr(block_sendmask(), ((unsigned long long)hi << 32) | lo);
     }
-    if (need) vc.records++;
-    if (V.dist) {
-        // A target shipped once this BFS was claimed by its owner at that
-        // level (or already visited), so later records for it are redundant:
-        // one bit per global id, test-then-set, keeps each remote target to a
-        // single record per sender.  The reference counters still see every
-        // record (vc.records, the destination mask above).
-        bool ship = need;
-        if (need && V.sent) {
-            const uint32_t gv = c * (uint32_t)V.p + o;
+    if (!V.dist) {
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            if (!need[u]) continue;
+            if (V.uniquify) {  // staging group of (sender, dest): comm.py:165-171
+                int grp = V.local_all2all ? (V.w % V.p_rank) + V.p_rank * ((int)o[u] / V.p_rank) : V.w;
+                const int64_t nwo = (V.n_local_of_w[o[u]] + 31) >> 5;
+                uint32_t old = atomicOr(&V.uq_all[o[u]][(int64_t)grp * nwo + (c[u] >> 5)], 1u << (c[u] & 31));
+                if (!(old & (1u << (c[u] & 31)))) vc.uq++;
+            }
+            claim_on(V.nvis_all[o[u]], V.nfront_all[(L + 1) & 1][o[u]], V.nlevel_all[o[u]], V.nparent_all[o[u]],
+                     V.parents, L, c[u], parent[u], true);
+        }
+        return;
+    }
+    bool ship[UNR];
+    if (V.sent) {
+        uint32_t w[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {  // all tests in flight, then all sets
+            const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
+            w[u] = need[u] ? __ldcg(&V.sent[gv >> 5]) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
             const uint32_t bit = 1u << (gv & 31);
-            uint32_t *wp = &V.sent[gv >> 5];
-            ship = !(__ldcg(wp) & bit) && !(atomicOr(wp, bit) & bit);
+            ship[u] = need[u] && !(w[u] & bit);
+            if (ship[u]) w[u] = atomicOr(&V.sent[gv >> 5], bit);
         }
-        const unsigned ms = __ballot_sync(FULL, ship);
-        if (!ms) return;
-        const unsigned speers = __match_any_sync(FULL, ship ? o : 0xffffffffu);
-        const int sl = __ffs(speers) - 1;
-        const unsigned srank = __popc(speers & ((1u << lane_id()) - 1));
-        unsigned long long sbase = 0;
-        if (ship && (int)lane_id() == sl) sbase = atomicAdd(&V.ctl->s[L % 3].sent[o], (unsigned long long)__popc(speers));
-        sbase = __shfl_sync(FULL, sbase, sl);
-        if (ship) V.sendbin[o][sbase + srank] = make_uint2(c, (uint32_t)parent);
+#pragma unroll
+        for (int u = 0; u < UNR; u++) ship[u] = ship[u] && !(w[u] & (1u << ((c[u] * (uint32_t)V.p + o[u]) & 31)));
     } else {
-        if (!need) return;
-        if (V.uniquify) {  // staging group of (sender, dest): comm.py:165-171
-            int grp = V.local_all2all ? (V.w % V.p_rank) + V.p_rank * ((int)o / V.p_rank) : V.w;
-            const int64_t nwo = (V.n_local_of_w[o] + 31) >> 5;
-            uint32_t old = atomicOr(&V.uq_all[o][(int64_t)grp * nwo + (c >> 5)], 1u << (c & 31));
-            if (!(old & (1u << (c & 31)))) vc.uq++;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) ship[u] = need[u];
+    }
+    // destinations with records to ship, then one slot reservation per destination
+    unsigned long long dm = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; u++)
+        if (ship[u]) dm |= 1ull << o[u];
+    {
+        const unsigned lo = __reduce_or_sync(FULL, (unsigned)dm);
+        const unsigned hi = V.p > 32 ? __reduce_or_sync(FULL, (unsigned)(dm >> 32)) : 0u;
+        dm = ((unsigned long long)hi << 32) | lo;
+    }
+    const unsigned lt = (1u << lane_id()) - 1;
+    while (dm) {
+        const uint32_t dst = __ffsll(dm) - 1;
+        dm &= dm - 1;
+        unsigned b[UNR], tot = 0;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            b[u] = __ballot_sync(FULL, ship[u] && o[u] == dst);
+            tot += __popc(b[u]);
         }
-        claim_on(V.nvis_all[o], V.nfront_all[(L + 1) & 1][o], V.nlevel_all[o], V.nparent_all[o], V.parents, L, c,
-                 parent, true);
+        unsigned long long base = 0;
+        if (lane_id() == 0) base = atomicAdd(&V.ctl->s[L % 3].sent[dst], (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 0);
+        unsigned before = 0;
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+            if (ship[u] && o[u] == dst)
+                V.sendbin[dst][base + before + __popc(b[u] & lt)] = make_uint2(c[u], parent[u]);
+            before += __popc(b[u]);
+        }
     }
 }
 
@@ -464,11 +518,14 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         }
     }
     if (ACT == ACT_NN && V.p > 1) {
+        bool remote[UNR];
+        uint32_t own[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; u++) {
-            bool remote = valid[u] && !local[u];
-            warp_send(V, L, remote, V.pd.mod(cc[u]), tgt[u], pp[u], vc);
+            remote[u] = valid[u] && !local[u];
+            own[u] = V.pd.mod(cc[u]);
         }
+        warp_send_batch(V, L, remote, own, tgt, pp, vc);
     }
 }
 
