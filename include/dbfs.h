@@ -20,6 +20,8 @@
  *   dbfs_validate             <- NEW: Graph500 certificate (nearest
  *                                reference analogue is cli.cmd_verify, cli.py:159-174)
  *   dbfs_min_parents          <- NEW: min-ID parent rule
+ *   dbfs_edges_parse_text     <- rmat.load_edge_list, text format         (rmat.py:232-286)
+ *   dbfs_edges_write_text     <- rmat.save_edge_list, text format         (rmat.py:211-229)
  */
 #ifndef DBFS_H
 #define DBFS_H
@@ -44,7 +46,9 @@ typedef enum {
     DBFS_EROUTING = 8,   /* RoutingError, comm.py:16-17                          */
     DBFS_ESTRUCT = 9,    /* StructuralError, comm.py:20-21                       */
     DBFS_ETIMEOUT = 10,  /* device watchdog fired (grid barrier)                 */
-    DBFS_EINTERNAL = 11
+    DBFS_EINTERNAL = 11,
+    DBFS_EFORMAT = 12,   /* FormatError, rmat.py:35-36 (malformed edge-list file) */
+    DBFS_EIO = 13        /* OSError (file could not be opened / written)          */
 } dbfs_status;
 
 typedef struct dbfs_ctx dbfs_ctx;
@@ -198,6 +202,17 @@ int32_t dbfs_min_parents(dbfs_graph *g, int64_t *parents_out);
  * 8 parent level, 16 tree edge missing, 32 parent of unreached / missing parent. */
 int32_t dbfs_validate(dbfs_graph *g, int64_t root, const int32_t *levels, const int64_t *parents,
                       int32_t *report);
+
+/* Edge-list text files (rmat.py:211-286).  Host-only, no device.
+ * dbfs_edges_text_capacity: upper bound on the edge count of a buffer (its line count).
+ * dbfs_edges_parse_text: "u v" lines, '#' comments, "# n <count>" header (*header_n = -1
+ * when absent); DBFS_EFORMAT with "<line>: ..." on a malformed line.  Ids are not range
+ * checked here (the caller checks them against n, as load_edge_list does). */
+int32_t dbfs_edges_text_capacity(const char *buf, int64_t len, int64_t *lines);
+int32_t dbfs_edges_parse_text(const char *buf, int64_t len, int64_t cap, int64_t *src, int64_t *dst,
+                              int64_t *m_out, int64_t *header_n);
+/* Writes "# n <n>" then one "u v" line per edge (DBFS_EIO on failure). */
+int32_t dbfs_edges_write_text(const char *path, int64_t n, const int64_t *src, const int64_t *dst, int64_t m);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ vp = ctypes.c_void_p
 
 DBFS_OK, DBFS_EINVAL, DBFS_ERANGE, DBFS_ECAPACITY, DBFS_ERESOURCE = 0, 1, 2, 3, 4
 DBFS_ENOMEM, DBFS_ECUDA, DBFS_ENCCL, DBFS_EROUTING, DBFS_ESTRUCT = 5, 6, 7, 8, 9
-DBFS_ETIMEOUT, DBFS_EINTERNAL = 10, 11
+DBFS_ETIMEOUT, DBFS_EINTERNAL, DBFS_EFORMAT, DBFS_EIO = 10, 11, 12, 13
 
 KIND_INDEX = {"nn": 0, "nd": 1, "dn": 2, "dd": 3}
 
@@ -102,6 +102,9 @@ SIGNATURES = {
     "dbfs_bfs_iteration": (i32, [vp, i64, P(IterationC), vp, vp]),
     "dbfs_min_parents": (i32, [vp, vp]),
     "dbfs_validate": (i32, [vp, i64, vp, vp, P(i32)]),
+    "dbfs_edges_text_capacity": (i32, [vp, i64, P(i64)]),
+    "dbfs_edges_parse_text": (i32, [vp, i64, i64, vp, vp, P(i64), P(i64)]),
+    "dbfs_edges_write_text": (i32, [ctypes.c_char_p, i64, vp, vp, i64]),
 }
 
 _lib = None
@@ -133,7 +136,7 @@ def check(rc, what="dbfs"):
         return
     msg = load().dbfs_last_error().decode(errors="replace") or what
     from .partition import CapacityError
-    from .rmat import ResourceError
+    from .rmat import FormatError, ResourceError
     from .comm import RoutingError, StructuralError
     if rc in (DBFS_EINVAL, DBFS_ERANGE):
         raise ValueError(msg)
@@ -147,6 +150,10 @@ def check(rc, what="dbfs"):
         raise StructuralError(msg)
     if rc == DBFS_ENOMEM:
         raise MemoryError(msg)
+    if rc == DBFS_EFORMAT:
+        raise FormatError(msg)
+    if rc == DBFS_EIO:
+        raise OSError(msg)
     raise DbfsError(rc, msg)
 
 

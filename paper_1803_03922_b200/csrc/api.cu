@@ -407,4 +407,26 @@ int32_t dbfs_validate(dbfs_graph *gg, int64_t root, const int32_t *levels, const
     });
 }
 
+int32_t dbfs_edges_text_capacity(const char *buf, int64_t len, int64_t *lines) {
+    return guard([&] {
+        DBFS_CHECK(len >= 0 && (buf || !len) && lines, DBFS_EINVAL, "bad buffer");
+        *lines = count_text_lines(buf, len);
+    });
+}
+
+int32_t dbfs_edges_parse_text(const char *buf, int64_t len, int64_t cap, int64_t *src, int64_t *dst,
+                              int64_t *m_out, int64_t *header_n) {
+    return guard([&] {
+        DBFS_CHECK(len >= 0 && (buf || !len) && m_out && header_n, DBFS_EINVAL, "bad buffer");
+        parse_edge_text(buf, len, cap, src, dst, m_out, header_n);
+    });
+}
+
+int32_t dbfs_edges_write_text(const char *path, int64_t n, const int64_t *src, const int64_t *dst, int64_t m) {
+    return guard([&] {
+        DBFS_CHECK(path && m >= 0 && (m == 0 || (src && dst)), DBFS_EINVAL, "bad arguments");
+        write_edge_text(path, n, src, dst, m);
+    });
+}
+
 }  // extern "C"

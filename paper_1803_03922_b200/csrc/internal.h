@@ -305,6 +305,12 @@ void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, c
 void nccl_barrier(Ctx &ctx);
 void nccl_allreduce_u8_max(Ctx &ctx, uint8_t *dbuf, int64_t count);
 
+// io.cu (host only)
+int64_t count_text_lines(const char *buf, int64_t len);
+void parse_edge_text(const char *buf, int64_t len, int64_t cap, int64_t *src, int64_t *dst, int64_t *m_out,
+                     int64_t *header_n);
+void write_edge_text(const char *path, int64_t n, const int64_t *src, const int64_t *dst, int64_t m);
+
 // scan.cu helpers (device-wide exclusive scans)
 void exclusive_scan_u32_to_i64(Ctx &ctx, const uint32_t *in, int64_t *out, int64_t n);  // out has n+1
 void radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, uint32_t *vals_alt,

@@ -6,13 +6,20 @@ histogram, delegate classification, Alg. 1 routing, stable per-worker CSR
 construction.  The returned :class:`PartitionedGraph` owns the device
 partition; its ``workers[w].nn.row_offsets`` etc. are copied to host lazily
 (exactly the reference's arrays: int64 offsets, int64 nn columns, uint32
-nd/dn/dd columns) for inspection and parity tests.  Bucket verification and
-DPG1 serialization (partition.py:199-260, 392-464) are outside the hot path.
+nd/dn/dd columns) for inspection and parity tests.
+
+DPG1 files (partition.py:392-464): ``save_partitioned_graph`` writes the
+device partition byte-identically to the reference's writer;
+``load_partitioned_graph`` turns the files back into a device partition by
+replaying each worker's CSR entries as edges through the GPU build (see its
+docstring for why that reproduces the stored arrays exactly).
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,6 +29,9 @@ from .rmat import EdgeList, RmatEdgeList
 from .storage import KINDS, CsrSubgraph
 
 KIND_CODES = {"nn": 0, "nd": 1, "dn": 2, "dd": 3}
+DPG_MAGIC = b"DPG1"
+DPG_VERSION = 1
+_DPG_HEADER = "<IQQIIqQIQ"  # version, n, m, p_rank, p_gpu, theta, d, worker, n_local
 
 
 class CapacityError(OverflowError):
@@ -247,3 +257,199 @@ def partition_graph(g: EdgeList, theta: int, shape: ClusterShape, verify: bool =
     if verify and sum(pg.kind_totals.values()) != pg.m:
         raise BucketViolation("edge conservation violated")
     return pg
+
+
+# ---------------------------------------------------------------------------
+# DPG1 serialization (partition.py:380-464)
+# ---------------------------------------------------------------------------
+
+def _put_array(f, arr: np.ndarray, dtype) -> None:
+    data = np.ascontiguousarray(arr, dtype=dtype)
+    f.write(struct.pack("<Q", len(data)))
+    f.write(data.tobytes())
+
+
+def _get_array(f, dtype, name: str) -> np.ndarray:
+    head = f.read(8)
+    if len(head) != 8:
+        raise ValueError(f"{name}: truncated file")
+    (count,) = struct.unpack("<Q", head)
+    item = np.dtype(dtype).itemsize
+    body = f.read(count * item)
+    if len(body) != count * item:
+        raise ValueError(f"{name}: truncated file")
+    return np.frombuffer(body, dtype=dtype).copy()
+
+
+def save_partitioned_graph(pg: PartitionedGraph, directory) -> None:
+    """One DPG1 file per worker, ``worker_{index:05d}.dpg`` (partition.py:392-421).
+
+    Little-endian: magic "DPG1", then u32 version, u64 n, u64 m, u32 p_rank,
+    u32 p_gpu, i64 theta, u64 d, u32 worker, u64 n_local; the nn/nd/dn/dd CSRs
+    (u64-counted int64 offsets, u64-counted columns: int64 for nn, uint32
+    otherwise); the delegate global ids (int64), the nd source list (int64) and
+    the dn/dd source masks (np.packbits, u64-counted bytes).  The arrays come
+    from the device partition (dbfs_graph_export_*); a distributed partition
+    writes the workers of this rank (rank r writes worker r).
+    """
+    directory = os.fspath(directory)
+    os.makedirs(directory, exist_ok=True)
+    cls = pg.classification
+    for w in pg.workers:
+        path = os.path.join(directory, f"worker_{w.index:05d}.dpg")
+        with open(path, "wb") as f:
+            f.write(DPG_MAGIC)
+            f.write(struct.pack(_DPG_HEADER, DPG_VERSION, pg.n, pg.m, pg.shape.p_rank, pg.shape.p_gpu,
+                                cls.theta, cls.d, w.index, w.n_local))
+            for kind in KINDS:
+                csr = w.subgraph(kind)
+                _put_array(f, csr.row_offsets, np.int64)
+                _put_array(f, csr.col_indices, np.int64 if kind == "nn" else np.uint32)
+            _put_array(f, cls.delegate_global_ids, np.int64)
+            _put_array(f, w.nd_source_list, np.int64)
+            _put_array(f, np.packbits(w.dn_source_mask), np.uint8)
+            _put_array(f, np.packbits(w.dd_source_mask), np.uint8)
+
+
+@dataclass
+class _DpgWorker:
+    index: int
+    n_local: int
+    header: tuple
+    csr: dict
+    del_gid: np.ndarray
+    nd_sources: np.ndarray
+    dn_mask: np.ndarray
+    dd_mask: np.ndarray
+
+
+def _read_dpg(path: str) -> _DpgWorker:
+    name = os.path.basename(path)
+    with open(path, "rb") as f:
+        if f.read(4) != DPG_MAGIC:
+            raise ValueError(f"{name}: bad magic")
+        raw = f.read(struct.calcsize(_DPG_HEADER))
+        if len(raw) != struct.calcsize(_DPG_HEADER):
+            raise ValueError(f"{name}: truncated file")
+        version, n, m, p_rank, p_gpu, theta, d, index, n_local = struct.unpack(_DPG_HEADER, raw)
+        if version != DPG_VERSION:
+            raise ValueError(f"{name}: unsupported version {version}")
+        csr = {}
+        for kind in KINDS:
+            off = _get_array(f, np.int64, name)
+            cols = _get_array(f, np.int64 if kind == "nn" else np.uint32, name)
+            csr[kind] = CsrSubgraph(kind, off, cols)
+        del_gid = _get_array(f, np.int64, name)
+        nd_sources = _get_array(f, np.int64, name)
+        dn_mask = np.unpackbits(_get_array(f, np.uint8, name))[:d].astype(bool)
+        dd_mask = np.unpackbits(_get_array(f, np.uint8, name))[:d].astype(bool)
+    return _DpgWorker(index, n_local, (n, m, p_rank, p_gpu, theta, d), csr, del_gid, nd_sources, dn_mask, dd_mask)
+
+
+def _worker_edges(wf: _DpgWorker, p: int) -> tuple[np.ndarray, np.ndarray]:
+    """A worker's CSR entries as global (src, dst) pairs, kinds nn, nd, dn, dd, rows
+    ascending, each row's columns in stored order (partition.py:319-326 inverted)."""
+    w, gid = wf.index, wf.del_gid
+    srcs, dsts = [], []
+    for kind in KINDS:
+        c = wf.csr[kind]
+        rows = np.repeat(np.arange(c.num_rows, dtype=np.int64), np.diff(c.row_offsets))
+        cols = c.col_indices.astype(np.int64)
+        if kind in ("nn", "nd"):
+            srcs.append(rows * p + w)
+        else:
+            srcs.append(gid[rows])
+        if kind == "nn":
+            dsts.append(cols)
+        elif kind == "dn":
+            dsts.append(cols * p + w)
+        else:
+            dsts.append(gid[cols])
+    return np.concatenate(srcs), np.concatenate(dsts)
+
+
+def load_partitioned_graph(directory, symmetric: bool | None = None, verify: bool = False,
+                           ctx=None) -> PartitionedGraph:
+    """Read DPG1 worker files back into a device partition (partition.py:424-464).
+
+    Every worker's CSR entries are replayed as global (src, dst) edges --
+    workers in index order, kinds nn, nd, dn, dd, rows ascending, columns in
+    stored order -- and fed to the GPU build (``dbfs_graph_build_edges``) with
+    the stored theta and shape.  That edge list is the partition's own edge
+    multiset, so degrees, the delegate set and Alg. 1 routing are the same; the
+    build's stable (worker, kind, row) grouping keeps every row's stored column
+    order, so the device CSRs equal the files' arrays.  The stored d, kind
+    sizes and (with ``verify``) every array are checked against the rebuilt
+    partition (ValueError on a mismatch).  In a distributed context (one
+    worker per rank) rank r reads and builds from ``worker_r`` only.
+
+    ``symmetric`` declares that every edge's reverse is present (it enables the
+    executor's pull substitution); None checks the edge multiset on
+    the host (single-process loads only).
+    """
+    directory = os.fspath(directory)
+    files = sorted(f for f in os.listdir(directory) if f.endswith(".dpg"))
+    if not files:
+        raise FileNotFoundError(f"no .dpg worker files in {directory}")
+    ctx = ctx or _lib.default_context()
+    if ctx.nranks > 1:
+        mine = [f for f in files if f == f"worker_{ctx.rank:05d}.dpg"]
+        if len(files) != ctx.nranks or not mine:
+            raise ValueError(f"{directory}: a distributed load needs one worker file per rank "
+                             f"({len(files)} files, {ctx.nranks} ranks)")
+        files = mine
+    wfs = [_read_dpg(os.path.join(directory, f)) for f in files]
+    n, m, p_rank, p_gpu, theta, d = wfs[0].header
+    for wf in wfs[1:]:
+        if wf.header != wfs[0].header:
+            raise ValueError(f"{directory}: worker headers disagree")
+    shape = ClusterShape(p_rank=p_rank, p_gpu=p_gpu)
+    if ctx.nranks == 1 and sorted(wf.index for wf in wfs) != list(range(shape.p)):
+        raise ValueError(f"{directory}: expected workers 0..{shape.p - 1}")
+    wfs.sort(key=lambda wf: wf.index)
+    parts = [_worker_edges(wf, shape.p) for wf in wfs]
+    src = np.concatenate([a for a, _ in parts]) if parts else np.zeros(0, np.int64)
+    dst = np.concatenate([b for _, b in parts]) if parts else np.zeros(0, np.int64)
+    if symmetric is None:
+        symmetric = _is_symmetric(src, dst, n, ctx)
+    L = _lib.load()
+    h = _lib.vp()
+    _lib.check(L.dbfs_graph_build_edges(ctx.handle, src.ctypes.data_as(_lib.vp), dst.ctypes.data_as(_lib.vp),
+                                        len(src), int(n), int(theta), p_rank, p_gpu, ctypes.byref(h)),
+               "graph_build_edges")
+    if symmetric:
+        _lib.check(L.dbfs_graph_set_symmetric(h, 1))
+    pg = PartitionedGraph(h, ctx, shape)
+    if pg.m != m or pg.classification.d != d:
+        raise ValueError(f"{directory}: rebuilt partition disagrees with the files (m {pg.m} vs {m}, "
+                         f"d {pg.classification.d} vs {d})")
+    for wf, wg in zip(wfs, pg.workers):
+        rows, nnz = wg.sizes()
+        for k, kind in enumerate(KINDS):
+            c = wf.csr[kind]
+            if rows[k] != c.num_rows or nnz[k] != c.num_edges:
+                raise ValueError(f"worker {wf.index} {kind}: rebuilt CSR size differs from the file")
+        if verify:
+            for kind in KINDS:
+                a, b = wf.csr[kind], wg.subgraph(kind)
+                if not (np.array_equal(a.row_offsets, b.row_offsets)
+                        and np.array_equal(a.col_indices, b.col_indices)):
+                    raise ValueError(f"worker {wf.index} {kind}: rebuilt CSR differs from the file")
+            if not (np.array_equal(wf.del_gid, pg.classification.delegate_global_ids)
+                    and np.array_equal(wf.nd_sources, wg.nd_source_list)
+                    and np.array_equal(wf.dn_mask, wg.dn_source_mask)
+                    and np.array_equal(wf.dd_mask, wg.dd_source_mask)):
+                raise ValueError(f"worker {wf.index}: rebuilt source lists differ from the file")
+    return pg
+
+
+def _is_symmetric(src: np.ndarray, dst: np.ndarray, n: int, ctx) -> bool:
+    """Edge multiset closed under reversal.  A distributed load holds one
+    worker's edges per rank, and Alg. 1 may place an nn edge and its reverse on
+    different workers, so there the answer is False unless the caller declares
+    the graph symmetric."""
+    if n > (1 << 32) or ctx.nranks > 1:
+        return False
+    fwd = np.sort((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64))
+    rev = np.sort((dst.astype(np.uint64) << np.uint64(32)) | src.astype(np.uint64))
+    return bool(np.array_equal(fwd, rev))

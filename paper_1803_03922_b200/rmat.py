@@ -5,19 +5,24 @@ Generation runs in libdbfs (counter-based SplitMix64 draws, bit-exact with
 rmat.py:107-150).  ``build_rmat_graph`` returns an :class:`RmatEdgeList`
 whose arrays are generated lazily: ``partition_graph`` builds the partition
 straight on the device from the parameters, so at scale >= 24 the edge list
-never crosses PCIe.  Edge-list file I/O (rmat.py:211-286) is outside the hot
-path and not provided.
+never crosses PCIe.  Edge-list files (rmat.py:211-286): the packed binary
+"DEL1" format goes through numpy; the text format is parsed and written by
+libdbfs's host code (``dbfs_edges_parse_text`` / ``dbfs_edges_write_text``)
+with the reference's line rules and errors.
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
+import struct
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
 
+BINARY_MAGIC = b"DEL1"
 DESK_SCALE_CAP = 24
 DEFAULT_EDGE_FACTOR = 16
 DEFAULT_QUADS = (0.57, 0.19, 0.19, 0.05)
@@ -211,3 +216,82 @@ def build_rmat_graph(params: RmatParams, randomize: bool = True, do_symmetrize: 
             g = hash_randomize_vertices(g, params.seed)
         return symmetrize(g) if do_symmetrize else g
     return RmatEdgeList(params, randomize, do_symmetrize)
+
+
+def save_edge_list(g: EdgeList, path, fmt: str = "binary") -> None:
+    """Write ``g`` as packed binary ("DEL1", <Q n, then <u8 (src, dst) pairs) or as
+    text ("# n <n>" then "u v" lines) -- rmat.py:211-229."""
+    path = os.fspath(path)
+    if fmt == "binary":
+        pairs = np.empty((g.m, 2), dtype="<u8")
+        pairs[:, 0] = g.src
+        pairs[:, 1] = g.dst
+        with open(path, "wb") as f:
+            f.write(BINARY_MAGIC)
+            f.write(struct.pack("<Q", g.n))
+            f.write(pairs.tobytes())
+    elif fmt == "text":
+        src = np.ascontiguousarray(g.src, dtype=np.int64)
+        dst = np.ascontiguousarray(g.dst, dtype=np.int64)
+        _lib.check(_lib.load().dbfs_edges_write_text(path.encode(), int(g.n), src.ctypes.data_as(_lib.vp),
+                                                     dst.ctypes.data_as(_lib.vp), len(src)), "edges_write_text")
+    else:
+        raise ValueError(f"unknown format {fmt!r}")
+
+
+def _parse_text(path: str):
+    L = _lib.load()
+    with open(path, "rb") as f:
+        data = f.read()
+    if not data:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64), None
+    cap = _lib.i64()
+    _lib.check(L.dbfs_edges_text_capacity(data, len(data), ctypes.byref(cap)))
+    src = np.empty(cap.value, dtype=np.int64)
+    dst = np.empty(cap.value, dtype=np.int64)
+    m, hn = _lib.i64(), _lib.i64()
+    try:
+        _lib.check(L.dbfs_edges_parse_text(data, len(data), cap.value, src.ctypes.data_as(_lib.vp),
+                                           dst.ctypes.data_as(_lib.vp), ctypes.byref(m), ctypes.byref(hn)),
+                   "edges_parse_text")
+    except FormatError as exc:
+        raise FormatError(f"{path}:{exc}") from None
+    return src[:m.value].copy(), dst[:m.value].copy(), (hn.value if hn.value >= 0 else None)
+
+
+def load_edge_list(path, fmt: str = "auto") -> EdgeList:
+    """Load a text ("u v" per line, '#' comments) or packed binary edge list
+    (rmat.py:232-286).  n defaults to 1 + max id; the binary header and the text
+    "# n <count>" comment override it.  Errors: FormatError (truncated binary,
+    malformed line "<path>:<line>: ...", id overflow, id out of range)."""
+    path = os.fspath(path)
+    if fmt == "auto":
+        with open(path, "rb") as f:
+            fmt = "binary" if f.read(4) == BINARY_MAGIC else "text"
+    if fmt == "binary":
+        with open(path, "rb") as f:
+            magic = f.read(4)
+            header_n = None
+            if magic == BINARY_MAGIC:
+                header_n = struct.unpack("<Q", f.read(8))[0]
+                body = f.read()
+            else:
+                body = magic + f.read()
+        if len(body) % 16:
+            raise FormatError(f"{path}: truncated binary edge list")
+        pairs = np.frombuffer(body, dtype="<u8").reshape(-1, 2)
+        if pairs.size and pairs.max() >= np.uint64(1 << 62):
+            raise FormatError(f"{path}: vertex id overflow")
+        src = pairs[:, 0].astype(np.int64)
+        dst = pairs[:, 1].astype(np.int64)
+    elif fmt == "text":
+        src, dst, header_n = _parse_text(path)
+    else:
+        raise ValueError(f"unknown format {fmt!r}")
+    if header_n is not None:
+        n = int(header_n)
+    else:
+        n = int(max(src.max(initial=-1), dst.max(initial=-1))) + 1
+    if len(src) and (src.min() < 0 or dst.min() < 0 or src.max() >= n or dst.max() >= n):
+        raise FormatError(f"{path}: vertex id out of range [0, {n})")
+    return EdgeList(src, dst, n=n)
