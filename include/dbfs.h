@@ -16,6 +16,7 @@
  *   dbfs_graph_build_edges    <- partition_graph(EdgeList, theta, shape) (partition.py:343-351)
  *   dbfs_graph_export_*       <- PartitionedGraph / WorkerGraph fields    (partition.py:263-292)
  *   dbfs_bfs                  <- engine.run_bfs                           (engine.py:98-330)
+ *   dbfs_bfs_batch            <- engine.benchmark's per-source loop       (engine.py:333-364)
  *   dbfs_bfs_iteration        <- BfsRun.per_iteration records             (engine.py:291-302)
  *   dbfs_validate             <- NEW: Graph500 certificate (nearest
  *                                reference analogue is cli.cmd_verify, cli.py:159-174)
@@ -89,8 +90,11 @@ typedef struct {
     int32_t engine;             /* 0 auto, 1 host-driven level loop, 2 persistent kernel, 3 peer (multi-GPU persistent over CUDA IPC) */
     int32_t record_iterations;  /* keep per-iteration records for dbfs_bfs_iteration */
     int32_t exec_policy;        /* 1: on symmetric graphs in dobfs mode, execute a FORWARD-reported
-                                   kind as the equivalent pull when cheaper (reported directions and
-                                   counters unchanged); 0: execute exactly the reported directions */
+                                   kind as the equivalent pull, or a BACKWARD-reported kind as a
+                                   counting push (twin positions recover the pull's early-exit
+                                   counters), when cheaper -- reported directions and counters
+                                   unchanged; 2: counting push wherever possible (tests);
+                                   0: execute exactly the reported directions */
 } dbfs_bfs_options;
 
 typedef struct {
@@ -190,6 +194,12 @@ int32_t dbfs_graph_export_classification(const dbfs_graph *g, int64_t *out_degre
 int32_t dbfs_bfs(dbfs_graph *g, const dbfs_bfs_options *opts, int32_t *levels_out,
                  int64_t *parents_out, dbfs_run_stats *stats);
 int32_t dbfs_fetch_result(dbfs_graph *g, int32_t *levels_out, int64_t *parents_out);
+/* Many roots in one call (benchmark(), Graph500's 64-root loop): root k's depth and
+ * parent arrays land in levels_out[k] / parents_out[k] (host, pinned for overlap; the
+ * arrays of pointers and any entry may be NULL).  The D2H of root k runs on a copy
+ * stream while root k+1 traverses.  stats (nullable) receives count entries. */
+int32_t dbfs_bfs_batch(dbfs_graph *g, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
+                       int32_t *const *levels_out, int64_t *const *parents_out, dbfs_run_stats *stats);
 /* Per-iteration record `it` of the last dbfs_bfs; directions int8[p*4] (0 fwd, 1 bwd) and
  * bv double[p*4] (inf = None) are per worker (both nullable). */
 int32_t dbfs_bfs_iteration(const dbfs_graph *g, int64_t it, dbfs_iteration *rec, int8_t *directions,

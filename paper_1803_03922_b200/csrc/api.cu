@@ -115,6 +115,11 @@ int32_t dbfs_ctx_destroy(dbfs_ctx *ctx) {
         ctx->c.flush.release();
         if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
         if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
+        for (int b = 0; b < 2; b++) {
+            if (ctx->c.ev_ready[b]) cudaEventDestroy(ctx->c.ev_ready[b]);
+            if (ctx->c.ev_done[b]) cudaEventDestroy(ctx->c.ev_done[b]);
+        }
+        if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
         if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
         delete ctx;
     });
@@ -309,6 +314,16 @@ int32_t dbfs_bfs(dbfs_graph *gg, const dbfs_bfs_options *opts, int32_t *levels_o
         run_bfs(g, *opts, stats);
         if (levels_out || parents_out) fetch_result(g, levels_out, parents_out);
         if (stats) stats->d2h_bytes += (levels_out ? 4 * g.n : 0) + (parents_out ? 8 * g.n : 0);
+    });
+}
+
+int32_t dbfs_bfs_batch(dbfs_graph *gg, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
+                       int32_t *const *levels_out, int64_t *const *parents_out, dbfs_run_stats *stats) {
+    return guard([&] {
+        DBFS_CHECK(opts && count >= 0 && (roots || count == 0), DBFS_EINVAL, "bad arguments");
+        Graph &g = gg->g;
+        DBFS_CUDA(cudaSetDevice(g.ctx->device));
+        run_bfs_batch(g, *opts, roots, count, levels_out, parents_out, stats);
     });
 }
 

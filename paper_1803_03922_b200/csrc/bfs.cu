@@ -157,7 +157,7 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
 __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__restrict__ views, int W, int64_t source,
                                                        uint32_t src_del, GridBar *bar, int rec_cap,
                                                        AsmArgs asm_args, int do_assemble, GridBar *gbar,
-                                                       int nranks) {
+                                                       int nranks, const uint32_t *__restrict__ del_id) {
     extern __shared__ uint4 dsm[];
     Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     if (timer) V.ctl->t_start = globaltimer_ns();
     phase_init(V, wb, nb);
     if (!grid_sync(bar, nblocks, gbar, nranks)) return;
-    if (wb == 0 && threadIdx.x == 0) seed_worker(V, source, src_del);
+    if (wb == 0 && threadIdx.x == 0)  // SRC_DEL_LOOKUP: the host did not read del_id[source] (dbfs_bfs_batch)
+        seed_worker(V, source, src_del == SRC_DEL_LOOKUP ? __ldg(&del_id[source]) : src_del);
     if (!grid_sync(bar, nblocks, gbar, nranks)) return;
     if (timer) V.ctl->t_seeded = globaltimer_ns();
     int L = 0;
@@ -198,6 +199,29 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     // start the next BFS (host resets the block) before every GPU is past it
     if (gbar && !grid_sync(bar, nblocks, gbar, nranks)) return;
     if (do_assemble) phase_assemble(asm_args, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
+}
+
+// dbfs_bfs_batch helpers.  Between roots the stream only runs kernels: a
+// cudaMemset/cudaMemcpy would queue on a copy engine behind the previous
+// root's result D2H and serialise the pipeline.
+__global__ void k_batch_prep(const View *__restrict__ views, GridBar *bar) {
+    static_assert(sizeof(Ctl) % 8 == 0, "Ctl is cleared in 8-byte words");
+    unsigned long long *c = reinterpret_cast<unsigned long long *>(views[blockIdx.x].ctl);
+    for (size_t i = threadIdx.x; i < sizeof(Ctl) / 8; i += blockDim.x) c[i] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *bar = GridBar{0u, 0u, 0u, 0u};
+}
+
+__global__ void k_batch_info(const Ctl *__restrict__ ctl0, const GridBar *__restrict__ bar, int2 *info) {
+    *info = make_int2(ctl0->last_level, (int)bar->abort);
+}
+
+__global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, int64_t bytes) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n16 = bytes >> 4;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (int64_t i = tid; i < n16; i += nth) d4[i] = __ldcs(&s4[i]);
+    for (int64_t i = (n16 << 4) + tid; i < bytes; i += nth) dst[i] = src[i];
 }
 
 __global__ void __launch_bounds__(BT) k_init(const View *__restrict__ views, int W) {
@@ -241,6 +265,7 @@ void build_sorted_dd(Graph &g);
 static void ensure_resources(Graph &g) {
     if (g.bfs_ready) return;
     if (g.symmetric) build_sorted_dd(g);
+    if (g.symmetric && !getenv("DBFS_NO_TWINS")) build_twins(g);
     Ctx &ctx = *g.ctx;
     const int W = (int)g.workers.size();
     g.W = W;
@@ -299,6 +324,11 @@ static void ensure_resources(Graph &g) {
         }
         Wk.ctl.alloc(1);
         Wk.rec.alloc(g.rec_cap);
+        for (int k = 1; k < 4; k++)
+            if (Wk.twin[k].n && !Wk.first[k].n) {
+                Wk.first[k].alloc(std::max<int64_t>(k == KIND_DN ? nl : g.d, 1));
+                DBFS_CUDA(cudaMemset(Wk.first[k].p, 0xff, Wk.first[k].bytes()));
+            }
     }
     if (g.p > 1 || g.dist) {
         g.glevel.alloc(std::max<int64_t>(g.n, 1));
@@ -350,6 +380,10 @@ static void ensure_resources(Graph &g) {
         V.del_gid = g.del_gid.p;
         // indexed with absolute dd offsets (the worker's copy starts at dd_base)
         V.col_sorted_dd = Wk.col_sorted.n ? Wk.col_sorted.p - Wk.dd_base : nullptr;
+        for (int k = 1; k < 4; k++) {
+            V.twin[k] = Wk.twin[k].n ? Wk.twin[k].p - Wk.twin_base[k] : nullptr;
+            V.first[k] = Wk.twin[k].n ? Wk.first[k].p : nullptr;
+        }
         V.nlevel = Wk.nlevel.p;
         V.nparent = Wk.nparent.p;
         V.dlevel = Wk.dlevel.p;
@@ -629,11 +663,10 @@ static void setup_peer(Graph &g) {
 
 // ------------------------------------------------------------------ driver
 
-void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
+// Options of one run into the device views (uploaded on the context stream);
+// returns the engine to use (1 host loop, 2 persistent, 3 peer).
+static int configure_run(Graph &g, const dbfs_bfs_options &o) {
     Ctx &ctx = *g.ctx;
-    DBFS_CHECK(o.mode == 0 || o.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
-    DBFS_CHECK(0 <= o.source && o.source < g.n, DBFS_ERANGE,
-               "source " + std::to_string(o.source) + " out of range [0, " + std::to_string(g.n) + ")");
     ensure_resources(g);
     const int W = g.W;
     const bool parents = o.parent_mode != 0;
@@ -700,6 +733,17 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         DBFS_CUDA(cudaMemcpyAsync(g.peer_view.p, &P, sizeof(View), cudaMemcpyHostToDevice, ctx.stream));
     }
     DBFS_CUDA(cudaMemcpyAsync(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice, ctx.stream));
+    return engine;
+}
+
+void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
+    Ctx &ctx = *g.ctx;
+    DBFS_CHECK(o.mode == 0 || o.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
+    DBFS_CHECK(0 <= o.source && o.source < g.n, DBFS_ERANGE,
+               "source " + std::to_string(o.source) + " out of range [0, " + std::to_string(g.n) + ")");
+    const int engine = configure_run(g, o);
+    const int W = g.W;
+    const bool parents = o.parent_mode != 0;
     uint32_t src_del = 0xffffffffu;
     DBFS_CUDA(cudaMemcpyAsync(&src_del, g.del_id.p + o.source, 4, cudaMemcpyDeviceToHost, ctx.stream));
     for (auto &Wk : g.workers) DBFS_CUDA(cudaMemsetAsync(Wk.ctl.p, 0, sizeof(Ctl), ctx.stream));
@@ -729,7 +773,11 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         pgrid = g.pgrid;
         g.warps_per_worker = (double)pgrid / W * WPB;
     }
-    if (engine == 3) DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    // Distributed: line the ranks up right before the launch.  The persistent
+    // kernel's first grid barrier spans all GPUs, so a rank whose host reached
+    // the launch early would otherwise spend the others' host skew (python,
+    // driver calls: up to ~1 ms) spinning inside its own event window.
+    if (g.dist) nccl_barrier(ctx);
     DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
     if (engine >= 2) {
         int grid = pgrid;
@@ -739,8 +787,10 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         int do_asm = assemble ? 1 : 0;
         GridBar *gb = engine == 3 ? (GridBar *)g.gbar : nullptr;
         int nr = engine == 3 ? g.p : 1;
+        const uint32_t *dil = g.del_id.p;
         void *args[] = {(void *)&vp,      (void *)&W,  (void *)&src,    (void *)&src_del, (void *)&bar,
-                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm, (void *)&gb,      (void *)&nr};
+                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm, (void *)&gb,      (void *)&nr,
+                        (void *)&dil};
         DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, sizeof(Smem),
                                               ctx.stream));
         DBFS_LAUNCHED();
@@ -974,6 +1024,151 @@ void fetch_result(Graph &g, int32_t *levels, int64_t *parents) {
         DBFS_CUDA(cudaMemcpyAsync(parents, g.parents_dev(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
     }
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+// Pipelined roots (dbfs_bfs_batch): after root k traverses, its depth/parent
+// arrays are copied device-to-device into staging buffer k%2 (a few tens of
+// us at HBM speed) and then to the caller's host buffers on a non-blocking
+// copy stream, so the PCIe transfer of root k overlaps the traversal of root
+// k+1.  Staging buffer b is reused only after its previous D2H has finished.
+static void ensure_copy_stream(Ctx &ctx) {
+    if (ctx.copy_stream) return;
+    DBFS_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+        DBFS_CUDA(cudaEventCreateWithFlags(&ctx.ev_ready[b], cudaEventDisableTiming));
+        DBFS_CUDA(cudaEventCreateWithFlags(&ctx.ev_done[b], cudaEventDisableTiming));
+    }
+}
+
+void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, int64_t count, int32_t *const *levels,
+                   int64_t *const *parents, dbfs_run_stats *st) {
+    Ctx &ctx = *g.ctx;
+    DBFS_CHECK(o0.mode == 0 || o0.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
+    for (int64_t k = 0; k < count; k++)
+        DBFS_CHECK(0 <= roots[k] && roots[k] < g.n, DBFS_ERANGE,
+                   "source " + std::to_string(roots[k]) + " out of range [0, " + std::to_string(g.n) + ")");
+    if (count == 0) return;
+    ensure_copy_stream(ctx);
+    const bool want_par = parents != nullptr && o0.parent_mode != 0;
+    for (int b = 0; b < 2; b++) {
+        if (levels && g.stage_lv[b].n != g.n) g.stage_lv[b].alloc(g.n);
+        if (want_par && g.stage_pv[b].n != g.n) g.stage_pv[b].alloc(g.n);
+    }
+    auto stage_and_copy = [&](int64_t k, bool used_b) {
+        const int b = (int)(k & 1);
+        if (used_b) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[b], 0));
+        const int blocks = ctx.num_sms * 4;
+        if (levels && levels[k]) {
+            k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.levels_dev(), (uint8_t *)g.stage_lv[b].p,
+                                                         4 * g.n);
+            DBFS_LAUNCHED();
+        }
+        if (want_par && parents[k]) {
+            k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(), (uint8_t *)g.stage_pv[b].p,
+                                                         8 * g.n);
+            DBFS_LAUNCHED();
+        }
+        DBFS_CUDA(cudaEventRecord(ctx.ev_ready[b], ctx.stream));
+        DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
+        if (levels && levels[k])
+            DBFS_CUDA(cudaMemcpyAsync(levels[k], g.stage_lv[b].p, 4 * g.n, cudaMemcpyDeviceToHost, ctx.copy_stream));
+        if (want_par && parents[k])
+            DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * g.n, cudaMemcpyDeviceToHost, ctx.copy_stream));
+        DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
+        if (st) st[k].d2h_bytes += (levels && levels[k] ? 4 * g.n : 0) + (want_par && parents[k] ? 8 * g.n : 0);
+    };
+    const int engine = configure_run(g, o0);
+    if (engine != 2) {
+        // distributed / host-loop engines: run_bfs per root (its host round trips
+        // bound the overlap), copies still on the copy stream
+        for (int64_t k = 0; k < count; k++) {
+            dbfs_bfs_options o = o0;
+            o.source = roots[k];
+            run_bfs(g, o, st ? &st[k] : nullptr);
+            dist_assemble(g);
+            stage_and_copy(k, k >= 2);
+        }
+        DBFS_CUDA(cudaStreamSynchronize(ctx.copy_stream));
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+        return;
+    }
+    // Single-process persistent engine: every root is enqueued without a host
+    // round trip -- prep kernel (control blocks, barrier), the traversal (the
+    // source's delegate id looked up on device), an info kernel (iterations,
+    // watchdog) and the staging copy; the D2H runs on the copy stream.
+    const int W = g.W;
+    set_smem_attrs();
+    if (g.pgrid <= 0) {
+        int bps = 0;
+        g.pgrid = persistent_grid(g, &bps);
+    }
+    int grid = g.pgrid;
+    g.warps_per_worker = (double)grid / W * WPB;
+    AsmArgs aa = make_asm(g, o0.parent_mode != 0);
+    int do_asm = g.p > 1 ? 1 : 0;
+    GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
+    DArray<int2> info;
+    info.alloc(count);
+    std::vector<cudaEvent_t> evs(2 * count, nullptr);
+    for (auto &e : evs) DBFS_CUDA(cudaEventCreate(&e));
+    const int64_t launches0 = g_kernel_launches;
+    const View *vp = g.views.p;
+    int rec_cap = g.rec_cap;
+    GridBar *gb = nullptr;
+    int nr = 1;
+    const uint32_t *dil = g.del_id.p;
+    uint32_t sdel = SRC_DEL_LOOKUP;
+    for (int64_t k = 0; k < count; k++) {
+        int64_t src = roots[k];
+        k_batch_prep<<<W, 256, 0, ctx.stream>>>(g.views.p, bar);
+        DBFS_LAUNCHED();
+        DBFS_CUDA(cudaEventRecord(evs[2 * k], ctx.stream));
+        void *args[] = {(void *)&vp,      (void *)&W,  (void *)&src,    (void *)&sdel, (void *)&bar,
+                        (void *)&rec_cap, (void *)&aa, (void *)&do_asm, (void *)&gb,   (void *)&nr,
+                        (void *)&dil};
+        DBFS_CUDA(cudaLaunchCooperativeKernel((void *)k_bfs_persistent, dim3(grid), dim3(BT), args, sizeof(Smem),
+                                              ctx.stream));
+        DBFS_LAUNCHED();
+        DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
+        k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k);
+        DBFS_LAUNCHED();
+        stage_and_copy(k, k >= 2);
+    }
+    DBFS_CUDA(cudaStreamSynchronize(ctx.copy_stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::vector<int2> hi(count);
+    DBFS_CUDA(cudaMemcpy(hi.data(), info.p, sizeof(int2) * count, cudaMemcpyDeviceToHost));
+    const int64_t launches = g_kernel_launches - launches0;
+    bool aborted = false;
+    for (int64_t k = 0; k < count; k++) {
+        aborted |= hi[k].y != 0;
+        if (st) {
+            float ms = 0.f;
+            DBFS_CUDA(cudaEventElapsedTime(&ms, evs[2 * k], evs[2 * k + 1]));
+            dbfs_run_stats &r = st[k];
+            const int64_t d2h = r.d2h_bytes;
+            memset(&r, 0, sizeof(r));
+            r.iterations = hi[k].x;
+            r.reached = -1;
+            r.device_ms = ms;
+            r.kernel_launches = launches / count;
+            r.engine_used = 2;
+            r.per_iteration_truncated = 1;  // records are not collected in batch mode
+            r.h2d_bytes = k == 0 ? (int64_t)(sizeof(View) * W) : 0;
+            r.d2h_bytes = d2h + (int64_t)sizeof(int2);
+        }
+    }
+    for (auto &e : evs) cudaEventDestroy(e);
+    DBFS_CHECK(!aborted, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
+    g.last_iterations = hi[count - 1].x;
+    g.last_truncated = true;
+    g.last_rec.clear();
+    g.last_source = roots[count - 1];
+    g.last_parent_mode = o0.parent_mode;
+    g.last_valid = true;
+    g.last_mode = o0.mode;
+    g.last_la = o0.local_all2all;
+    g.last_uq = o0.uniquify;
 }
 
 // ------------------------------------------------ min-ID parents (A19) / A20

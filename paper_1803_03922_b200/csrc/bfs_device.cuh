@@ -55,6 +55,8 @@ __device__ __forceinline__ bool coarse_hit(const uint32_t *filt, uint32_t x) {
     return (filt[(x >> 10) & (FW - 1)] >> (x & 31)) & 1u;
 }
 
+constexpr uint32_t SRC_DEL_LOOKUP = 0xfffffffeu;  // seed: look the source's delegate id up on device
+
 struct GridBar {
     unsigned int count;
     unsigned int gen;
@@ -162,6 +164,19 @@ __host__ __device__ inline void level_dirs(const View &V, const Ctl &c, int L, i
 // k-candidates find the same vertex set, so the executor takes the cheaper one
 // (estimated L2 requests: push ~4 per edge with its atomics, pull ~1.5 per
 // scanned entry with hit probability FV_k / nnz_k).
+//
+// A BACKWARD-reported kind may run as a counting push (PUSHC): the frontier's
+// k-rows are pushed and every unvisited target v keeps the minimum twin
+// position (where v's reverse row holds the pushing parent), so F(L) knows the
+// pull's early-exit index of every found v; the unvisited candidates' row
+// lengths sum to nnz[rev] - cumfv[rev].  The pull counter is that sum minus
+// (len - first - 1) per found v.  With FV_k = 0 no candidate can hit and the
+// counter is the sum alone (no twins needed).  exec_policy 2 (tests) takes
+// PUSHC whenever twins exist.
+constexpr int PUSHC = 2;
+
+__host__ __device__ inline int rev_kind(int k) { return k == KIND_ND ? KIND_DN : (k == KIND_DN ? KIND_ND : KIND_DD); }
+
 __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, const unsigned long long *cum,
                                           const int dirs[4], int ex[4]) {
     for (int k = 0; k < 4; k++) ex[k] = dirs[k];
@@ -170,7 +185,29 @@ __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, con
     const unsigned long long u_dn = V.total_src[KIND_DN] - cum[KIND_DN];
     const unsigned long long u_dd = V.total_src[KIND_DD] - cum[KIND_DD];
     for (int k = 1; k < 4; k++) {
-        if (dirs[k] != FWD || S.fv[k] == 0) continue;
+        if (dirs[k] == BWD) {
+            if (S.fv[k] == 0) {
+                ex[k] = PUSHC;
+                continue;
+            }
+            if (!V.twin[k]) continue;
+            if (V.exec_policy == 2) {
+                ex[k] = PUSHC;
+                continue;
+            }
+            const int rev = rev_kind(k);
+            double U = (double)(k == KIND_ND ? u_dn : (k == KIND_DN ? u_nd : u_dd));
+            double rows = (double)(V.total_src[rev] ? V.total_src[rev] : 1);
+            double avg = (double)V.nnz[rev] / rows;
+            double scan = (double)V.nnz[k] / (double)S.fv[k];
+            if (scan > avg) scan = avg;
+            double words = (double)(rev == KIND_ND ? V.nw_n : V.nw_d);
+            double pull = 1.5 * U * scan + 0.25 * words;
+            double push = 5.0 * (double)S.fv[k];  // push + twin load + atomicMin
+            if (push < pull) ex[k] = PUSHC;
+            continue;
+        }
+        if (V.exec_policy == 2 || S.fv[k] == 0) continue;
         // reverse kind scanned by the equivalent pull, and its candidate count
         int rev = k == KIND_ND ? KIND_DN : (k == KIND_DN ? KIND_ND : KIND_DD);
         double U = (double)(k == KIND_ND ? u_dn : (k == KIND_DN ? u_nd : u_dd));
@@ -216,7 +253,7 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
     r.dfront = S.dfront;
     r.rows = S.pull_rows;
     for (int k = 0; k < 4; k++)
-        if (k == KIND_NN || r.dir[k] == FWD) r.rows += S.q[k];
+        if (k == KIND_NN || S.exec_dir[k] != BWD) r.rows += S.q[k];
     r.dirty = S.dirty;
     r.new_del = S.new_del;
     unsigned long long msgs = 0;
@@ -475,9 +512,10 @@ __device__ __forceinline__ bool push_edge(const View &V, int L, uint32_t col, in
 // Second stage of a push step: UNR columns per lane are resolved with all
 // status loads issued before any store (stores through the non-restrict state
 // pointers would otherwise serialise one L2 round trip per edge).
-template <int ACT>
+template <int ACT, bool CNT>
 __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t (&cc)[UNR], const uint32_t (&pp)[UNR],
-                                           const bool (&valid)[UNR], VisitCounters &vc) {
+                                           const uint32_t (&tw)[UNR], uint32_t *first, const bool (&valid)[UNR],
+                                           VisitCounters &vc) {
     // map the column to the (worker-local) vertex it names
     uint32_t tgt[UNR];
     bool local[UNR];
@@ -501,6 +539,9 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
     for (int u = 0; u < UNR; u++) {
         bool open = !((s[u] >> (tgt[u] & 31)) & 1u);
         if (ACT == ACT_DELEG && open) vc.dirty = 1;
+        // counting push: every parent of an unvisited target bids its twin
+        // position, claimed this level or not (the pull stops at the first)
+        if (CNT && open) atomicMin(&first[tgt[u]], tw[u]);
         s[u] = open ? __ldcg(&nxt[tgt[u] >> 5]) : 0xffffffffu;
     }
     // stage 3: fire-and-forget marks (RED.OR, no return value) and plain stores:
@@ -531,15 +572,17 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
 
 // Expand <= 32 rows held one per lane (row start rb, length len, payload par)
 // with all lanes on consecutive edges and UNR independent loads per lane.
-template <int ACT>
+template <int ACT, bool CNT = false>
 __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint32_t *__restrict__ col, int64_t rb,
-                                               uint32_t len, uint32_t par, VisitCounters &vc) {
+                                               uint32_t len, uint32_t par, VisitCounters &vc,
+                                               const uint32_t *__restrict__ twin = nullptr, uint32_t *first = nullptr) {
     unsigned tot;
     unsigned excl = warp_excl_scan(len, &tot);
     const unsigned lane = lane_id();
     for (unsigned base = 0; base < tot; base += 32 * UNR) {
         uint32_t cc[UNR];
         uint32_t pp[UNR];
+        uint32_t tw[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; u++) {
             unsigned x = base + u * 32 + lane;
@@ -548,21 +591,23 @@ __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint3
             unsigned eo = __shfl_sync(FULL, excl, o);
             pp[u] = __shfl_sync(FULL, par, o);
             cc[u] = x < tot ? __ldg(&col[rbo + (x - eo)]) : 0u;
+            tw[u] = (CNT && x < tot) ? __ldg(&twin[rbo + (x - eo)]) : 0u;
         }
         bool valid[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < tot;
-        push_stage<ACT>(V, L, cc, pp, valid, vc);
+        push_stage<ACT, CNT>(V, L, cc, pp, tw, first, valid, vc);
     }
 }
 
 // Load-balanced push over a delegate frontier list (dlist, exclusive prefix
 // dpre, `cnt` rows, `total` edges): this warp handles edges [x0, x1).
-template <int ACT>
+template <int ACT, bool CNT>
 __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *__restrict__ off,
                                           const uint32_t *__restrict__ col, const uint32_t *__restrict__ list,
                                           const int64_t *__restrict__ pre, int64_t cnt, int64_t total, int64_t x0,
-                                          int64_t x1, VisitCounters &vc) {
+                                          int64_t x1, VisitCounters &vc, const uint32_t *__restrict__ twin,
+                                          uint32_t *first) {
     if (x0 >= x1) return;
     const unsigned lane = lane_id();
     // 32-ary search: largest e with pre[e] <= x0
@@ -596,6 +641,7 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
         for (int64_t base = x0; base < lim; base += 32 * UNR) {
             uint32_t cc[UNR];
             uint32_t pp[UNR];
+            uint32_t tw[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) {
                 int64_t x = base + u * 32 + lane;
@@ -604,11 +650,12 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
                 int64_t pbo = __shfl_sync(FULL, pb, o);
                 pp[u] = __shfl_sync(FULL, gx, o);
                 cc[u] = x < lim ? __ldg(&col[rbo + (x - pbo)]) : 0u;
+                tw[u] = (CNT && x < lim) ? __ldg(&twin[rbo + (x - pbo)]) : 0u;
             }
             bool valid[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < lim;
-            push_stage<ACT>(V, L, cc, pp, valid, vc);
+            push_stage<ACT, CNT>(V, L, cc, pp, tw, first, valid, vc);
         }
         x0 = lim;
         i += 32;
@@ -829,11 +876,17 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     int ex[4];
     exec_dirs(V, S, cum, dirs, ex);
     if (wb == 0 && threadIdx.x == 0) {
+        unsigned long long cumfv[4];
+        for (int k = 0; k < 4; k++) cumfv[k] = (L == 0 ? 0ull : C.cumfv[(L + 1) & 1][k]) + S.fv[k];
         for (int k = 0; k < 4; k++) {
             C.dir[L & 1][k] = dirs[k];
             C.cumq[L & 1][k] = cum[k];
+            C.cumfv[L & 1][k] = cumfv[k];
             C.s[L % 3].exec_dir[k] = ex[k];
-            if (k > 0 && ex[k] == FWD) C.s[L % 3].work[k] = S.fv[k];
+            if (k > 0 && ex[k] != BWD) C.s[L % 3].work[k] = S.fv[k];
+            // counting push: the candidates' reverse-row lengths; F(L) takes off
+            // what the early exits of the found ones skip
+            if (k > 0 && ex[k] == PUSHC) atomicAdd(&C.s[L % 3].insp_bwd[k], V.nnz[rev_kind(k)] - cumfv[rev_kind(k)]);
         }
     }
     VisitCounters vc = {};
@@ -852,7 +905,8 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     // T1: normal frontier -- nn push (always, engine.py:207-222) + nd push.
     tt.start();
     if (S.nfront > 0) {
-        const bool nd_fwd = ex[KIND_ND] == FWD;
+        const bool nd_fwd = ex[KIND_ND] != BWD && S.fv[KIND_ND] > 0;
+        const bool nd_cnt = ex[KIND_ND] == PUSHC && V.first[KIND_ND];
         const uint32_t *has_nn = V.src_bits[KIND_NN], *has_nd = V.src_bits[KIND_ND];
         for (WarpChunks ch(S.nfront > (unsigned long long)TW ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW);
              ch.valid(); ch.next()) {
@@ -872,7 +926,11 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                 warp_rows_push<ACT_NN>(V, L, V.col[KIND_NN], b, (uint32_t)(e - b), gid, vc);
                 if (nd_fwd) {
                     int64_t b2 = ok ? __ldg(&V.off[KIND_ND][u]) : 0, e2 = ok ? __ldg(&V.off[KIND_ND][u + 1]) : 0;
-                    warp_rows_push<ACT_DELEG>(V, L, V.col[KIND_ND], b2, (uint32_t)(e2 - b2), gid, vc);
+                    if (nd_cnt)
+                        warp_rows_push<ACT_DELEG, true>(V, L, V.col[KIND_ND], b2, (uint32_t)(e2 - b2), gid, vc,
+                                                        V.twin[KIND_ND], V.first[KIND_ND]);
+                    else
+                        warp_rows_push<ACT_DELEG>(V, L, V.col[KIND_ND], b2, (uint32_t)(e2 - b2), gid, vc);
                 }
             }
             __syncwarp();
@@ -884,19 +942,27 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     // edge space (engine.py:238-263).
     tt.start();
     const unsigned long long EM = (1ull << V.dshift) - 1;  // packed list: count << dshift | edges
-    if (ex[KIND_DN] == FWD && (S.dpack[0] & EM)) {
+    if (ex[KIND_DN] != BWD && (S.dpack[0] & EM)) {
         int64_t cnt = (int64_t)(S.dpack[0] >> V.dshift), total = (int64_t)(S.dpack[0] & EM);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
-        list_push<ACT_NORMAL>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1], cnt, total,
-                              x0, x1, vc);
+        if (ex[KIND_DN] == PUSHC && V.first[KIND_DN])
+            list_push<ACT_NORMAL, true>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1], cnt,
+                                        total, x0, x1, vc, V.twin[KIND_DN], V.first[KIND_DN]);
+        else
+            list_push<ACT_NORMAL, false>(V, L, V.off[KIND_DN], V.col[KIND_DN], V.dlist[0][L & 1], V.dpre[0][L & 1],
+                                         cnt, total, x0, x1, vc, nullptr, nullptr);
     }
     tt.stop(AT, 1);
     tt.start();
-    if (ex[KIND_DD] == FWD && (S.dpack[1] & EM)) {
+    if (ex[KIND_DD] != BWD && (S.dpack[1] & EM)) {
         int64_t cnt = (int64_t)(S.dpack[1] >> V.dshift), total = (int64_t)(S.dpack[1] & EM);
         int64_t x0 = gw * total / TW, x1 = (gw + 1) * total / TW;
-        list_push<ACT_DELEG>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1], cnt, total,
-                             x0, x1, vc);
+        if (ex[KIND_DD] == PUSHC && V.first[KIND_DD])
+            list_push<ACT_DELEG, true>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1], cnt,
+                                       total, x0, x1, vc, V.twin[KIND_DD], V.first[KIND_DD]);
+        else
+            list_push<ACT_DELEG, false>(V, L, V.off[KIND_DD], V.col[KIND_DD], V.dlist[1][L & 1], V.dpre[1][L & 1],
+                                        cnt, total, x0, x1, vc, nullptr, nullptr);
     }
     tt.stop(AT, 2);
 
@@ -1010,7 +1076,20 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
 struct FinishCounters {
     unsigned long long dfv_dn, dq_dn, dfv_dd, dq_dd, new_del;
     unsigned long long nfv_nd, nq_nd, ncount;
+    unsigned long long skip[4];  // counting pushes: sum over found targets of (len - first - 1)
 };
+
+constexpr uint32_t NO_FIRST = 0xffffffffu;
+
+// Counting push of kind k at level L found target x (reverse-row length len):
+// the pull would have stopped after first+1 entries.  Resets the slot.
+__device__ __forceinline__ void take_first(uint32_t *first, uint32_t x, uint64_t len, unsigned long long &skip) {
+    const uint32_t f = first[x];
+    if (f != NO_FIRST) {
+        skip += len - f - 1;
+        first[x] = NO_FIRST;
+    }
+}
 
 // Delegate state of new delegate x (lane-held): level, parent, global output,
 // push-list row lengths.
@@ -1059,6 +1138,9 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     __syncthreads();
     const unsigned long long src = s_src;
     const bool dyn = src != 0;  // delegates were found: new-delegate work to balance
+    const LevelSlot &SL = V.ctl->s[L % 3];
+    uint32_t *cnt_nd = SL.exec_dir[KIND_ND] == PUSHC ? V.first[KIND_ND] : nullptr;
+    uint32_t *cnt_dd = SL.exec_dir[KIND_DD] == PUSHC ? V.first[KIND_DD] : nullptr;
     for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, DBFS_CWD, gw, TW); ch.valid(); ch.next()) {
         const int64_t base = ch.base();
         const int64_t wi = ch.word(V.nw_d);
@@ -1089,6 +1171,8 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
             if (i < cnt) {
                 uint64_t ldn, ldd;
                 new_delegate(V, L, list[i], ldn, ldd);
+                if (cnt_nd) take_first(cnt_nd, list[i], ldn, fc.skip[KIND_ND]);
+                if (cnt_dd) take_first(cnt_dd, list[i], ldd, fc.skip[KIND_DD]);
                 cdn += ldn > 0;
                 edn += ldn;
                 cdd += ldd > 0;
@@ -1192,6 +1276,7 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
     const uint32_t *nxt = V.nfront[(L + 1) & 1];
     const LevelSlot &A = V.ctl->s[L % 3];
     const bool dyn = A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
+    uint32_t *cnt_dn = A.exec_dir[KIND_DN] == PUSHC ? V.first[KIND_DN] : nullptr;
     for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[5] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
         const int64_t base = ch.base();
         const int64_t wi = ch.word(V.nw_n);
@@ -1214,6 +1299,7 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
             if (i < cnt) {
                 uint32_t c = list[i];
                 int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
+                if (cnt_dn) take_first(cnt_dn, c, (uint64_t)dnd, fc.skip[KIND_DN]);
                 fc.nfv_nd += (unsigned long long)dnd;
                 fc.nq_nd += dnd > 0;
                 fc.ncount++;
@@ -1247,6 +1333,10 @@ __device__ void flush_finish(const View &V, int L, FinishCounters &fc, int wb, b
     if (lane == 0) {
         atomic_add_u64(&N.dfront, v);
         atomic_add_u64(&A.new_del, v);
+    }
+    for (int k = 1; k < 4; k++) {
+        v = warp_sum(fc.skip[k]);
+        if (lane == 0 && v) atomicAdd(&A.insp_bwd[k], 0ull - v);  // V(L) added the full row lengths
     }
     if (zero_slot && wb == 0 && threadIdx.x == 0) {
         // slot (L+2)%3 is idle during level L: clear it for level L+2

@@ -922,6 +922,107 @@ void build_sorted_dd(Graph &g) {
     }
 }
 
+// ------------------------------------------------- twin positions (pull counters by push)
+
+// key = column, val = entry index, over one kind's entries [0, nnz)
+__global__ void k_col_keys(const uint32_t *__restrict__ col, int64_t nnz, uint32_t *__restrict__ key,
+                           uint32_t *__restrict__ val) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x) {
+        key[j] = col[j];
+        val[j] = (uint32_t)j;
+    }
+}
+
+// Sorted forward entries (by target, then source) and sorted reverse entries
+// (by row, then column) pair up index by index when the kind pair is the
+// reverse of itself; entry fv[t] of kind K gets the position of its source in
+// the target's reverse row.  Any mismatch (not symmetric) raises *bad.
+__global__ void k_twin_fill(const uint32_t *__restrict__ fv, const uint32_t *__restrict__ rv,
+                            const uint32_t *__restrict__ colK, const uint32_t *__restrict__ rowK,
+                            const uint32_t *__restrict__ colR, const uint32_t *__restrict__ rowR,
+                            const int64_t *__restrict__ offR, int64_t n, uint32_t *__restrict__ twin,
+                            unsigned *__restrict__ bad) {
+    const int64_t r0 = offR[0];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = fv[t], e2 = rv[t];
+        const uint32_t b = rowR[e2];
+        if (colK[e] != b || rowK[e] != colR[e2]) atomicOr(bad, 1u);
+        twin[e] = (uint32_t)((int64_t)e2 - (offR[b] - r0));
+    }
+}
+
+// Twin positions for the kinds a BACKWARD-reported level may execute as a
+// push: for every entry (u -> v) of kind K (nd, dn, dd) the
+// position of u in v's row of the reverse kind R (dn, nd, dd) -- the place a
+// pull of v would find u.  Alg. 1 keeps an edge and its reverse on one worker
+// for these kinds, so this is per worker.  Three stable radix sorts per kind.
+// A kind whose temporaries do not fit, or that is not its own reverse, keeps
+// no twins (its levels always pull).
+void build_twins(Graph &g) {
+    Ctx &ctx = *g.ctx;
+    static const int PAIR[4] = {-1, KIND_DN, KIND_ND, KIND_DD};
+    DArray<unsigned> bad;
+    bad.alloc(1);
+    for (auto &W : g.workers) {
+        for (int K = 1; K < 4; K++) {
+            const int R = PAIR[K];
+            const int64_t n = W.nnz[K];
+            if (n == 0 || n != W.nnz[R] || n >= ((int64_t)1 << 32) || W.twin[K].n) continue;
+            size_t fr = 0, tot = 0;
+            DBFS_CUDA(cudaMemGetInfo(&fr, &tot));
+            if ((double)n * 4.0 * 9.0 > 0.8 * (double)fr) continue;  // 8 temporaries + the twins
+            const int64_t *offK = g.off_all.p + W.base[K], *offR = g.off_all.p + W.base[R];
+            int64_t k0 = 0, r0 = 0;
+            DBFS_CUDA(cudaMemcpy(&k0, offK, 8, cudaMemcpyDeviceToHost));
+            DBFS_CUDA(cudaMemcpy(&r0, offR, 8, cudaMemcpyDeviceToHost));
+            const uint32_t *colK = g.col_all.p + k0, *colR = g.col_all.p + r0;
+            DArray<uint32_t> key, val, key2, val2, fv, rowK, rowR;
+            key.alloc(n);
+            val.alloc(n);
+            key2.alloc(n);
+            val2.alloc(n);
+            fv.alloc(n);
+            rowK.alloc(n);
+            rowR.alloc(n);
+            const int blocks = ctx.num_sms * 16;
+            k_row_ids<<<blocks, 256, 0, ctx.stream>>>(offK, W.rows[K], rowK.p);
+            DBFS_LAUNCHED();
+            k_row_ids<<<blocks, 256, 0, ctx.stream>>>(offR, W.rows[R], rowR.p);
+            DBFS_LAUNCHED();
+            // forward entries by (target, source): CSR order is by source, one stable pass by target
+            k_col_keys<<<blocks, 256, 0, ctx.stream>>>(colK, n, key.p, val.p);
+            DBFS_LAUNCHED();
+            bool alt = false;
+            radix_sort_pairs(ctx, key.p, val.p, key2.p, val2.p, n, bits_for(W.rows[R]), &alt);
+            DBFS_CUDA(cudaMemcpyAsync(fv.p, alt ? val2.p : val.p, 4 * n, cudaMemcpyDeviceToDevice, ctx.stream));
+            // reverse entries by (row, column): stable by column, then stable by row
+            k_col_keys<<<blocks, 256, 0, ctx.stream>>>(colR, n, key.p, val.p);
+            DBFS_LAUNCHED();
+            radix_sort_pairs(ctx, key.p, val.p, key2.p, val2.p, n, bits_for(W.rows[K]), &alt);
+            uint32_t *sv = alt ? val2.p : val.p, *kk = alt ? key.p : key2.p;  // kk: a free key buffer
+            k_row_keys<<<blocks, 256, 0, ctx.stream>>>(sv, rowR.p, n, kk);
+            DBFS_LAUNCHED();
+            uint32_t *k3 = kk == key.p ? key2.p : key.p, *v3 = sv == val.p ? val2.p : val.p;
+            bool alt2 = false;
+            radix_sort_pairs(ctx, kk, sv, k3, v3, n, bits_for(W.rows[R]), &alt2);
+            const uint32_t *rv = alt2 ? v3 : sv;
+            W.twin[K].alloc(n);
+            DBFS_CUDA(cudaMemsetAsync(bad.p, 0, 4, ctx.stream));
+            k_twin_fill<<<blocks, 256, 0, ctx.stream>>>(fv.p, rv, colK, rowK.p, colR, rowR.p, offR, n, W.twin[K].p,
+                                                        bad.p);
+            DBFS_LAUNCHED();
+            unsigned hb = 0;
+            DBFS_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, ctx.stream));
+            DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+            if (hb) {
+                W.twin[K].release();
+                continue;
+            }
+            W.twin_base[K] = k0;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ exports
 
 void export_csr(const Graph &g, int worker, int kind, int64_t *off, void *cols) {

@@ -46,6 +46,7 @@ struct Ctl {
     LevelSlot s[3];
     int dir[2][4];                   // sticky DirectionState by level parity
     unsigned long long cumq[2][4];   // visited source counts through the level, by parity
+    unsigned long long cumfv[2][4];  // sum of FV[k] over frontiers 0..L (row lengths of visited sources), by parity
     unsigned int bar_count, bar_gen; // grid barrier (persistent engine)
     unsigned int abort;              // watchdog / error flag
     int last_level;                  // iterations when the loop ended
@@ -104,6 +105,8 @@ struct View {
     const uint32_t *src_bits[4];     // rows present: [NN]/[ND] per local normal, [DN]/[DD] per delegate
     const uint32_t *deg[4];          // row lengths ([ND], [DN], [DD])
     const uint32_t *col_sorted_dd;   // dd rows reordered by neighbour degree (executor pulls only)
+    const uint32_t *twin[4];         // indexed by absolute entry position (nullptr: kind has no twins)
+    uint32_t *first[4];              // counting pushes: ND/DD per delegate, DN per local normal
     const int64_t *del_gid;
     int32_t *nlevel;
     int64_t *nparent;
@@ -187,6 +190,8 @@ struct Ctx {
     void *comm = nullptr;            // ncclComm_t
     DArray<unsigned char> scratch;   // reusable device scratch
     DArray<unsigned char> flush;     // L2 flush buffer (bench hygiene)
+    cudaStream_t copy_stream = nullptr;  // non-blocking: result D2H of dbfs_bfs_batch
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     int flush_val = 1;
     void *ensure_scratch(size_t bytes);
 };
@@ -202,6 +207,9 @@ struct WorkerHost {
     DArray<uint32_t> src_bits[4];
     DArray<uint32_t> deg[4];         // row lengths: [ND] per local normal, [DN]/[DD] per delegate
     DArray<uint32_t> col_sorted;     // dd rows with neighbours by descending degree (executor pulls)
+    DArray<uint32_t> twin[4];        // [ND]/[DN]/[DD]: per entry, the source's position in the target's reverse row
+    int64_t twin_base[4] = {0, 0, 0, 0};  // absolute col_all position of the kind's first entry
+    DArray<uint32_t> first[4];       // per target: min twin position found by a counting push (0xffffffff = none)
     DArray<uint32_t> sentbits;       // dist: remote targets already shipped this BFS (bit per global id)
     int64_t dd_base = 0;             // absolute offset of this worker's first dd entry
     // BFS state
@@ -270,6 +278,8 @@ struct Graph {
     std::vector<int64_t *> peer_nparent, peer_dparent;
     DArray<int32_t> asm_lv, asm_mylv;    // NCCL assembly buffers (kept between runs)
     DArray<int64_t> asm_pv, asm_mypv;
+    DArray<int32_t> stage_lv[2];     // dbfs_bfs_batch: result staging, double-buffered
+    DArray<int64_t> stage_pv[2];
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();
@@ -279,6 +289,7 @@ struct Graph {
 void mem_note(const Ctx &ctx, const char *what);  // DBFS_VERBOSE=1: free device memory at build stages
 void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm);
 void build_graph_edges(Graph &g, const int64_t *src, const int64_t *dst, int64_t m_local);
+void build_twins(Graph &g);
 void export_csr(const Graph &g, int worker, int kind, int64_t *off, void *cols);
 void export_sources(const Graph &g, int worker, int64_t *nd_src, uint8_t *dn, uint8_t *dd);
 void export_classification(const Graph &g, int64_t *deg, int64_t *del);
@@ -289,6 +300,8 @@ void rmat_generate_host(Ctx &ctx, const dbfs_rmat_params &prm, int64_t begin, in
 // bfs.cu
 void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st);
 void fetch_result(Graph &g, int32_t *levels, int64_t *parents);
+void run_bfs_batch(Graph &g, const dbfs_bfs_options &o, const int64_t *roots, int64_t count, int32_t *const *levels,
+                   int64_t *const *parents, dbfs_run_stats *st);
 void min_parents(Graph &g, int64_t *out);
 int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents);
 

@@ -31,6 +31,11 @@ MODES = ("bfs", "dobfs")
 KINDS = ("nn", "nd", "dn", "dd")
 PARENT_MODES = {None: 0, "none": 0, "any": 1, "min": 2}
 ENGINES = {"auto": 0, "host": 1, "persistent": 2, "peer": 3}
+# executor: "reported" runs the reference's directions; "cost" may pull a
+# FORWARD-reported kind or push a BACKWARD-reported one (counters recovered
+# exactly) when cheaper; "push" pushes every BACKWARD-reported kind
+# it can (tests of the counter recovery)
+EXEC_POLICIES = {"reported": 0, "cost": 1, "push": 2}
 
 
 class EmptyReportError(RuntimeError):
@@ -60,8 +65,8 @@ class BfsOptions:
             raise ValueError(f"parents must be one of {list(PARENT_MODES)}")
         if self.engine not in ENGINES:
             raise ValueError(f"engine must be one of {list(ENGINES)}")
-        if self.exec_policy not in ("cost", "reported"):
-            raise ValueError("exec_policy must be 'cost' or 'reported'")
+        if self.exec_policy not in EXEC_POLICIES:
+            raise ValueError(f"exec_policy must be one of {list(EXEC_POLICIES)}")
 
     def to_c(self) -> _lib.BfsOptionsC:
         o = _lib.BfsOptionsC()
@@ -76,7 +81,7 @@ class BfsOptions:
         o.parent_mode = PARENT_MODES[self.parents]
         o.engine = ENGINES[self.engine]
         o.record_iterations = 1
-        o.exec_policy = 1 if self.exec_policy == "cost" else 0
+        o.exec_policy = EXEC_POLICIES[self.exec_policy]
         return o
 
 
@@ -245,6 +250,40 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
     if parents == "min":
         par = min_parents(pg)
     return (levels, par, st) if stats else (levels, par)
+
+
+def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
+              stats: bool = False):
+    """Graph500's multi-root loop in one call (``dbfs_bfs_batch``): returns one
+    (depth, parent) pair per root.  The device-to-host copy of root k runs on a
+    separate stream while root k+1 traverses, so PCIe time hides behind the
+    BFS.  ``outs`` is a list of (levels int32[n], parents int64[n]) host arrays
+    (pinned for the overlap, see ``_lib.pinned_empty``); entries may repeat,
+    e.g. two buffer pairs used alternately, in which case each root's result is
+    in its pair until root k+2 overwrites it.  ``stats=True`` also returns the
+    per-root C run-stats structs."""
+    roots = np.ascontiguousarray([int(r) for r in roots], dtype=np.int64)
+    for r in roots:
+        if not (0 <= r < pg.n):
+            raise ValueError(f"source {r} out of range [0, {pg.n})")
+    count = len(roots)
+    if outs is None:
+        outs = [(np.empty(pg.n, dtype=np.int32), np.empty(pg.n, dtype=np.int64) if parents else None)
+                for _ in range(count)]
+    if len(outs) != count:
+        raise ValueError("outs must hold one (levels, parents) pair per root")
+    for lv, pa in outs:
+        if lv is not None and (lv.dtype != np.int32 or lv.size < pg.n or not lv.flags.c_contiguous):
+            raise ValueError("levels buffers must be contiguous int32[n]")
+        if pa is not None and (pa.dtype != np.int64 or pa.size < pg.n or not pa.flags.c_contiguous):
+            raise ValueError("parents buffers must be contiguous int64[n]")
+    lv_ptrs = (_lib.vp * max(count, 1))(*[lv.ctypes.data if lv is not None else None for lv, _ in outs])
+    pa_ptrs = (_lib.vp * max(count, 1))(*[pa.ctypes.data if pa is not None else None for _, pa in outs])
+    st = (_lib.RunStatsC * max(count, 1))()
+    opts = BfsOptions(mode=mode, source=int(roots[0]) if count else 0, parents=parents).to_c()
+    _lib.check(_lib.load().dbfs_bfs_batch(pg.handle, ctypes.byref(opts), roots.ctypes.data_as(_lib.vp), count,
+                                          lv_ptrs, pa_ptrs if parents else None, st), "bfs_batch")
+    return (outs, list(st)[:count]) if stats else outs
 
 
 def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any",

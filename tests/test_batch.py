@@ -1,0 +1,58 @@
+"""bfs_batch (dbfs_bfs_batch): the multi-root loop with overlapped result copies
+returns, for every root, exactly what one bfs() call returns (depths equal the
+oracle's; the parent tree passes the Graph500 certificate)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_1803_03922_b200 as api
+    from paper_1803_03922_b200 import _lib
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible for a -m gpu test")
+    return api
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2)])
+def test_batch_matches_single_calls_and_oracle(api, shape):
+    from paper_1803_03922_b200 import _lib
+    scale, seed, theta = 12, 3, 16
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=seed)), theta,
+                             api.ClusterShape(*shape))
+    src, dst = O.rmat_edges(scale, seed=seed)
+    og = O.partition(src, dst, 1 << scale, theta, *shape)
+    roots = [7, 100, 7, 4000, 17, 2]
+    outs, st = api.bfs_batch(pg, roots, stats=True)
+    assert len(outs) == len(roots) and len(st) == len(roots)
+    for r, (lv, pa), s in zip(roots, outs, st):
+        ref = O.run_bfs(og, r, mode="dobfs")
+        assert api.levels_digest(lv) == ref["levels_digest"]
+        assert s.iterations == ref["iterations"]
+        assert api.validate_bfs_tree(pg, r, lv, pa) == 0
+        lv1, _ = api.bfs(pg, r)
+        assert np.array_equal(lv, lv1)
+    # two pinned pairs used alternately: the last two roots' results survive
+    pairs = [(_lib.pinned_empty(pg.n, np.int32), _lib.pinned_empty(pg.n, np.int64)) for _ in range(2)]
+    outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(len(roots))]
+    api.bfs_batch(pg, roots, outs=outs, mode="bfs")
+    for i in (len(roots) - 2, len(roots) - 1):
+        lv, pa = outs[i]
+        assert api.levels_digest(lv) == O.run_bfs(og, roots[i], mode="bfs")["levels_digest"]
+        assert api.validate_bfs_tree(pg, roots[i], lv, pa) == 0
+
+
+def test_batch_errors(api):
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=8, seed=1)), 16, api.ClusterShape(1, 1))
+    with pytest.raises(ValueError):
+        api.bfs_batch(pg, [0, 1 << 8])
+    with pytest.raises(ValueError):
+        api.bfs_batch(pg, [0], outs=[(np.empty(3, np.int32), None)])
+    assert api.bfs_batch(pg, []) == []
+    lv = api.bfs_batch(pg, [5], parents=None)[0][0]
+    assert lv[5] == 0

@@ -81,12 +81,17 @@ def test_gpu_partition_matches_golden(api, gp):
 _RUNS = list(iter_runs(GOLD))
 
 
+@pytest.mark.parametrize("policy", ["cost", "push", "reported"])
 @pytest.mark.parametrize("gpr", _RUNS, ids=lambda x: graph_id(*x))
-def test_gpu_run_bfs_matches_golden(api, gpr):
+def test_gpu_run_bfs_matches_golden(api, gpr, policy):
+    """Every reported output equals the reference's, whatever the executor runs:
+    'cost' (the default), 'push' (every BACKWARD-reported kind as a counting
+    push, counters recovered from twin positions), 'reported' (pulls exactly
+    where the reference pulls)."""
     g, p, r = gpr
     pg = _pg(api, g, p)
     run = api.run_bfs(pg, api.BfsOptions(mode=r["mode"], source=r["source"], local_all2all=r["local_all2all"],
-                                         uniquify=r["uniquify"]))
+                                         uniquify=r["uniquify"], exec_policy=policy))
     want = r["report"]
     got = run.to_dict()
     assert got["levels_digest"] == want["levels_digest"]
@@ -214,9 +219,11 @@ def test_exec_policy_does_not_change_results(api, scale, theta):
     pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=1)), theta, api.ClusterShape(1, 1))
     rng = np.random.default_rng(scale)
     for root in rng.integers(0, 1 << scale, size=6):
-        a = api.run_bfs(pg, api.BfsOptions(source=int(root), exec_policy="cost"))
         b = api.run_bfs(pg, api.BfsOptions(source=int(root), exec_policy="reported"))
-        da, db = a.to_dict(), b.to_dict()
-        for key in ("iterations", "per_iteration", "inspections", "comm", "levels_digest"):
-            assert da[key] == db[key], key
-        assert api.validate_bfs_tree(pg, int(root), a.levels, a.parents) == 0
+        db = b.to_dict()
+        for policy in ("cost", "push"):
+            a = api.run_bfs(pg, api.BfsOptions(source=int(root), exec_policy=policy))
+            da = a.to_dict()
+            for key in ("iterations", "per_iteration", "inspections", "comm", "levels_digest"):
+                assert da[key] == db[key], (policy, key)
+            assert api.validate_bfs_tree(pg, int(root), a.levels, a.parents) == 0

@@ -45,7 +45,7 @@ for eng in engines:
         for it in range(st.iterations):
             L.dbfs_bfs_iteration(pg.handle, it, ctypes.byref(rec), dirs.ctypes.data_as(_lib.vp), None)
             lines.append(f"  L{it}: V {rec.visit_us:8.1f} F {rec.finish_us:7.1f} us  n={rec.frontier_normals:9d} "
-                         f"d={rec.frontier_delegates:8d} exec {''.join('FB'[x] for x in rec.exec_dirs)} "
+                         f"d={rec.frontier_delegates:8d} exec {''.join('FBP'[x] for x in rec.exec_dirs)} "
                          f"insp {list(rec.inspections)} work {list(rec.work)} nbytes {rec.normal_bytes} "
                          f"sync {[round(x, 1) for x in rec.sync_us]}")
             if max(rec.task_max_us) > 1:
