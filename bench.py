@@ -45,6 +45,25 @@ UNIT = "GTEPS"
 L2_BYTES = 126 << 20
 
 
+# The JSON line is the only thing on stdout: native libraries (NCCL's version
+# banner, CUDA) write to fd 1 directly, so fd 1 is pointed at stderr for the
+# whole run and the line goes to the saved original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    (_JSON_OUT or sys.stdout).write(json.dumps(line) + "\n")
+    (_JSON_OUT or sys.stdout).flush()
+
+
 GRAPH_NAME = {"rmat": "RMAT", "er": "Uniform random (Erdos-Renyi, RMAT with uniform quadrants)"}
 
 
@@ -153,7 +172,7 @@ def alg_bytes(st, n_total: int) -> float:
 def run_ours(args, world, rank, local_rank):
     import paper_1803_03922_b200 as api
     from paper_1803_03922_b200 import _lib
-    from paper_1803_03922_b200.engine import bfs, bfs_batch, bfs_device
+    from paper_1803_03922_b200.engine import batch_output_count, bfs, bfs_batch, bfs_device
 
     dist = world > 1
     tdist = None
@@ -213,17 +232,21 @@ def run_ours(args, world, rank, local_rank):
     # the traversal of step k+1; two pinned buffer pairs used alternately);
     # beside it the one-call-per-root bfs() loop.  No L2 flush inside the
     # timed batch: the graph (and each step's 12n-byte result) exceed L2.
-    pairs = [(_lib.pinned_empty(n, np.int32), _lib.pinned_empty(n, np.int64)) for _ in range(2)]
+    # (N > 1: each rank receives the vertices it owns, v mod N == rank -- the
+    # distributed Graph500 result; the one-call bfs() figure gathers all n on
+    # every rank)
+    nout = batch_output_count(pg, local=dist)
+    pairs = [(_lib.pinned_empty(nout, np.int32), _lib.pinned_empty(nout, np.int64)) for _ in range(2)]
     outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(args.steps)]
     step_roots = [roots[i % len(roots)] for i in range(args.steps)]
     if dist:
         ctx.barrier()
     t = time.perf_counter()
-    _, bst = bfs_batch(pg, step_roots, outs=outs, mode=args.mode, stats=True)
+    _, bst = bfs_batch(pg, step_roots, outs=outs, mode=args.mode, stats=True, local=dist)
     e2e_batch_s = time.perf_counter() - t
     h2d = sum(int(x.h2d_bytes) + 8 for x in bst)
     d2h = sum(int(x.d2h_bytes) for x in bst)
-    lv_buf, pa_buf = pairs[0]
+    lv_buf, pa_buf = _lib.pinned_empty(n, np.int32), _lib.pinned_empty(n, np.int64)
     e2e_s = []
     for i in range(args.steps):
         ctx.flush_l2()
@@ -279,7 +302,8 @@ def run_ours(args, world, rank, local_rank):
         "geomean_gteps": round(geomean, 4),
         "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h / args.steps),
-                "api": "bfs_batch: all steps in one call, D2H of step k overlapped with step k+1 (no L2 flush; graph > L2)",
+                "api": "bfs_batch: all steps in one call, D2H of step k overlapped with step k+1 (no L2 flush; graph > L2)"
+                       + ("; each rank receives the depth/parent entries of the vertices it owns" if dist else ""),
                 "per_call_bfs": round(e2e_single, 4)},
         "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
         "build_s": round(build_s, 3), "wall_s_timed": round(wall, 4), "validated_roots": validated,
@@ -303,7 +327,7 @@ def run_ours(args, world, rank, local_rank):
         del pg
         line["reference_labeling"] = _device_series(api, ctx, args, scale, theta, world, dist)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         tdist.barrier()
         tdist.destroy_process_group()
@@ -438,7 +462,7 @@ def run_reference(args, world, rank):
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build_s": round(build_s, 2),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def _oracle_degrees(og, O):
@@ -468,6 +492,7 @@ def main():
     ap.add_argument("--no-alt-labeling", action="store_true",
                     help="skip the extra device-time series on the reference labeling")
     args = ap.parse_args()
+    _claim_stdout()
     if args.warmup < 0 or args.steps < 1:
         ap.error("need steps >= 1")
     world = int(os.environ.get("WORLD_SIZE", "1"))

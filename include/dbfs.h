@@ -197,9 +197,15 @@ int32_t dbfs_fetch_result(dbfs_graph *g, int32_t *levels_out, int64_t *parents_o
 /* Many roots in one call (benchmark(), Graph500's 64-root loop): root k's depth and
  * parent arrays land in levels_out[k] / parents_out[k] (host, pinned for overlap; the
  * arrays of pointers and any entry may be NULL).  The D2H of root k runs on a copy
- * stream while root k+1 traverses.  stats (nullable) receives count entries. */
+ * stream while root k+1 traverses.  local != 0 in a distributed context: each rank
+ * receives only the vertices it owns (v mod p == rank, output i = vertex rank + i*p),
+ * the distributed Graph500 result; otherwise every rank gets all n.  Per-iteration
+ * records are not kept.  stats (nullable) receives count entries. */
 int32_t dbfs_bfs_batch(dbfs_graph *g, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
-                       int32_t *const *levels_out, int64_t *const *parents_out, dbfs_run_stats *stats);
+                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local,
+                       dbfs_run_stats *stats);
+/* Entries per output array of dbfs_bfs_batch (n, or this rank's own count when local). */
+int32_t dbfs_bfs_batch_output_count(const dbfs_graph *g, int32_t local, int64_t *count);
 /* Per-iteration record `it` of the last dbfs_bfs; directions int8[p*4] (0 fwd, 1 bwd) and
  * bv double[p*4] (inf = None) are per worker (both nullable). */
 int32_t dbfs_bfs_iteration(const dbfs_graph *g, int64_t it, dbfs_iteration *rec, int8_t *directions,

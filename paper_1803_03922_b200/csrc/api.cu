@@ -318,13 +318,17 @@ int32_t dbfs_bfs(dbfs_graph *gg, const dbfs_bfs_options *opts, int32_t *levels_o
 }
 
 int32_t dbfs_bfs_batch(dbfs_graph *gg, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
-                       int32_t *const *levels_out, int64_t *const *parents_out, dbfs_run_stats *stats) {
+                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local, dbfs_run_stats *stats) {
     return guard([&] {
         DBFS_CHECK(opts && count >= 0 && (roots || count == 0), DBFS_EINVAL, "bad arguments");
         Graph &g = gg->g;
         DBFS_CUDA(cudaSetDevice(g.ctx->device));
-        run_bfs_batch(g, *opts, roots, count, levels_out, parents_out, stats);
+        run_bfs_batch(g, *opts, roots, count, levels_out, parents_out, local, stats);
     });
+}
+
+int32_t dbfs_bfs_batch_output_count(const dbfs_graph *gg, int32_t local, int64_t *count) {
+    return guard([&] { *count = batch_output_count(gg->g, local != 0); });
 }
 
 int32_t dbfs_fetch_result(dbfs_graph *gg, int32_t *levels_out, int64_t *parents_out) {

@@ -33,6 +33,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -61,24 +67,31 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBa
         if (arrived == nblocks - 1) {
             if (ts) ts[0] = globaltimer_ns();
             if (gbar) {
-                unsigned ggen = ld_acquire_sys_u32(&gbar->gen);
-                unsigned garr = atomicAdd_system(&gbar->count, 1u);
-                if (garr == nranks - 1) {
-                    atomicExch_system(&gbar->count, 0u);
-                    __threadfence_system();
-                    atomicAdd_system(&gbar->gen, 1u);
-                } else {
-                    unsigned long long t0 = globaltimer_ns();
-                    while (ld_acquire_sys_u32(&gbar->gen) == ggen) {
-                        if (ld_acquire_sys_u32(&gbar->abort)) break;
-                        if (globaltimer_ns() - t0 > 4000000000ull) {
-                            atomicExch_system(&gbar->abort, 1u);
+                // one 64-bit arrival counter in rank 0's memory, never reset: the
+                // k-th barrier completes when it reaches k * nranks, so a GPU
+                // needs one NVLink atomic and then polls (abort every 64 polls)
+                unsigned long long *gc = reinterpret_cast<unsigned long long *>(&gbar->count);
+                const unsigned long long old = atomicAdd_system(gc, 1ull);
+                const unsigned long long target = old - old % nranks + nranks;
+                unsigned long long t0 = 0;
+                unsigned polls = 0;
+                bool aborted = false;
+                while (ld_acquire_sys_u64(gc) < target) {
+                    if ((++polls & 63u) == 0) {
+                        if (ld_acquire_sys_u32(&gbar->abort)) {
+                            aborted = true;
                             break;
                         }
-                        __nanosleep(32);
+                        const unsigned long long t = globaltimer_ns();
+                        if (t0 == 0) t0 = t;
+                        else if (t - t0 > 4000000000ull) {
+                            atomicExch_system(&gbar->abort, 1u);
+                            aborted = true;
+                            break;
+                        }
                     }
                 }
-                if (ld_acquire_sys_u32(&gbar->abort)) atomicExch(&bar->abort, 1u);
+                if (aborted) atomicExch(&bar->abort, 1u);
             }
             if (ts) ts[1] = globaltimer_ns();
             if (cv) cv->ctl->cont = level_continue(*cv, cont_level) ? 1 : 0;
@@ -121,14 +134,18 @@ struct AsmArgs {
     int32_t *glevel;
     int64_t *gparent;
     int parents;
+    int64_t first, step, count;  // output i is vertex first + i*step (global: 0, 1, n; rank r's own: r, p, n_local)
 };
 
 // levels[v] for normals from worker v mod p, then delegates (engine.py:308-314).
+// Output i holds vertex first + i*step: the whole graph, or (distributed) the
+// vertices a rank owns, v mod p == rank -- a distributed Graph500 result.
 __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
-    for (int64_t v = tid; v < a.n; v += nth) {
+    for (int64_t o = tid; o < a.count; o += nth) {
+        const int64_t v = a.first + o * a.step;
         uint32_t di = a.del_id[v];
         if (di != 0xffffffffu) {
-            a.glevel[v] = a.dlevel[di];
+            a.glevel[o] = a.dlevel[di];
             if (a.parents) {
                 int64_t par = -1;
                 if (a.dlevel[di] >= 0) {
@@ -142,12 +159,12 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
                         par = a.dparent[di];
                     }
                 }
-                a.gparent[v] = par;
+                a.gparent[o] = par;
             }
         } else {
             uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
-            a.glevel[v] = a.nlevel[w][i];
-            if (a.parents) a.gparent[v] = a.nparent[w][i];
+            a.glevel[o] = a.nlevel[w][i];
+            if (a.parents) a.gparent[o] = a.nparent[w][i];
         }
     }
 }
@@ -483,6 +500,9 @@ static AsmArgs make_asm(Graph &g, bool parents) {
     a.glevel = g.glevel.p;
     a.gparent = g.gparent.p;
     a.parents = parents;
+    a.first = 0;
+    a.step = 1;
+    a.count = g.n;
     return a;
 }
 
@@ -1040,8 +1060,37 @@ static void ensure_copy_stream(Ctx &ctx) {
     }
 }
 
+// Assembly arguments of the outputs a batch copies: the whole graph, or in a
+// distributed graph with `local` the vertices this rank owns (v mod p == rank),
+// read from the peer-mapped (or NCCL min-reduced) delegate candidates.
+static AsmArgs batch_asm(Graph &g, bool parents, bool local) {
+    AsmArgs aa = make_asm(g, parents);
+    if (g.dist) {
+        if (g.peer_state == 1) {
+            for (int w = 0; w < g.p; w++) {
+                aa.nlevel[w] = g.peer_nlevel[w];
+                aa.nparent[w] = g.peer_nparent[w];
+                aa.dpar_src[w] = g.peer_dparent[w];
+            }
+            aa.n_dpar = g.p;
+        } else {
+            WorkerHost &Wk = g.workers[0];
+            aa.nlevel[Wk.w] = Wk.nlevel.p;
+            aa.nparent[Wk.w] = Wk.nparent.p;
+        }
+    }
+    if (local && g.dist) {
+        aa.first = g.ctx->rank;
+        aa.step = g.p;
+        aa.count = g.workers[0].n_local;
+    }
+    return aa;
+}
+
+int64_t batch_output_count(const Graph &g, bool local) { return (local && g.dist) ? g.workers[0].n_local : g.n; }
+
 void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, int64_t count, int32_t *const *levels,
-                   int64_t *const *parents, dbfs_run_stats *st) {
+                   int64_t *const *parents, int local, dbfs_run_stats *st) {
     Ctx &ctx = *g.ctx;
     DBFS_CHECK(o0.mode == 0 || o0.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
     for (int64_t k = 0; k < count; k++)
@@ -1050,53 +1099,75 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     if (count == 0) return;
     ensure_copy_stream(ctx);
     const bool want_par = parents != nullptr && o0.parent_mode != 0;
+    const int64_t nout = batch_output_count(g, local != 0);
     for (int b = 0; b < 2; b++) {
-        if (levels && g.stage_lv[b].n != g.n) g.stage_lv[b].alloc(g.n);
-        if (want_par && g.stage_pv[b].n != g.n) g.stage_pv[b].alloc(g.n);
+        if (levels && g.stage_lv[b].n < nout) g.stage_lv[b].alloc(std::max<int64_t>(nout, 1));
+        if (want_par && g.stage_pv[b].n < nout) g.stage_pv[b].alloc(std::max<int64_t>(nout, 1));
     }
-    auto stage_and_copy = [&](int64_t k, bool used_b) {
+    const int engine = configure_run(g, o0);
+    // root k's outputs -> staging buffer k%2 (kernels only on ctx.stream), then
+    // D2H on the copy stream; staging b is reused once its previous D2H is done
+    auto stage_and_copy = [&](int64_t k, const AsmArgs *asm_src) {
         const int b = (int)(k & 1);
-        if (used_b) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[b], 0));
+        if (k >= 2) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[b], 0));
         const int blocks = ctx.num_sms * 4;
-        if (levels && levels[k]) {
-            k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.levels_dev(), (uint8_t *)g.stage_lv[b].p,
-                                                         4 * g.n);
+        const bool lv = levels && levels[k], pa = want_par && parents[k];
+        if (asm_src) {
+            AsmArgs aa = *asm_src;
+            aa.glevel = g.stage_lv[b].p;
+            aa.gparent = pa ? g.stage_pv[b].p : nullptr;
+            aa.parents = pa;
+            k_assemble<<<blocks, BT, 0, ctx.stream>>>(aa);
             DBFS_LAUNCHED();
-        }
-        if (want_par && parents[k]) {
-            k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(), (uint8_t *)g.stage_pv[b].p,
-                                                         8 * g.n);
-            DBFS_LAUNCHED();
+        } else {
+            if (lv) {
+                k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.levels_dev(),
+                                                             (uint8_t *)g.stage_lv[b].p, 4 * nout);
+                DBFS_LAUNCHED();
+            }
+            if (pa) {
+                k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(),
+                                                             (uint8_t *)g.stage_pv[b].p, 8 * nout);
+                DBFS_LAUNCHED();
+            }
         }
         DBFS_CUDA(cudaEventRecord(ctx.ev_ready[b], ctx.stream));
         DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
-        if (levels && levels[k])
-            DBFS_CUDA(cudaMemcpyAsync(levels[k], g.stage_lv[b].p, 4 * g.n, cudaMemcpyDeviceToHost, ctx.copy_stream));
-        if (want_par && parents[k])
-            DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * g.n, cudaMemcpyDeviceToHost, ctx.copy_stream));
+        if (lv) DBFS_CUDA(cudaMemcpyAsync(levels[k], g.stage_lv[b].p, 4 * nout, cudaMemcpyDeviceToHost, ctx.copy_stream));
+        if (pa)
+            DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * nout, cudaMemcpyDeviceToHost, ctx.copy_stream));
         DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
-        if (st) st[k].d2h_bytes += (levels && levels[k] ? 4 * g.n : 0) + (want_par && parents[k] ? 8 * g.n : 0);
+        if (st) st[k].d2h_bytes += (lv ? 4 * nout : 0) + (pa ? 8 * nout : 0);
     };
-    const int engine = configure_run(g, o0);
-    if (engine != 2) {
-        // distributed / host-loop engines: run_bfs per root (its host round trips
-        // bound the overlap), copies still on the copy stream
+    if (engine == 1) {
+        // host-driven level loop: run_bfs per root (its host round trips bound
+        // the overlap); delegate parents min-reduced over ranks before assembly
         for (int64_t k = 0; k < count; k++) {
             dbfs_bfs_options o = o0;
             o.source = roots[k];
             run_bfs(g, o, st ? &st[k] : nullptr);
-            dist_assemble(g);
-            stage_and_copy(k, k >= 2);
+            if (g.dist) {
+                if (o0.parent_mode && g.d) nccl_allreduce_i64(ctx, g.workers[0].dparent.p, g.d, 1);
+                AsmArgs aa = batch_asm(g, o0.parent_mode != 0, local != 0);
+                stage_and_copy(k, &aa);
+                g.assembled = false;
+            } else {
+                stage_and_copy(k, nullptr);
+            }
         }
         DBFS_CUDA(cudaStreamSynchronize(ctx.copy_stream));
         DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
         return;
     }
-    // Single-process persistent engine: every root is enqueued without a host
-    // round trip -- prep kernel (control blocks, barrier), the traversal (the
-    // source's delegate id looked up on device), an info kernel (iterations,
-    // watchdog) and the staging copy; the D2H runs on the copy stream.
+    // Persistent engines (one GPU, or one per rank over peer memory): every
+    // root is enqueued without a host round trip -- prep kernel (control
+    // block, grid barrier), the traversal (the source's delegate id looked up
+    // on device), an info kernel (iterations, watchdog), the assembly / staging
+    // copy; the D2H runs on the copy stream.  Distributed ranks pass an NCCL
+    // all-reduce (a device-side barrier) before each traversal, so no rank
+    // overwrites its state while a peer still assembles from it.
     const int W = g.W;
+    const bool peer = engine == 3;
     set_smem_attrs();
     if (g.pgrid <= 0) {
         int bps = 0;
@@ -1105,21 +1176,25 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     int grid = g.pgrid;
     g.warps_per_worker = (double)grid / W * WPB;
     AsmArgs aa = make_asm(g, o0.parent_mode != 0);
-    int do_asm = g.p > 1 ? 1 : 0;
+    int do_asm = (!g.dist && g.p > 1) ? 1 : 0;
+    AsmArgs out_asm = batch_asm(g, o0.parent_mode != 0, local != 0);
+    void *flag = (char *)ctx.ensure_scratch(256) + 128;  // NCCL barrier word (the grid barrier is at offset 0)
     GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
     DArray<int2> info;
     info.alloc(count);
     std::vector<cudaEvent_t> evs(2 * count, nullptr);
     for (auto &e : evs) DBFS_CUDA(cudaEventCreate(&e));
+    if (peer) nccl_barrier(ctx);
     const int64_t launches0 = g_kernel_launches;
-    const View *vp = g.views.p;
+    const View *vp = peer ? g.peer_view.p : g.views.p;
     int rec_cap = g.rec_cap;
-    GridBar *gb = nullptr;
-    int nr = 1;
+    GridBar *gb = peer ? (GridBar *)g.gbar : nullptr;
+    int nr = peer ? g.p : 1;
     const uint32_t *dil = g.del_id.p;
     uint32_t sdel = SRC_DEL_LOOKUP;
     for (int64_t k = 0; k < count; k++) {
         int64_t src = roots[k];
+        if (peer && k > 0) nccl_allreduce_async(ctx, flag);
         k_batch_prep<<<W, 256, 0, ctx.stream>>>(g.views.p, bar);
         DBFS_LAUNCHED();
         DBFS_CUDA(cudaEventRecord(evs[2 * k], ctx.stream));
@@ -1132,8 +1207,9 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
         k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k);
         DBFS_LAUNCHED();
-        stage_and_copy(k, k >= 2);
+        stage_and_copy(k, g.dist ? &out_asm : nullptr);
     }
+    if (peer) nccl_allreduce_async(ctx, flag);  // peers may read this rank's arrays until every assembly is done
     DBFS_CUDA(cudaStreamSynchronize(ctx.copy_stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
     std::vector<int2> hi(count);
@@ -1152,13 +1228,14 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             r.reached = -1;
             r.device_ms = ms;
             r.kernel_launches = launches / count;
-            r.engine_used = 2;
+            r.engine_used = engine;
             r.per_iteration_truncated = 1;  // records are not collected in batch mode
             r.h2d_bytes = k == 0 ? (int64_t)(sizeof(View) * W) : 0;
             r.d2h_bytes = d2h + (int64_t)sizeof(int2);
         }
     }
     for (auto &e : evs) cudaEventDestroy(e);
+    if (aborted && peer) g.peer_state = -1;
     DBFS_CHECK(!aborted, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
     g.last_iterations = hi[count - 1].x;
     g.last_truncated = true;
@@ -1169,6 +1246,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     g.last_mode = o0.mode;
     g.last_la = o0.local_all2all;
     g.last_uq = o0.uniquify;
+    g.assembled = !g.dist;
 }
 
 // ------------------------------------------------ min-ID parents (A19) / A20

@@ -1128,27 +1128,39 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     // sources that found delegates this level (a clean source's mask is all
     // zero): the others' masks -- NVLink reads in the peer engine -- are skipped
     __shared__ unsigned long long s_src;
-    if (threadIdx.x == 0) {
-        unsigned long long m = 0;
+    if (threadIdx.x == 0) s_src = 0ull;
+    __syncthreads();
+    {
+        // one thread per source reads its dirty flag (NVLink loads in the peer engine run in parallel)
         const bool flags = V.peer || !V.dist;  // control blocks of every source are mapped
-        for (int s = 0; s < V.P_sources; s++)
-            if (!flags || __ldcg(&V.ctl_all[s]->s[L % 3].dirty)) m |= 1ull << s;
-        s_src = m;
+        const int s = threadIdx.x;
+        if (s < V.P_sources && (!flags || __ldcg(&V.ctl_all[s]->s[L % 3].dirty))) atomicOr(&s_src, 1ull << s);
     }
     __syncthreads();
     const unsigned long long src = s_src;
     const bool dyn = src != 0;  // delegates were found: new-delegate work to balance
+    // remote masks: 32-word chunks, so every lane has a word and its sources'
+    // loads are in flight together (8 per batch) -- NVLink latency, not bandwidth
+    const int cw = (V.peer && __popcll(src) > 1) ? 32 : DBFS_CWD;
     const LevelSlot &SL = V.ctl->s[L % 3];
     uint32_t *cnt_nd = SL.exec_dir[KIND_ND] == PUSHC ? V.first[KIND_ND] : nullptr;
     uint32_t *cnt_dd = SL.exec_dir[KIND_DD] == PUSHC ? V.first[KIND_DD] : nullptr;
-    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, DBFS_CWD, gw, TW); ch.valid(); ch.next()) {
+    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, cw, gw, TW); ch.valid(); ch.next()) {
         const int64_t base = ch.base();
         const int64_t wi = ch.word(V.nw_d);
         uint32_t nw = 0u;
         if (wi >= 0) {
             uint32_t r = 0;
-            for (int s = 0; s < V.P_sources; s++)
-                if ((src >> s) & 1) r |= __ldcg(&V.mask_src[L & 1][s][wi]);
+            for (int s0 = 0; s0 < V.P_sources; s0 += 8) {
+                uint32_t t[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    const int s = s0 + j;
+                    t[j] = (s < V.P_sources && ((src >> s) & 1)) ? __ldcg(&V.mask_src[L & 1][s][wi]) : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; j++) r |= t[j];
+            }
             uint32_t dv = V.dvis[wi];
             nw = r & ~dv;
             next_mask[wi] = 0u;
@@ -1453,11 +1465,21 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
 // delegates, or any record in flight (over all in-process workers).
 __device__ __forceinline__ bool level_continue(const View &V, int L) {
     if (V.ctl->s[L % 3].new_del) return true;
-    for (int i = 0; i < V.P_sources; i++) {
-        const Ctl *c = V.ctl_all[i];  // a peer GPU's block in the peer engine: read at L2
-        if (__ldcg(&c->s[(L + 1) % 3].nfront) || __ldcg(&c->s[L % 3].records)) return true;
+    // a peer GPU's block in the peer engine: the loads of 8 sources are in flight together
+    unsigned long long any = 0;
+    for (int i0 = 0; i0 < V.P_sources; i0 += 8) {
+        unsigned long long t[16];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int i = i0 + j;
+            const Ctl *c = V.ctl_all[i < V.P_sources ? i : 0];
+            t[2 * j] = i < V.P_sources ? __ldcg(&c->s[(L + 1) % 3].nfront) : 0ull;
+            t[2 * j + 1] = i < V.P_sources ? __ldcg(&c->s[L % 3].records) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) any |= t[j];
     }
-    return false;
+    return any != 0;
 }
 
 }  // namespace dbfs

@@ -83,6 +83,12 @@ void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, c
     DBFS_NCCL(ncclGroupEnd());
 }
 
+// Device-side barrier: an all-reduce of one word enqueued on the context
+// stream, no host wait (later work on the stream runs after every rank got here).
+void nccl_allreduce_async(Ctx &ctx, void *word) {
+    DBFS_NCCL(ncclAllReduce(word, word, 1, ncclInt32, ncclSum, comm_of(ctx), ctx.stream));
+}
+
 void nccl_barrier(Ctx &ctx) {
     void *p = ctx.ensure_scratch(64);
     DBFS_NCCL(ncclAllReduce(p, p, 1, ncclInt32, ncclSum, comm_of(ctx), ctx.stream));

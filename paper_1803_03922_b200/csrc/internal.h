@@ -301,7 +301,8 @@ void rmat_generate_host(Ctx &ctx, const dbfs_rmat_params &prm, int64_t begin, in
 void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st);
 void fetch_result(Graph &g, int32_t *levels, int64_t *parents);
 void run_bfs_batch(Graph &g, const dbfs_bfs_options &o, const int64_t *roots, int64_t count, int32_t *const *levels,
-                   int64_t *const *parents, dbfs_run_stats *st);
+                   int64_t *const *parents, int local, dbfs_run_stats *st);
+int64_t batch_output_count(const Graph &g, bool local);
 void min_parents(Graph &g, int64_t *out);
 int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents);
 
@@ -316,6 +317,7 @@ void nccl_allgather_bytes(Ctx &ctx, const void *send, void *recv, int64_t bytes)
 void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, const int64_t *send_bytes,
                           void *recv, const int64_t *recv_off, const int64_t *recv_bytes);
 void nccl_barrier(Ctx &ctx);
+void nccl_allreduce_async(Ctx &ctx, void *word);
 void nccl_allreduce_u8_max(Ctx &ctx, uint8_t *dbuf, int64_t count);
 
 // io.cu (host only)

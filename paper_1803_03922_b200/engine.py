@@ -253,37 +253,49 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
 
 
 def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
-              stats: bool = False):
+              stats: bool = False, local: bool = False):
     """Graph500's multi-root loop in one call (``dbfs_bfs_batch``): returns one
     (depth, parent) pair per root.  The device-to-host copy of root k runs on a
     separate stream while root k+1 traverses, so PCIe time hides behind the
-    BFS.  ``outs`` is a list of (levels int32[n], parents int64[n]) host arrays
-    (pinned for the overlap, see ``_lib.pinned_empty``); entries may repeat,
-    e.g. two buffer pairs used alternately, in which case each root's result is
-    in its pair until root k+2 overwrites it.  ``stats=True`` also returns the
-    per-root C run-stats structs."""
+    BFS.  ``outs`` is a list of (levels int32, parents int64) host arrays of
+    ``batch_output_count(pg, local)`` entries (pinned for the overlap, see
+    ``_lib.pinned_empty``); entries may repeat, e.g. two buffer pairs used
+    alternately, in which case each root's result is in its pair until root
+    k+2 overwrites it.  ``local=True`` in a distributed run gives each rank
+    only the vertices it owns (entry i = vertex rank + i*world), the
+    distributed Graph500 result.  Per-iteration records are not kept.
+    ``stats=True`` also returns the per-root C run-stats structs."""
     roots = np.ascontiguousarray([int(r) for r in roots], dtype=np.int64)
     for r in roots:
         if not (0 <= r < pg.n):
             raise ValueError(f"source {r} out of range [0, {pg.n})")
     count = len(roots)
+    nout = batch_output_count(pg, local)
     if outs is None:
-        outs = [(np.empty(pg.n, dtype=np.int32), np.empty(pg.n, dtype=np.int64) if parents else None)
+        outs = [(np.empty(nout, dtype=np.int32), np.empty(nout, dtype=np.int64) if parents else None)
                 for _ in range(count)]
     if len(outs) != count:
         raise ValueError("outs must hold one (levels, parents) pair per root")
     for lv, pa in outs:
-        if lv is not None and (lv.dtype != np.int32 or lv.size < pg.n or not lv.flags.c_contiguous):
-            raise ValueError("levels buffers must be contiguous int32[n]")
-        if pa is not None and (pa.dtype != np.int64 or pa.size < pg.n or not pa.flags.c_contiguous):
-            raise ValueError("parents buffers must be contiguous int64[n]")
+        if lv is not None and (lv.dtype != np.int32 or lv.size < nout or not lv.flags.c_contiguous):
+            raise ValueError(f"levels buffers must be contiguous int32[{nout}]")
+        if pa is not None and (pa.dtype != np.int64 or pa.size < nout or not pa.flags.c_contiguous):
+            raise ValueError(f"parents buffers must be contiguous int64[{nout}]")
     lv_ptrs = (_lib.vp * max(count, 1))(*[lv.ctypes.data if lv is not None else None for lv, _ in outs])
     pa_ptrs = (_lib.vp * max(count, 1))(*[pa.ctypes.data if pa is not None else None for _, pa in outs])
     st = (_lib.RunStatsC * max(count, 1))()
     opts = BfsOptions(mode=mode, source=int(roots[0]) if count else 0, parents=parents).to_c()
     _lib.check(_lib.load().dbfs_bfs_batch(pg.handle, ctypes.byref(opts), roots.ctypes.data_as(_lib.vp), count,
-                                          lv_ptrs, pa_ptrs if parents else None, st), "bfs_batch")
+                                          lv_ptrs, pa_ptrs if parents else None, int(bool(local)), st), "bfs_batch")
     return (outs, list(st)[:count]) if stats else outs
+
+
+def batch_output_count(pg: PartitionedGraph, local: bool = False) -> int:
+    """Entries per output array of ``bfs_batch``: n, or this rank's own vertex
+    count when ``local`` in a distributed run."""
+    c = ctypes.c_int64()
+    _lib.check(_lib.load().dbfs_bfs_batch_output_count(pg.handle, int(bool(local)), ctypes.byref(c)))
+    return int(c.value)
 
 
 def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any",

@@ -32,14 +32,14 @@ roots = [1, 77, 4242 % (1 << scale), 9999 % (1 << scale)]
 engines = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] != "-" else ["host", "peer"]
 res = []
 local_ok = True
-for engine in engines:
-    for mode in ("dobfs", "bfs"):
+for engine, policy in [(e, "cost") for e in engines] + [(e, "push") for e in engines]:
+    for mode in ("dobfs", "bfs") if policy == "cost" else ("dobfs",):
         for r in roots:
             lv = np.empty(pg.n, dtype=np.int32)
             pa = np.empty(pg.n, dtype=np.int64)
-            st = _bfs_raw(pg, BfsOptions(mode=mode, source=r, engine=engine), lv, pa)
+            st = _bfs_raw(pg, BfsOptions(mode=mode, source=r, engine=engine, exec_policy=policy), lv, pa)
             bad = api.validate_bfs_tree(pg, r)
-            res.append((engine, st.engine_used, mode, r, levels_digest(lv), st.iterations,
+            res.append((f"{engine}/{policy}", st.engine_used, mode, r, levels_digest(lv), st.iterations,
                         [[int(st.inspections[k][0]), int(st.inspections[k][1])] for k in range(4)], bad, st.device_ms))
 # per-rank records (directions, FV, comm accounting incl. uniquify) must not depend on the engine
 for opts in (dict(), dict(uniquify=True), dict(uniquify=True, local_all2all=True)):
@@ -48,6 +48,24 @@ for opts in (dict(), dict(uniquify=True), dict(uniquify=True, local_all2all=True
         if any(x[key] != runs[0][key] for x in runs[1:]):
             local_ok = False
             print(f"rank {rank}: engines disagree on {key} with {opts}", flush=True)
+# bfs_batch: pipelined roots, full outputs and each rank's own vertices (local)
+from paper_1803_03922_b200.engine import bfs_batch
+for local in (False, True):
+    outs = bfs_batch(pg, roots, local=local)
+    for r, (blv, bpa) in zip(roots, outs):
+        lv = np.empty(pg.n, dtype=np.int32)
+        _bfs_raw(pg, BfsOptions(source=r), lv, None)
+        want = lv[rank::world] if local else lv
+        if not np.array_equal(blv, want):
+            local_ok = False
+            print(f"rank {rank}: bfs_batch(local={local}) levels differ for root {r}", flush=True)
+        reached = blv >= 0
+        vids = (np.arange(len(blv)) * world + rank) if local else np.arange(len(blv))
+        par = bpa[reached]
+        okp = np.where(vids[reached] == r, par == r, lv[np.clip(par, 0, pg.n - 1)] == blv[reached] - 1)
+        if not okp.all() or (bpa[~reached] != -1).any():
+            local_ok = False
+            print(f"rank {rank}: bfs_batch(local={local}) parents inconsistent for root {r}", flush=True)
 flags = [None] * world
 tdist.all_gather_object(flags, local_ok)
 ok = all(flags)
