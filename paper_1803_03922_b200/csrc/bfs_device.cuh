@@ -883,6 +883,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             C.cumq[L & 1][k] = cum[k];
             C.cumfv[L & 1][k] = cumfv[k];
             C.s[L % 3].exec_dir[k] = ex[k];
+            if (k == 0) C.s[L % 3].prev_dirty = L > 0 ? C.s[(L + 2) % 3].dirty : 0ull;
             if (k > 0 && ex[k] != BWD) C.s[L % 3].work[k] = S.fv[k];
             // counting push: the candidates' reverse-row lengths; F(L) takes off
             // what the early exits of the found ones skip
@@ -1143,6 +1144,9 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     // loads are in flight together (8 per batch) -- NVLink latency, not bandwidth
     const int cw = (V.peer && __popcll(src) > 1) ? 32 : DBFS_CWD;
     const LevelSlot &SL = V.ctl->s[L % 3];
+    // nothing found anywhere, no delegate frontier to clear, and this worker's
+    // mask of level L-1 (cleared here for level L+1) is already zero: no-op
+    if (src == 0 && SL.dfront == 0 && SL.prev_dirty == 0) return;
     uint32_t *cnt_nd = SL.exec_dir[KIND_ND] == PUSHC ? V.first[KIND_ND] : nullptr;
     uint32_t *cnt_dd = SL.exec_dir[KIND_DD] == PUSHC ? V.first[KIND_DD] : nullptr;
     for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[4] : nullptr, V.nw_d, cw, gw, TW); ch.valid(); ch.next()) {

@@ -29,6 +29,7 @@ struct LevelSlot {
     unsigned long long insp_bwd[4];  // backward inspections at this level
     unsigned long long records;      // remote normal records sent at this level
     unsigned long long dirty;        // this worker found >= 1 new delegate (comm.py:33-36)
+    unsigned long long prev_dirty;   // copy of level L-1's `dirty` (set at V(L)): dnext[(L+1)&1] may hold bits
     unsigned long long new_del;      // delegates discovered at the barrier
     unsigned long long inbox;        // records delivered to this worker
     unsigned long long pull_rows;    // reverse rows scanned by pulls at this level
