@@ -31,7 +31,8 @@ for r in roots[:nroots]:
         L.dbfs_bfs_iteration(pg.handle, it, ctypes.byref(rec), dirs.ctypes.data_as(_lib.vp), None)
         print(f"  L{it}: V {rec.visit_us:8.1f} us  F {rec.finish_us:7.1f} us  front n={rec.frontier_normals:9d} "
               f"d={rec.frontier_delegates:8d}  dirs {''.join('FB'[x] for x in dirs)}  "
-              f"exec {''.join('FBP'[x] for x in rec.exec_dirs)}  work {list(rec.work)}")
+              f"exec {''.join('FBP'[x] for x in rec.exec_dirs)}  work {list(rec.work)}  "
+              f"sync {[round(x, 1) for x in rec.sync_us]}")
         names = ["T1n", "T2dn", "T2dd", "T4dn", "T5nd", "T6dd", "F1d", "F3n"]
         print("       tasks avg/max us: " + "  ".join(f"{nm} {rec.task_avg_us[i]:.0f}/{rec.task_max_us[i]:.0f}"
                                                    for i, nm in enumerate(names) if rec.task_max_us[i] > 1))
