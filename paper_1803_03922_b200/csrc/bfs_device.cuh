@@ -18,8 +18,9 @@
 //   visited(<= L) normal   = nvis   (claims go to nfront[(L+1)&1], folded in F)
 //   frontier L normal      = nfront[L&1]
 //   visited(<= L) delegate = dvis   (finds go to dnext[L&1], folded in F)
-// Discoveries are fire-and-forget (RED.OR on the next bitmap + plain stores of
-// level / parent; any concurrent writer's parent is a valid one), so no lane
+// Discoveries are fire-and-forget (RED.OR on the next bitmap + a plain store of
+// the parent; any concurrent writer's parent is a valid one; a normal's level is
+// written when F folds it into visited), so no lane
 // ever waits on an atomic's return value in the traversal loops.  Frontier
 // statistics for the direction rule are counted from the bitmaps in F.
 #pragma once
@@ -353,8 +354,7 @@ __device__ __forceinline__ void claim_on(uint32_t *__restrict__ nvis, uint32_t *
     if (check && (nvis[wd] & bit)) return;
     if (nx[wd] & bit) return;  // already claimed this level (possibly stale: then harmless)
     atomicOr(&nx[wd], bit);    // result unused -> RED.OR
-    nlevel[c] = L + 1;
-    if (parents) nparent[c] = parent;
+    if (parents) nparent[c] = parent;  // the level is written by F3 (word order, coalesced)
 }
 
 __device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool check) {
@@ -553,9 +553,8 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         atomicOr(&nxt[x >> 5], 1u << (x & 31));
         if (ACT == ACT_DELEG) {
             if (V.parents) V.dcand[x] = pp[u];
-        } else {
-            V.nlevel[x] = L + 1;
-            if (V.parents) V.nparent[x] = pp[u];
+        } else if (V.parents) {
+            V.nparent[x] = pp[u];
         }
     }
     if (ACT == ACT_NN && V.p > 1) {
@@ -990,10 +989,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](bool hit, uint32_t c, uint32_t x) {
                       warp_mark(V.nfront[(L + 1) & 1], hit, c);
-                      if (hit) {
-                          V.nlevel[c] = L + 1;
-                          if (V.parents) V.nparent[c] = __ldg(&V.del_gid[x]);
-                      }
+                      if (hit && V.parents) V.nparent[c] = __ldg(&V.del_gid[x]);
                   });
     }
     tt.stop(AT, 3);
@@ -1314,6 +1310,7 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
             unsigned i = g0 + lane;
             if (i < cnt) {
                 uint32_t c = list[i];
+                V.nlevel[c] = L + 1;  // every claim of level L+1 (push, pull, remote record) lands here
                 int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
                 if (cnt_dn) take_first(cnt_dn, c, (uint64_t)dnd, fc.skip[KIND_DN]);
                 fc.nfv_nd += (unsigned long long)dnd;
