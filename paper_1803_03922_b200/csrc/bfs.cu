@@ -299,7 +299,11 @@ static void ensure_resources(Graph &g) {
         s.alloc(g.p);
         r.alloc((int64_t)g.p * g.p);
         std::vector<int64_t> mine(g.p);
-        for (int o = 0; o < g.p; o++) mine[o] = g.workers[0].remote_cap[o];
+        // peer engine: senders reserve inbox slots in chunks (SEND_CHUNK per warp,
+        // bfs_device.cuh), so every non-empty segment gets one chunk per resident warp of slack
+        const int64_t slack = (int64_t)ctx.num_sms * 64 * SEND_CHUNK;
+        for (int o = 0; o < g.p; o++)
+            mine[o] = g.workers[0].remote_cap[o] + (o != ctx.rank && g.workers[0].remote_cap[o] > 0 ? slack : 0);
         DBFS_CUDA(cudaMemcpy(s.p, mine.data(), 8 * g.p, cudaMemcpyHostToDevice));
         nccl_allgather_bytes(ctx, s.p, r.p, 8 * g.p);
         std::vector<int64_t> all((size_t)g.p * g.p);

@@ -336,8 +336,17 @@ struct TaskTimer {
     }
 };
 
+// Peer engine: a warp reserves inbox slots per destination SEND_CHUNK at a time
+// (lane d holds its cursor for destination d), so the per-destination counter
+// sees one atomic per chunk instead of one per warp step; the unused tail of
+// each chunk is filled with sentinels at the end of V (receivers skip them).
+constexpr unsigned SEND_CHUNK = 256;
+constexpr uint32_t REC_SKIP = 0xffffffffu;
+static_assert(32 * UNR <= SEND_CHUNK, "a warp step must fit one fresh chunk");
+
 struct VisitCounters {
     unsigned long long fv_nn;       // FV_nn of this level's frontier (activity slot)
+    unsigned long long scur, send;  // peer engine: this warp's inbox chunk for destination lane_id()
     unsigned long long records;     // remote normal records (comm accounting)
     unsigned long long uq;          // records surviving uniquify
     unsigned long long insp_bwd[4];
@@ -469,6 +478,36 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
         for (int u = 0; u < UNR; u++) {
             b[u] = __ballot_sync(FULL, ship[u] && o[u] == dst);
             tot += __popc(b[u]);
+        }
+        if (V.peer && V.p <= 32) {
+            // records [0, rem) finish this warp's chunk, the rest open a new one
+            unsigned long long cur = __shfl_sync(FULL, vc.scur, dst), end = __shfl_sync(FULL, vc.send, dst);
+            const unsigned long long rem = end - cur;
+            unsigned long long nb = 0;
+            if (rem < tot) {
+                if (lane_id() == 0) nb = atomicAdd(&V.ctl->s[L % 3].sent[dst], (unsigned long long)SEND_CHUNK);
+                nb = __shfl_sync(FULL, nb, 0);
+            }
+            unsigned before = 0;
+#pragma unroll
+            for (int u = 0; u < UNR; u++) {
+                if (ship[u] && o[u] == dst) {
+                    const unsigned long long r = before + __popc(b[u] & lt);
+                    V.sendbin[dst][r < rem ? cur + r : nb + (r - rem)] = make_uint2(c[u], parent[u]);
+                }
+                before += __popc(b[u]);
+            }
+            if (rem < tot) {
+                cur = nb + (tot - rem);
+                end = nb + SEND_CHUNK;
+            } else {
+                cur += tot;
+            }
+            if (lane_id() == dst) {
+                vc.scur = cur;
+                vc.send = end;
+            }
+            continue;
         }
         unsigned long long base = 0;
         if (lane_id() == 0) base = atomicAdd(&V.ctl->s[L % 3].sent[dst], (unsigned long long)tot);
@@ -1037,6 +1076,12 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                   });
     }
     tt.stop(AT, 4);
+    if (V.peer && V.p <= 32) {  // sentinel-fill the unused tails of this warp's inbox chunks
+        for (int dst = 0; dst < V.p; dst++) {
+            const unsigned long long cur = __shfl_sync(FULL, vc.scur, dst), end = __shfl_sync(FULL, vc.send, dst);
+            for (unsigned long long i = cur + lane; i < end; i += 32) V.sendbin[dst][i] = make_uint2(REC_SKIP, 0u);
+        }
+    }
     // flush: one atomic per warp per counter
     LevelSlot &A = C.s[L % 3];
     unsigned long long v;
@@ -1251,6 +1296,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
             const int grp = V.local_all2all ? (s % V.p_rank) + V.p_rank * (V.w / V.p_rank) : s;
             for (int64_t i = tid; i < (int64_t)cnt; i += nth) {
                 uint2 rec = __ldcg(&seg[i]);
+                if (rec.x == REC_SKIP) continue;  // unused tail of a sender's chunk
                 if (V.uniquify) {
                     uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
                     if (!(old & (1u << (rec.x & 31)))) uq++;

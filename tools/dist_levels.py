@@ -18,6 +18,7 @@ nroots = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 engines = sys.argv[3].split(",") if len(sys.argv) > 3 else ["peer", "host"]
 er = "er" in sys.argv[4:]
 theta = int(sys.argv[5]) if len(sys.argv) > 5 else 16
+mode = sys.argv[6] if len(sys.argv) > 6 else "dobfs"
 world, rank, local = env_world()
 tdist.init_process_group("gloo", timeout=datetime.timedelta(minutes=10))
 ctx = _lib.Context(local)
@@ -35,7 +36,7 @@ for eng in engines:
     for r in roots:
         for _ in range(3):
             lv = np.empty(pg.n, dtype=np.int32)
-            st = _bfs_raw(pg, BfsOptions(source=int(r), engine=eng), lv, None)
+            st = _bfs_raw(pg, BfsOptions(source=int(r), engine=eng, mode=mode), lv, None)
         ms = [None] * world
         tdist.all_gather_object(ms, st.device_ms)
         lines = [f"[{eng}:{st.engine_used}] rank {rank} root {r}: device {st.device_ms:.3f} ms (max {max(ms):.3f}) "
