@@ -7,6 +7,7 @@
 //   host loop : one launch per phase with the NCCL exchange between V and F;
 //               used with one worker per process (torchrun, NCCL over NVLink).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -182,6 +183,12 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     const unsigned nblocks = gridDim.x;
     const bool timer = wb == 0 && threadIdx.x == 0;
     if (timer) V.ctl->t_start = globaltimer_ns();
+    // DBFS_TRACE diagnostics: every block's phase boundaries (block-uniform branch)
+    auto stamp = [&](int lv, int ph) {
+        if (!V.trace || lv >= 64) return;
+        __syncthreads();
+        if (threadIdx.x == 0) V.trace[((size_t)lv * 8 + ph) * gridDim.x + blockIdx.x] = globaltimer_ns();
+    };
     phase_init(V, wb, nb);
     if (!grid_sync(bar, nblocks, gbar, nranks)) return;
     if (wb == 0 && threadIdx.x == 0)  // SRC_DEL_LOOKUP: the host did not read del_id[source] (dbfs_bfs_batch)
@@ -193,14 +200,26 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
         if (L > 0) {
             // evaluated once by the barrier's last arriver (NVLink loads in the peer engine)
             const bool cont = __ldcg(&views[0].ctl->cont) != 0;
-            if (wb == 0 && threadIdx.x == 0 && L - 1 < rec_cap) make_record(V, *V.ctl, L - 1, V.rec[L - 1]);
-            if (!cont) break;
+            if (!cont) {
+                if (wb == 0 && threadIdx.x < 32 && L - 1 < rec_cap) make_record_warp(V, *V.ctl, L - 1, V.rec[L - 1]);
+                break;
+            }
         }
         if (timer && L < rec_cap) V.rec[L].t[0] = globaltimer_ns();
         unsigned long long *tb = L < rec_cap ? views[0].rec[L].tb : nullptr;
+        stamp(L, 0);
         phase_visit(V, L, wb, nb, sm);
+        // the record of level L-1 (its slot lives until F(L) ends) is made by the
+        // first of the worker's blocks to finish V(L): off the critical path
+        if (L > 0 && threadIdx.x < 32 && L - 1 < rec_cap) {
+            int mine = 0;
+            if (threadIdx.x == 0) mine = atomicCAS(&V.ctl->rec_level, L - 1, L) == L - 1;
+            if (__shfl_sync(0xffffffffu, mine, 0)) make_record_warp(V, *V.ctl, L - 1, V.rec[L - 1]);
+        }
+        stamp(L, 5);
         if (!grid_sync(bar, nblocks, gbar, nranks, nullptr, 0, tb)) return;
         if (timer && L < rec_cap) V.rec[L].t[1] = globaltimer_ns();
+        stamp(L, 6);
         if (V.peer) {  // peers' records are claimed before the frontier is folded
             phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_INGEST);
             if (!grid_sync(bar, nblocks)) return;
@@ -208,6 +227,7 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
         } else {
             phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
         }
+        stamp(L, 7);
         if (!grid_sync(bar, nblocks, gbar, nranks, &views[0], L, tb ? tb + 2 : nullptr)) return;
         if (timer && L < rec_cap) V.rec[L].t[2] = globaltimer_ns();
     }
@@ -801,6 +821,16 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     // kernel's first grid barrier spans all GPUs, so a rank whose host reached
     // the launch early would otherwise spend the others' host skew (python,
     // driver calls: up to ~1 ms) spinning inside its own event window.
+    const char *trace_path = engine >= 2 ? getenv("DBFS_TRACE") : nullptr;
+    if (trace_path) {
+        const int64_t tn = 64 * 8 * (int64_t)std::max(g.pgrid, 1);
+        if (g.trace.n != tn) g.trace.alloc(tn);
+        DBFS_CUDA(cudaMemset(g.trace.p, 0, g.trace.bytes()));
+        for (auto &V : g.views_h) V.trace = g.trace.p;
+        g.peer_view_h.trace = g.trace.p;
+        DBFS_CUDA(cudaMemcpy(g.views.p, g.views_h.data(), sizeof(View) * W, cudaMemcpyHostToDevice));
+        if (engine == 3) DBFS_CUDA(cudaMemcpy(g.peer_view.p, &g.peer_view_h, sizeof(View), cudaMemcpyHostToDevice));
+    }
     if (g.dist) nccl_barrier(ctx);
     DBFS_CUDA(cudaEventRecord(ctx.ev0, ctx.stream));
     if (engine >= 2) {
@@ -826,6 +856,23 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         Ctl c0;
         DBFS_CUDA(cudaMemcpy(&c0, g.workers[0].ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
         iterations = c0.last_level;
+        if (trace_path) {
+            std::vector<unsigned long long> tr(g.trace.n);
+            DBFS_CUDA(cudaMemcpy(tr.data(), g.trace.p, g.trace.bytes(), cudaMemcpyDeviceToHost));
+            if (FILE *f = fopen(trace_path, "a")) {
+                const int nbk = g.pgrid;
+                for (int lv = 0; lv < std::min(iterations, 64); lv++)
+                    for (int ph = 0; ph < 8; ph++)
+                        for (int b = 0; b < nbk; b++) {
+                            const unsigned long long t = tr[((size_t)lv * 8 + ph) * nbk + b];
+                            if (t) fprintf(f, "%d %lld %d %d %d %.3f\n", ctx.rank, (long long)o.source, lv, ph, b,
+                                           (double)(t - c0.t_start) / 1e3);
+                        }
+                fclose(f);
+            }
+            for (auto &V : g.views_h) V.trace = nullptr;
+            g.peer_view_h.trace = nullptr;
+        }
         if (engine == 3) {
             g.assembled = false;  // outputs stay distributed until fetched (dist_assemble)
             if (timeout) g.peer_state = -1;  // barrier state unknown: later runs use the NCCL level loop

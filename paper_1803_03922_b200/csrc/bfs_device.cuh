@@ -227,16 +227,15 @@ __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, con
 }
 
 // Per-iteration record of level L (engine.py:291-302, one worker).
-__host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, IterRec &r) {
+// Scalar fields of the record (everything but the per-task timers and the
+// per-destination message flags).
+__host__ __device__ inline void make_record_core(const View &V, const Ctl &c, int L, IterRec &r) {
     const LevelSlot &S = c.s[L % 3];
-    unsigned long long cum[4];
-    int dirs[4];
-    double bv[4];
-    // directions were published at V(L); recompute bv from the same inputs
-    level_dirs(V, c, L, dirs, bv, cum);
+    // directions and BV were published at V(L) (c.dir by parity, S.bv); nothing
+    // here reads state of level L+1, so any block may make it during V(L+1)
     for (int k = 0; k < 4; k++) {
         r.dir[k] = k == KIND_NN ? FWD : c.dir[L & 1][k];
-        r.bv[k] = bv[k];
+        r.bv[k] = S.bv[k];
         r.fv[k] = S.fv[k];
         r.insp[k] = r.dir[k] == FWD ? S.fv[k] : S.insp_bwd[k];
     }
@@ -246,10 +245,6 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         r.work[k] = S.work[k];
         r.exec_dir[k] = S.exec_dir[k];
     }
-    for (int k = 0; k < 8; k++) {
-        r.tsum[k] = S.tsum[k];
-        r.tmax[k] = S.tmax[k];
-    }
     r.nfront = S.nfront;
     r.dfront = S.dfront;
     r.rows = S.pull_rows;
@@ -257,6 +252,15 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
         if (k == KIND_NN || S.exec_dir[k] != BWD) r.rows += S.q[k];
     r.dirty = S.dirty;
     r.new_del = S.new_del;
+}
+
+__host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, IterRec &r) {
+    const LevelSlot &S = c.s[L % 3];
+    make_record_core(V, c, L, r);
+    for (int k = 0; k < 8; k++) {
+        r.tsum[k] = S.tsum[k];
+        r.tmax[k] = S.tmax[k];
+    }
     unsigned long long msgs = 0;
     for (int o = 0; o < MAXW; o++) {
         r.send[o] = S.send[o];
@@ -902,7 +906,65 @@ __device__ __forceinline__ bool dyn_pull(const View &V, const unsigned long long
     return U > 32ull * (unsigned long long)TW;
 }
 
+// The record of level L made by one whole warp (the message flags and timers
+// copied lane-parallel, the scalar fields by lane 0).
+__device__ __forceinline__ void make_record_warp(const View &V, const Ctl &c, int L, IterRec &r) {
+    const LevelSlot &S = c.s[L % 3];
+    const unsigned lane = lane_id();
+    unsigned long long msgs = 0;
+    for (int o = lane; o < MAXW; o += 32) {
+        const unsigned long long x = S.send[o];
+        r.send[o] = x;
+        msgs += x > 0;
+    }
+    msgs = warp_sum(msgs);
+    if (lane < 8) {
+        r.tsum[lane] = S.tsum[lane];
+        r.tmax[lane] = S.tmax[lane];
+    }
+    if (lane == 0) {
+        make_record_core(V, c, L, r);
+        r.messages = msgs;
+    }
+}
+
+// Block-level counter aggregation: warps add into shared memory, then one
+// global atomic per counter per block (instead of one per warp: thousands of
+// same-address atomics per counter and phase otherwise).
+constexpr int NACC = 16;
+__device__ __forceinline__ unsigned long long *block_acc() {
+    __shared__ unsigned long long s_acc[NACC];
+    return s_acc;
+}
+__device__ __forceinline__ void block_acc_clear() {
+    if (threadIdx.x < NACC) block_acc()[threadIdx.x] = 0ull;
+}
+__device__ __forceinline__ void warp_acc(int i, unsigned long long x) {
+    const unsigned long long v = warp_sum(x);
+    if (lane_id() == 0 && v) atomicAdd(&block_acc()[i], v);
+}
+// After a __syncthreads: thread i < n adds slot i to dst[i] (nullptr: skip).
+__device__ __forceinline__ void block_acc_flush(unsigned long long *const *dst, int n) {
+    if ((int)threadIdx.x < n && dst[threadIdx.x]) {
+        const unsigned long long v = block_acc()[threadIdx.x];
+        if (v) atomicAdd(dst[threadIdx.x], v);
+    }
+}
+
 // -------------------------------------------------------------- phase V(L)
+
+// DBFS_TRACE diagnostics: block-level timestamp of phase boundary `ph` of level
+// L -- 0 V start, 1 T1 start, 2 T1 end, 3 pulls start, 4 V work end, 5 V done,
+// 6 F start, 7 F done (block-uniform; adds a __syncthreads only when tracing).
+__device__ __forceinline__ void trace_stamp(const View &V, int L, int ph) {
+    if (!V.trace || L >= 64) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        V.trace[((size_t)L * 8 + ph) * gridDim.x + blockIdx.x] = t;
+    }
+}
 
 __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     Ctl &C = *V.ctl;
@@ -921,6 +983,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             C.cumq[L & 1][k] = cum[k];
             C.cumfv[L & 1][k] = cumfv[k];
             C.s[L % 3].exec_dir[k] = ex[k];
+            C.s[L % 3].bv[k] = bv[k];
             if (k == 0) C.s[L % 3].prev_dirty = L > 0 ? C.s[(L + 2) % 3].dirty : 0ull;
             if (k > 0 && ex[k] != BWD) C.s[L % 3].work[k] = S.fv[k];
             // counting push: the candidates' reverse-row lengths; F(L) takes off
@@ -929,6 +992,8 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         }
     }
     VisitCounters vc = {};
+    block_acc_clear();
+    __syncthreads();
     const unsigned lane = lane_id(), warp = warp_id();
     const int64_t gw = (int64_t)wb * WPB + warp, TW = (int64_t)nb * WPB;
     uint32_t *list = sm.list[warp];
@@ -941,6 +1006,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
 
     LevelSlot &AT = C.s[L % 3];
     TaskTimer tt;
+    trace_stamp(V, L, 1);
     // T1: normal frontier -- nn push (always, engine.py:207-222) + nd push.
     tt.start();
     if (S.nfront > 0) {
@@ -977,6 +1043,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     }
 
     tt.stop(AT, 0);
+    trace_stamp(V, L, 2);
     // T2: delegate frontier -- dn / dd push, load balanced over the level's
     // edge space (engine.py:238-263).
     tt.start();
@@ -1005,6 +1072,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     }
     tt.stop(AT, 2);
 
+    trace_stamp(V, L, 3);
     // Pull frontiers that are sparse relative to the 2^18-bit coarse filter
     // are tested in shared memory first (block-uniform decisions).
     const bool dpull = ex[KIND_DN] == BWD || ex[KIND_DD] == BWD;
@@ -1076,37 +1144,35 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                   });
     }
     tt.stop(AT, 4);
+    trace_stamp(V, L, 4);
     if (V.peer && V.p <= 32) {  // sentinel-fill the unused tails of this warp's inbox chunks
         for (int dst = 0; dst < V.p; dst++) {
             const unsigned long long cur = __shfl_sync(FULL, vc.scur, dst), end = __shfl_sync(FULL, vc.send, dst);
             for (unsigned long long i = cur + lane; i < end; i += 32) V.sendbin[dst][i] = make_uint2(REC_SKIP, 0u);
         }
     }
-    // flush: one atomic per warp per counter
+    // flush: warps into shared slots, one global atomic per counter per block
     LevelSlot &A = C.s[L % 3];
-    unsigned long long v;
-    v = warp_sum(vc.fv_nn);
-    if (lane == 0 && v) {
-        atomicAdd(&A.fv[KIND_NN], v);
-        atomicAdd(&A.work[KIND_NN], v);
+    warp_acc(0, vc.fv_nn);
+    warp_acc(1, vc.records);
+    warp_acc(2, vc.uq);
+    warp_acc(3, vc.dirty);
+    warp_acc(4, vc.pull_rows);
+    for (int k = 1; k < 4; k++) warp_acc(4 + k, vc.insp_bwd[k]);
+    __syncthreads();
+    {
+        unsigned long long *dst[11] = {&A.fv[KIND_NN], &A.records, &A.uq_records, nullptr, &A.pull_rows,
+                                       dirs[KIND_ND] == BWD ? &A.insp_bwd[KIND_ND] : nullptr,
+                                       dirs[KIND_DN] == BWD ? &A.insp_bwd[KIND_DN] : nullptr,
+                                       dirs[KIND_DD] == BWD ? &A.insp_bwd[KIND_DD] : nullptr,
+                                       &A.work[KIND_ND], &A.work[KIND_DN], &A.work[KIND_DD]};
+        if (threadIdx.x >= 8 && threadIdx.x < 11) block_acc()[threadIdx.x] = block_acc()[threadIdx.x - 3];
+        // work[k] of an executed pull = its inspections (slots 5..7 mirrored to 8..10)
+        block_acc_flush(dst, 11);
+        if (threadIdx.x == 11 && block_acc()[0]) atomicAdd(&A.work[KIND_NN], block_acc()[0]);
+        if (threadIdx.x == 12 && block_acc()[3]) atomicOr(&A.dirty, 1ull);
     }
-    v = warp_sum(vc.records);
-    if (lane == 0) atomic_add_u64(&A.records, v);
-    v = warp_sum(vc.uq);
-    if (lane == 0) atomic_add_u64(&A.uq_records, v);
-    for (int k = 1; k < 4; k++) {
-        v = warp_sum(vc.insp_bwd[k]);
-        if (lane == 0 && v) {
-            if (dirs[k] == BWD) atomicAdd(&A.insp_bwd[k], v);
-            atomicAdd(&A.work[k], v);
-        }
-    }
-    v = warp_sum(vc.dirty);
-    if (lane == 0 && v) atomicOr(&A.dirty, 1ull);
-    v = warp_sum(vc.pull_rows);
-    if (lane == 0) atomic_add_u64(&A.pull_rows, v);
     if (V.p > 1) {
-        __syncthreads();
         const unsigned long long dm = *block_sendmask();
         for (int i = threadIdx.x; i < V.p; i += BT)
             if ((dm >> i) & 1) atomicOr(&A.send[i], 1ull);
@@ -1372,36 +1438,28 @@ __device__ void flush_finish(const View &V, int L, FinishCounters &fc, int wb, b
     Ctl &C = *V.ctl;
     LevelSlot &A = C.s[L % 3];
     LevelSlot &N = C.s[(L + 1) % 3];
-    const unsigned lane = lane_id();
-    unsigned long long v;
-    v = warp_sum(fc.nfv_nd);
-    if (lane == 0) atomic_add_u64(&N.fv[KIND_ND], v);
-    v = warp_sum(fc.nq_nd);
-    if (lane == 0) atomic_add_u64(&N.q[KIND_ND], v);
-    v = warp_sum(fc.ncount);
-    if (lane == 0) atomic_add_u64(&N.nfront, v);
-    v = warp_sum(fc.dfv_dn);
-    if (lane == 0) atomic_add_u64(&N.fv[KIND_DN], v);
-    v = warp_sum(fc.dq_dn);
-    if (lane == 0) atomic_add_u64(&N.q[KIND_DN], v);
-    v = warp_sum(fc.dfv_dd);
-    if (lane == 0) atomic_add_u64(&N.fv[KIND_DD], v);
-    v = warp_sum(fc.dq_dd);
-    if (lane == 0) atomic_add_u64(&N.q[KIND_DD], v);
-    v = warp_sum(fc.new_del);
-    if (lane == 0) {
-        atomic_add_u64(&N.dfront, v);
-        atomic_add_u64(&A.new_del, v);
+    warp_acc(0, fc.nfv_nd);
+    warp_acc(1, fc.nq_nd);
+    warp_acc(2, fc.ncount);
+    warp_acc(3, fc.dfv_dn);
+    warp_acc(4, fc.dq_dn);
+    warp_acc(5, fc.dfv_dd);
+    warp_acc(6, fc.dq_dd);
+    warp_acc(7, fc.new_del);
+    for (int k = 1; k < 4; k++) warp_acc(8 + k, fc.skip[k]);
+    __syncthreads();
+    {
+        unsigned long long *dst[9] = {&N.fv[KIND_ND], &N.q[KIND_ND], &N.nfront, &N.fv[KIND_DN], &N.q[KIND_DN],
+                                      &N.fv[KIND_DD], &N.q[KIND_DD], &N.dfront, &A.new_del};
+        if (threadIdx.x == 8) block_acc()[8] = block_acc()[7];  // new delegates: next frontier and this level
+        block_acc_flush(dst, 9);
+        const int k = (int)threadIdx.x - 8;  // counting pushes: V(L) added the full row lengths
+        if (k >= 1 && k < 4 && block_acc()[8 + k]) atomicAdd(&A.insp_bwd[k], 0ull - block_acc()[8 + k]);
     }
-    for (int k = 1; k < 4; k++) {
-        v = warp_sum(fc.skip[k]);
-        if (lane == 0 && v) atomicAdd(&A.insp_bwd[k], 0ull - v);  // V(L) added the full row lengths
-    }
-    if (zero_slot && wb == 0 && threadIdx.x == 0) {
+    if (zero_slot && wb == 0) {
         // slot (L+2)%3 is idle during level L: clear it for level L+2
-        LevelSlot &Z = C.s[(L + 2) % 3];
-        unsigned long long *z = (unsigned long long *)&Z;
-        for (size_t i = 0; i < sizeof(LevelSlot) / 8; i++) z[i] = 0ull;
+        unsigned long long *z = (unsigned long long *)&C.s[(L + 2) % 3];
+        for (size_t i = threadIdx.x; i < sizeof(LevelSlot) / 8; i += BT) z[i] = 0ull;
     }
 }
 
@@ -1409,6 +1467,8 @@ enum { F_DELEGATES = 1, F_INGEST = 2, F_NORMALS = 4 };
 
 __device__ void phase_finish(const View &V, int L, int wb, int nb, Smem &sm, int parts) {
     FinishCounters fc = {};
+    block_acc_clear();
+    __syncthreads();
     const int64_t gw = (int64_t)wb * WPB + warp_id(), TW = (int64_t)nb * WPB;
     const int64_t tid = (int64_t)wb * BT + threadIdx.x, nth = (int64_t)nb * BT;
     uint32_t *list = sm.list[warp_id()];

@@ -36,6 +36,7 @@ struct LevelSlot {
     unsigned long long uq_records;   // records left after per-group uniquify (comm.py:122-127)
     unsigned long long work[4];      // inspections actually executed (push: FV, pull: scanned)
     int exec_dir[4];                 // executed strategy per kind (may differ from the reported one)
+    double bv[4];                    // BV per kind as the direction rule saw it (for the record)
     unsigned long long tsum[8];      // per-task warp cycles: sum over warps (T1,T2dn,T2dd,T4,T5,T6,F1,F3)
     unsigned long long tmax[8];      // per-task warp cycles: max over warps
     unsigned int sched[8];           // dynamic chunk counters: T1, T4, T6, T5, F1, F3
@@ -53,7 +54,7 @@ struct Ctl {
     int last_level;                  // iterations when the loop ended
     unsigned long long t_start, t_seeded;  // globaltimer: kernel start, after init+seed
     int cont;                        // persistent engine: termination rule of the last level (1 = go on)
-    int pad;
+    int rec_level;                   // persistent engine: last level whose record a block claimed (CAS)
 };
 
 // Per worker per level record (BfsRun.per_iteration before summing workers).
@@ -131,6 +132,7 @@ struct View {
     const uint32_t *mask_src[2][MAXW];
     const int64_t *cand_src[MAXW];
     IterRec *rec;
+    unsigned long long *trace;       // DBFS_TRACE: per level x {V start, V done, F start, F done} x block globaltimer
     int32_t *glevel;                 // global outputs when p == 1 (alias nlevel)
     int64_t *gparent;
 };
@@ -279,6 +281,7 @@ struct Graph {
     std::vector<int64_t *> peer_nparent, peer_dparent;
     DArray<int32_t> asm_lv, asm_mylv;    // NCCL assembly buffers (kept between runs)
     DArray<int64_t> asm_pv, asm_mypv;
+    DArray<unsigned long long> trace;  // DBFS_TRACE=<file>: block phase timestamps (diagnostics)
     DArray<int32_t> stage_lv[2];     // dbfs_bfs_batch: result staging, double-buffered
     DArray<int64_t> stage_pv[2];
     ~Graph();
