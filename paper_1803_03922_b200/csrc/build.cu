@@ -271,7 +271,7 @@ __global__ void k_route(EdgeSrc es, int64_t begin, int64_t end, const uint32_t *
     __shared__ unsigned long long s_kind[4];
     if (threadIdx.x < 4) s_kind[threadIdx.x] = 0;
     __syncthreads();
-    const int p = rp->p, first = rp->first, W = rp->W;
+    const int first = rp->first, W = rp->W;
     const PDiv pd = rp->pd;
     for (int64_t e = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < end;
          e += (int64_t)gridDim.x * blockDim.x) {

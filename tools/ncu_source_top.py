@@ -1,41 +1,35 @@
-"""Top source lines by warp-stall samples from an ncu report (--page source)."""
-import csv, io, subprocess, sys
+"""Top CUDA source lines by warp-stall samples (ncu --page source --print-source cuda,sass)."""
+import collections, csv, subprocess, sys
 
-rep = sys.argv[1]
-out = sys.argv[2] if len(sys.argv) > 2 else None
-top = int(sys.argv[3]) if len(sys.argv) > 3 else 45
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda"],
+rep, out = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else None)
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
-rows, fname = [], None
-lines = raw.splitlines()
-i = 0
-hdr = None
-for ln in lines:
-    if ln.startswith('"File Path"'):
-        fname = next(csv.reader([ln]))[1].split("/")[-1]
-        hdr = None
+agg, text = collections.Counter(), {}
+fname, hdr, cur_line = None, None, None
+for rec in csv.reader(raw.splitlines()):
+    if not rec:
         continue
-    if ln.startswith('"Function Name"'):
+    if rec[0] == "File Path":
+        fname, hdr = rec[1].split("/")[-1], None
         continue
-    rec = next(csv.reader([ln]))
-    if rec and rec[0] == "Line No":
+    if rec[0] == "Line No":
         hdr = rec
         continue
-    if hdr is None or len(rec) != len(hdr):
+    if hdr is None or rec[0] in ("Function Name", "Kernel Name"):
         continue
-    d = dict(zip(hdr, rec))
+    if rec[0]:
+        cur_line = (fname, rec[0])
+        text[cur_line] = rec[1].strip()
     try:
-        s = int(d.get("Warp Stall Sampling (All Samples)", "0").replace(",", "") or 0)
-    except ValueError:
-        continue
-    if s:
-        rows.append((s, fname, d["Line No"], d["Source"].strip()))
-tot = sum(r[0] for r in rows)
-rows.sort(reverse=True)
-txt = [f"total warp-stall samples {tot}"]
-for s, f, l, src in rows[:top]:
-    txt.append(f"{s:8d} {100*s/tot:5.1f}% {f}:{l}  {src[:110]}")
-res = "\n".join(txt)
+        agg[cur_line] += int(rec[hdr.index("Warp Stall Sampling (All Samples)")] or 0)
+    except (ValueError, IndexError):
+        pass
+tot = sum(agg.values())
+lines = [f"total warp-stall samples {tot}"]
+for (f, ln), c in agg.most_common(top):
+    lines.append(f"{c:7d} {100 * c / max(tot, 1):5.1f}% {f}:{ln}  {text.get((f, ln), '')[:110]}")
+res = "\n".join(lines)
 print(res)
 if out:
-    open(out, "w").write(f"ncu --set full --import-source on: {rep}\n" + res + "\n")
+    open(out, "w").write(res + "\n")
