@@ -317,6 +317,19 @@ def run_ours(args, world, rank, local_rank):
     line["config"]["labeling"] = ("reference hash_randomize_vertices + Feistel relabeling (balanced v mod p owners)"
                                   if scrambled else "reference hash_randomize_vertices")
     line["worker_edges_max_over_mean"] = imbalance
+    if dist:
+        # bytes this rank moved over NVLink per BFS (8-byte records incl. parent,
+        # d/8-byte delegate masks read from each peer on dirty levels), the max
+        # over ranks, against NVLink 5's 900 GB/s per direction and the step time
+        wire = float(np.mean([s.wire_bytes for s in stats]))
+        wire_max = float(_allreduce_max(ctx, np.array([wire]))[0])
+        t_step = total_dev_s / args.steps
+        line["comm"] = {"wire_bytes_per_bfs_max_rank": round(wire_max),
+                        "nvlink_time_us_at_900GBps": round(wire_max / 900e9 * 1e6, 2),
+                        "share_of_step": round(wire_max / 900e9 / t_step, 4),
+                        "achieved_GBps_over_step": round(wire_max / t_step / 1e9, 2),
+                        "note": "exchange is fused into the persistent kernel (posted NVLink stores, peer mask "
+                                "reads), so its time overlaps the traversal; per-level bytes: tools/dist_levels.py"}
     if rank == 0 and not args.no_cpu_baseline and not dist:
         line["cpu_baseline"] = cpu_baseline_same_graph(pg, roots, args, n, m)
     # reference-labeling series where its skewed owners fit (build peak ~24 B per

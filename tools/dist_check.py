@@ -66,6 +66,23 @@ for local in (False, True):
         if not okp.all() or (bpa[~reached] != -1).any():
             local_ok = False
             print(f"rank {rank}: bfs_batch(local={local}) parents inconsistent for root {r}", flush=True)
+# DPG1 round trip in a distributed context: every rank writes its worker file,
+# then rank r rebuilds worker r from worker_r alone (partition.py:392-464)
+import tempfile
+from paper_1803_03922_b200.partition import load_partitioned_graph, save_partitioned_graph
+box = [tempfile.mkdtemp(prefix="dpg_") if rank == 0 else None]
+tdist.broadcast_object_list(box, src=0)
+save_partitioned_graph(pg, box[0])
+tdist.barrier()
+back = load_partitioned_graph(box[0], symmetric=True, verify=True, ctx=ctx)
+for r in roots[:2]:
+    a = api.run_bfs(pg, BfsOptions(source=r)).to_dict()
+    b = api.run_bfs(back, BfsOptions(source=r)).to_dict()
+    for key in ("iterations", "per_iteration", "inspections", "comm", "levels_digest"):
+        if a[key] != b[key]:
+            local_ok = False
+            print(f"rank {rank}: DPG1 round trip differs on {key} for root {r}", flush=True)
+back.close()
 flags = [None] * world
 tdist.all_gather_object(flags, local_ok)
 ok = all(flags)
