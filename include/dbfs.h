@@ -199,10 +199,13 @@ int32_t dbfs_fetch_result(dbfs_graph *g, int32_t *levels_out, int64_t *parents_o
  * arrays of pointers and any entry may be NULL).  The D2H of root k runs on a copy
  * stream while root k+1 traverses.  local != 0 in a distributed context: each rank
  * receives only the vertices it owns (v mod p == rank, output i = vertex rank + i*p),
- * the distributed Graph500 result; otherwise every rank gets all n.  Per-iteration
- * records are not kept.  stats (nullable) receives count entries. */
+ * the distributed Graph500 result; otherwise every rank gets all n.  compact != 0:
+ * depth travels as int8 and parent as int32 (5 instead of 12 bytes per vertex over
+ * PCIe; n < 2^31) and the host widens them into the caller's arrays on every core
+ * while later roots run; a root with a depth >= 127 is re-run with full arrays.
+ * Per-iteration records are not kept.  stats (nullable) receives count entries. */
 int32_t dbfs_bfs_batch(dbfs_graph *g, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
-                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local,
+                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local, int32_t compact,
                        dbfs_run_stats *stats);
 /* Entries per output array of dbfs_bfs_batch (n, or this rank's own count when local). */
 int32_t dbfs_bfs_batch_output_count(const dbfs_graph *g, int32_t local, int64_t *count);

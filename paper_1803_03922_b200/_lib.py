@@ -99,7 +99,7 @@ SIGNATURES = {
     "dbfs_graph_export_classification": (i32, [vp, vp, vp]),
     "dbfs_bfs": (i32, [vp, P(BfsOptionsC), vp, vp, P(RunStatsC)]),
     "dbfs_fetch_result": (i32, [vp, vp, vp]),
-    "dbfs_bfs_batch": (i32, [vp, P(BfsOptionsC), vp, i64, vp, vp, i32, vp]),
+    "dbfs_bfs_batch": (i32, [vp, P(BfsOptionsC), vp, i64, vp, vp, i32, i32, vp]),
     "dbfs_bfs_batch_output_count": (i32, [vp, i32, P(i64)]),
     "dbfs_bfs_iteration": (i32, [vp, i64, P(IterationC), vp, vp]),
     "dbfs_min_parents": (i32, [vp, vp]),

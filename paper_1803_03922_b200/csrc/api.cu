@@ -119,6 +119,8 @@ int32_t dbfs_ctx_destroy(dbfs_ctx *ctx) {
             if (ctx->c.ev_ready[b]) cudaEventDestroy(ctx->c.ev_ready[b]);
             if (ctx->c.ev_done[b]) cudaEventDestroy(ctx->c.ev_done[b]);
         }
+        for (int h = 0; h < 3; h++)
+            if (ctx->c.ev_hdone[h]) cudaEventDestroy(ctx->c.ev_hdone[h]);
         if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
         if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
         delete ctx;
@@ -318,12 +320,13 @@ int32_t dbfs_bfs(dbfs_graph *gg, const dbfs_bfs_options *opts, int32_t *levels_o
 }
 
 int32_t dbfs_bfs_batch(dbfs_graph *gg, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
-                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local, dbfs_run_stats *stats) {
+                       int32_t *const *levels_out, int64_t *const *parents_out, int32_t local, int32_t compact,
+                       dbfs_run_stats *stats) {
     return guard([&] {
         DBFS_CHECK(opts && count >= 0 && (roots || count == 0), DBFS_EINVAL, "bad arguments");
         Graph &g = gg->g;
         DBFS_CUDA(cudaSetDevice(g.ctx->device));
-        run_bfs_batch(g, *opts, roots, count, levels_out, parents_out, local, stats);
+        run_bfs_batch(g, *opts, roots, count, levels_out, parents_out, local, compact, stats);
     });
 }
 

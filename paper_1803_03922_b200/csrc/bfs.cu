@@ -136,7 +136,18 @@ struct AsmArgs {
     int64_t *gparent;
     int parents;
     int64_t first, step, count;  // output i is vertex first + i*step (global: 0, 1, n; rank r's own: r, p, n_local)
+    int8_t *glevel8;             // compact transfer form (dbfs_bfs_batch): depth as int8, parent as int32
+    int32_t *gparent32;
+    unsigned *esc;               // depths >= 127 (escaped: the root is re-run with full arrays)
 };
+
+// Compact wire form of one depth / parent entry (sign extension restores -1 on
+// the host; parents are global ids < 2^31).
+__device__ __forceinline__ int8_t pack_level(int32_t l, unsigned *esc) {
+    if (l < 127) return (int8_t)l;
+    atomicAdd(esc, 1u);
+    return (int8_t)127;
+}
 
 // levels[v] for normals from worker v mod p, then delegates (engine.py:308-314).
 // Output i holds vertex first + i*step: the whole graph, or (distributed) the
@@ -145,6 +156,31 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
     for (int64_t o = tid; o < a.count; o += nth) {
         const int64_t v = a.first + o * a.step;
         uint32_t di = a.del_id[v];
+        if (a.glevel8) {  // compact form
+            int32_t l;
+            int64_t par = -1;
+            if (di != 0xffffffffu) {
+                l = a.dlevel[di];
+                if (a.parents && l >= 0) {
+                    if (a.n_dpar) {
+                        par = 0x7fffffffffffffffLL;
+                        for (int s = 0; s < a.n_dpar; s++) {
+                            const int64_t c = a.dpar_src[s][di];
+                            par = c < par ? c : par;
+                        }
+                    } else {
+                        par = a.dparent[di];
+                    }
+                }
+            } else {
+                uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
+                l = a.nlevel[w][i];
+                if (a.parents) par = a.nparent[w][i];
+            }
+            a.glevel8[o] = pack_level(l, a.esc);
+            if (a.parents) a.gparent32[o] = (int32_t)par;
+            continue;
+        }
         if (di != 0xffffffffu) {
             a.glevel[o] = a.dlevel[di];
             if (a.parents) {
@@ -248,8 +284,10 @@ __global__ void k_batch_prep(const View *__restrict__ views, GridBar *bar) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *bar = GridBar{0u, 0u, 0u, 0u};
 }
 
-__global__ void k_batch_info(const Ctl *__restrict__ ctl0, const GridBar *__restrict__ bar, int2 *info) {
+__global__ void k_batch_info(const Ctl *__restrict__ ctl0, const GridBar *__restrict__ bar, int2 *info,
+                             unsigned *esc) {
     *info = make_int2(ctl0->last_level, (int)bar->abort);
+    if (esc) *esc = 0u;  // escape counter of this root's compact outputs
 }
 
 __global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, int64_t bytes) {
@@ -259,6 +297,30 @@ __global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restric
     uint4 *d4 = reinterpret_cast<uint4 *>(dst);
     for (int64_t i = tid; i < n16; i += nth) d4[i] = __ldcs(&s4[i]);
     for (int64_t i = (n16 << 4) + tid; i < bytes; i += nth) dst[i] = src[i];
+}
+
+// Compact wire form of the whole-graph outputs (single process): 4 entries per thread.
+__global__ void k_pack_result(const int32_t *__restrict__ lv, const int64_t *__restrict__ pa, int64_t n,
+                              int8_t *__restrict__ lv8, int32_t *__restrict__ p32, unsigned *esc) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = tid; q < (n >> 2); q += nth) {
+        const int4 l = reinterpret_cast<const int4 *>(lv)[q];
+        char4 c;
+        c.x = pack_level(l.x, esc);
+        c.y = pack_level(l.y, esc);
+        c.z = pack_level(l.z, esc);
+        c.w = pack_level(l.w, esc);
+        reinterpret_cast<char4 *>(lv8)[q] = c;
+        if (pa) {
+            const longlong2 a0 = reinterpret_cast<const longlong2 *>(pa)[2 * q];
+            const longlong2 a1 = reinterpret_cast<const longlong2 *>(pa)[2 * q + 1];
+            reinterpret_cast<int4 *>(p32)[q] = make_int4((int)a0.x, (int)a0.y, (int)a1.x, (int)a1.y);
+        }
+    }
+    for (int64_t i = ((n >> 2) << 2) + tid; i < n; i += nth) {
+        lv8[i] = pack_level(lv[i], esc);
+        if (pa) p32[i] = (int32_t)pa[i];
+    }
 }
 
 __global__ void __launch_bounds__(BT) k_init(const View *__restrict__ views, int W) {
@@ -290,6 +352,11 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 
 Graph::~Graph() {
     if (h_ctl) cudaFreeHost(h_ctl);
+    for (int h = 0; h < 3; h++) {
+        if (hstage8[h]) cudaFreeHost(hstage8[h]);
+        if (hstage32[h]) cudaFreeHost(hstage32[h]);
+    }
+    if (hesc) cudaFreeHost(hesc);
     if (h_status) cudaFreeHost(h_status);
     for (void *q : peer_opened) cudaIpcCloseMemHandle(q);
 }
@@ -1109,6 +1176,7 @@ static void ensure_copy_stream(Ctx &ctx) {
         DBFS_CUDA(cudaEventCreateWithFlags(&ctx.ev_ready[b], cudaEventDisableTiming));
         DBFS_CUDA(cudaEventCreateWithFlags(&ctx.ev_done[b], cudaEventDisableTiming));
     }
+    for (int h = 0; h < 3; h++) DBFS_CUDA(cudaEventCreateWithFlags(&ctx.ev_hdone[h], cudaEventDisableTiming));
 }
 
 // Assembly arguments of the outputs a batch copies: the whole graph, or in a
@@ -1138,10 +1206,42 @@ static AsmArgs batch_asm(Graph &g, bool parents, bool local) {
     return aa;
 }
 
+// Host side of the compact transfer: int8 depth / int32 parent -> the caller's
+// int32 / int64 arrays (sign extension keeps -1), on every host core.
+static void widen_result(const int8_t *l8, const int32_t *p32, int64_t n, int32_t *lv, int64_t *pa) {
+    const int64_t CH = 1 << 16, nch = (n + CH - 1) / CH;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nch; c++) {
+        const int64_t b = c * CH, e = std::min(n, b + CH);
+        if (lv)
+            for (int64_t i = b; i < e; i++) lv[i] = l8[i];
+        if (pa)
+            for (int64_t i = b; i < e; i++) pa[i] = p32[i];
+    }
+}
+
+static void ensure_compact_staging(Graph &g, int64_t nout) {
+    if (g.hstage_n < nout) {
+        for (int h = 0; h < 3; h++) {
+            if (g.hstage8[h]) cudaFreeHost(g.hstage8[h]);
+            if (g.hstage32[h]) cudaFreeHost(g.hstage32[h]);
+            g.hstage8[h] = nullptr;
+            g.hstage32[h] = nullptr;
+        }
+        for (int h = 0; h < 3; h++) {
+            DBFS_CUDA(cudaHostAlloc((void **)&g.hstage8[h], std::max<int64_t>(nout, 1), cudaHostAllocDefault));
+            DBFS_CUDA(cudaHostAlloc((void **)&g.hstage32[h], 4 * std::max<int64_t>(nout, 1), cudaHostAllocDefault));
+        }
+        g.hstage_n = nout;
+    }
+    if (!g.hesc) DBFS_CUDA(cudaHostAlloc((void **)&g.hesc, 3 * sizeof(unsigned), cudaHostAllocDefault));
+    if (g.esc.n < 2) g.esc.alloc(2);
+}
+
 int64_t batch_output_count(const Graph &g, bool local) { return (local && g.dist) ? g.workers[0].n_local : g.n; }
 
 void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, int64_t count, int32_t *const *levels,
-                   int64_t *const *parents, int local, dbfs_run_stats *st) {
+                   int64_t *const *parents, int local, int compact_req, dbfs_run_stats *st) {
     Ctx &ctx = *g.ctx;
     DBFS_CHECK(o0.mode == 0 || o0.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
     for (int64_t k = 0; k < count; k++)
@@ -1219,6 +1319,8 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     // overwrites its state while a peer still assembles from it.
     const int W = g.W;
     const bool peer = engine == 3;
+    const bool compact = compact_req && levels && g.n < ((int64_t)1 << 31);
+    if (compact) ensure_compact_staging(g, nout);
     set_smem_attrs();
     if (g.pgrid <= 0) {
         int bps = 0;
@@ -1243,7 +1345,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     int nr = peer ? g.p : 1;
     const uint32_t *dil = g.del_id.p;
     uint32_t sdel = SRC_DEL_LOOKUP;
-    for (int64_t k = 0; k < count; k++) {
+    auto enqueue_root = [&](int64_t k, unsigned *esc_k) {
         int64_t src = roots[k];
         if (peer && k > 0) nccl_allreduce_async(ctx, flag);
         k_batch_prep<<<W, 256, 0, ctx.stream>>>(g.views.p, bar);
@@ -1256,13 +1358,106 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                                               ctx.stream));
         DBFS_LAUNCHED();
         DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
-        k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k);
+        if (esc_k && k >= 2) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[k & 1], 0));
+        k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k, esc_k);
         DBFS_LAUNCHED();
-        stage_and_copy(k, g.dist ? &out_asm : nullptr);
+    };
+    std::vector<int64_t> rerun;
+    if (!compact) {
+        for (int64_t k = 0; k < count; k++) {
+            enqueue_root(k, nullptr);
+            stage_and_copy(k, g.dist ? &out_asm : nullptr);
+        }
+    } else {
+        // Compact transfers: depth as int8, parent as int32 on the wire (5 bytes per
+        // vertex instead of 12); the host widens them into the caller's arrays
+        // (sign extension restores -1) while the GPU runs later roots.  Three
+        // pinned host staging sets: root k's D2H lands in set k%3 once root k-3
+        // has been widened.  A root with a depth >= 127 is re-run with full
+        // arrays after the batch.
+        const int blocks = ctx.num_sms * 4;
+        for (int64_t k = 0; k < count + 2; k++) {
+            if (k < count) {
+                const int b = (int)(k & 1);
+                enqueue_root(k, g.esc.p + b);
+                int8_t *l8 = reinterpret_cast<int8_t *>(g.stage_lv[b].p);
+                int32_t *p32 = reinterpret_cast<int32_t *>(g.stage_pv[b].p);
+                if (g.dist) {
+                    AsmArgs ca = out_asm;
+                    ca.glevel8 = l8;
+                    ca.gparent32 = want_par ? p32 : nullptr;
+                    ca.parents = want_par;
+                    ca.esc = g.esc.p + b;
+                    k_assemble<<<blocks, BT, 0, ctx.stream>>>(ca);
+                } else {
+                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), want_par ? g.parents_dev() : nullptr,
+                                                                  nout, l8, p32, g.esc.p + b);
+                }
+                DBFS_LAUNCHED();
+                DBFS_CUDA(cudaEventRecord(ctx.ev_ready[b], ctx.stream));
+            }
+            if (k >= 1 && k - 1 < count) {
+                const int64_t j = k - 1;
+                const int b = (int)(j & 1), hb = (int)(j % 3);
+                DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
+                DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb], g.stage_lv[b].p, nout, cudaMemcpyDeviceToHost,
+                                          ctx.copy_stream));
+                if (want_par)
+                    DBFS_CUDA(cudaMemcpyAsync(g.hstage32[hb], g.stage_pv[b].p, 4 * nout, cudaMemcpyDeviceToHost,
+                                              ctx.copy_stream));
+                DBFS_CUDA(cudaMemcpyAsync(g.hesc + hb, g.esc.p + b, 4, cudaMemcpyDeviceToHost, ctx.copy_stream));
+                DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
+                DBFS_CUDA(cudaEventRecord(ctx.ev_hdone[hb], ctx.copy_stream));
+                if (st) st[j].d2h_bytes += nout + (want_par ? 4 * nout : 0) + 4;
+            }
+            if (k >= 2) {
+                const int64_t j = k - 2;
+                const int hb = (int)(j % 3);
+                DBFS_CUDA(cudaEventSynchronize(ctx.ev_hdone[hb]));
+                if (g.hesc[hb]) rerun.push_back(j);
+                else widen_result(g.hstage8[hb], want_par ? g.hstage32[hb] : nullptr, nout, levels[j],
+                                  want_par ? parents[j] : nullptr);
+            }
+        }
     }
     if (peer) nccl_allreduce_async(ctx, flag);  // peers may read this rank's arrays until every assembly is done
     DBFS_CUDA(cudaStreamSynchronize(ctx.copy_stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (compact) {
+        // roots with an escaped depth (>= 127) again, with full arrays; every rank
+        // of a distributed run takes part in the same re-runs
+        std::vector<int64_t> fl(count, 0);
+        for (int64_t j : rerun) fl[j] = 1;
+        if (g.dist) {
+            DArray<int64_t> d;
+            d.alloc(count);
+            DBFS_CUDA(cudaMemcpy(d.p, fl.data(), 8 * count, cudaMemcpyHostToDevice));
+            nccl_allreduce_i64(ctx, d.p, count, 0);
+            DBFS_CUDA(cudaMemcpy(fl.data(), d.p, 8 * count, cudaMemcpyDeviceToHost));
+        }
+        for (int64_t j = 0; j < count; j++) {
+            if (!fl[j]) continue;
+            dbfs_bfs_options o = o0;
+            o.source = roots[j];
+            run_bfs(g, o, nullptr);
+            if (g.dist) {
+                AsmArgs fa = batch_asm(g, want_par, local != 0);
+                fa.glevel = g.stage_lv[0].p;
+                fa.gparent = want_par ? g.stage_pv[0].p : nullptr;
+                fa.parents = want_par;
+                k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(fa);
+                DBFS_LAUNCHED();
+                if (peer) nccl_barrier(ctx);
+                DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+                if (levels[j]) DBFS_CUDA(cudaMemcpy(levels[j], g.stage_lv[0].p, 4 * nout, cudaMemcpyDeviceToHost));
+                if (want_par && parents[j])
+                    DBFS_CUDA(cudaMemcpy(parents[j], g.stage_pv[0].p, 8 * nout, cudaMemcpyDeviceToHost));
+                g.assembled = false;
+            } else {
+                fetch_result(g, levels[j], want_par ? parents[j] : nullptr);
+            }
+        }
+    }
     std::vector<int2> hi(count);
     DBFS_CUDA(cudaMemcpy(hi.data(), info.p, sizeof(int2) * count, cudaMemcpyDeviceToHost));
     const int64_t launches = g_kernel_launches - launches0;

@@ -195,6 +195,7 @@ struct Ctx {
     DArray<unsigned char> flush;     // L2 flush buffer (bench hygiene)
     cudaStream_t copy_stream = nullptr;  // non-blocking: result D2H of dbfs_bfs_batch
     cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+    cudaEvent_t ev_hdone[3] = {nullptr, nullptr, nullptr};  // compact batch: host staging set filled
     int flush_val = 1;
     void *ensure_scratch(size_t bytes);
 };
@@ -284,6 +285,11 @@ struct Graph {
     DArray<unsigned long long> trace;  // DBFS_TRACE=<file>: block phase timestamps (diagnostics)
     DArray<int32_t> stage_lv[2];     // dbfs_bfs_batch: result staging, double-buffered
     DArray<int64_t> stage_pv[2];
+    int8_t *hstage8[3] = {nullptr, nullptr, nullptr};   // compact batch: pinned host staging (depth int8)
+    int32_t *hstage32[3] = {nullptr, nullptr, nullptr}; //   and parent int32
+    int64_t hstage_n = 0;
+    unsigned *hesc = nullptr;        // pinned: escape counts of the 3 host sets
+    DArray<unsigned> esc;            // device escape counters (2 staging buffers)
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();
@@ -305,7 +311,7 @@ void rmat_generate_host(Ctx &ctx, const dbfs_rmat_params &prm, int64_t begin, in
 void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st);
 void fetch_result(Graph &g, int32_t *levels, int64_t *parents);
 void run_bfs_batch(Graph &g, const dbfs_bfs_options &o, const int64_t *roots, int64_t count, int32_t *const *levels,
-                   int64_t *const *parents, int local, dbfs_run_stats *st);
+                   int64_t *const *parents, int local, int compact, dbfs_run_stats *st);
 int64_t batch_output_count(const Graph &g, bool local);
 void min_parents(Graph &g, int64_t *out);
 int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents);

@@ -19,8 +19,9 @@ def api():
     return api
 
 
+@pytest.mark.parametrize("compact", [True, False])
 @pytest.mark.parametrize("shape", [(1, 1), (2, 2)])
-def test_batch_matches_single_calls_and_oracle(api, shape):
+def test_batch_matches_single_calls_and_oracle(api, shape, compact):
     from paper_1803_03922_b200 import _lib
     scale, seed, theta = 12, 3, 16
     pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=seed)), theta,
@@ -28,7 +29,7 @@ def test_batch_matches_single_calls_and_oracle(api, shape):
     src, dst = O.rmat_edges(scale, seed=seed)
     og = O.partition(src, dst, 1 << scale, theta, *shape)
     roots = [7, 100, 7, 4000, 17, 2]
-    outs, st = api.bfs_batch(pg, roots, stats=True)
+    outs, st = api.bfs_batch(pg, roots, stats=True, compact=compact)
     assert len(outs) == len(roots) and len(st) == len(roots)
     for r, (lv, pa), s in zip(roots, outs, st):
         ref = O.run_bfs(og, r, mode="dobfs")
@@ -40,7 +41,7 @@ def test_batch_matches_single_calls_and_oracle(api, shape):
     # two pinned pairs used alternately: the last two roots' results survive
     pairs = [(_lib.pinned_empty(pg.n, np.int32), _lib.pinned_empty(pg.n, np.int64)) for _ in range(2)]
     outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(len(roots))]
-    api.bfs_batch(pg, roots, outs=outs, mode="bfs")
+    api.bfs_batch(pg, roots, outs=outs, mode="bfs", compact=compact)
     for i in (len(roots) - 2, len(roots) - 1):
         lv, pa = outs[i]
         assert api.levels_digest(lv) == O.run_bfs(og, roots[i], mode="bfs")["levels_digest"]
@@ -56,3 +57,19 @@ def test_batch_errors(api):
     assert api.bfs_batch(pg, []) == []
     lv = api.bfs_batch(pg, [5], parents=None)[0][0]
     assert lv[5] == 0
+
+
+def test_compact_batch_escapes_deep_levels(api):
+    """Depths >= 127 do not fit the int8 wire form: such roots are re-run with
+    full arrays, results identical to single calls (a 400-vertex path)."""
+    n = 400
+    src = np.arange(n - 1, dtype=np.int64)
+    g = api.EdgeList(np.concatenate([src, src + 1]), np.concatenate([src + 1, src]), n=n, symmetric=True)
+    pg = api.partition_graph(g, 1, api.ClusterShape(1, 1))
+    roots = [0, 200, 5, 399]
+    outs = api.bfs_batch(pg, roots, compact=True)
+    for r, (lv, pa) in zip(roots, outs):
+        assert lv.tolist() == [abs(v - r) for v in range(n)]
+        assert api.validate_bfs_tree(pg, r, lv, pa) == 0
+        ref_lv, _ = api.bfs(pg, r)
+        assert np.array_equal(lv, ref_lv)
