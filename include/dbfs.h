@@ -200,9 +200,9 @@ int32_t dbfs_fetch_result(dbfs_graph *g, int32_t *levels_out, int64_t *parents_o
  * stream while root k+1 traverses.  local != 0 in a distributed context: each rank
  * receives only the vertices it owns (v mod p == rank, output i = vertex rank + i*p),
  * the distributed Graph500 result; otherwise every rank gets all n.  compact != 0:
- * depth travels as int8 and parent as int32 (5 instead of 12 bytes per vertex over
- * PCIe; n < 2^31) and the host widens them into the caller's arrays on every core
- * while later roots run; a root with a depth >= 127 is re-run with full arrays.
+ * the depth travels as int8 (9 instead of 12 bytes per vertex over PCIe; n < 2^31)
+ * and the host widens it into the caller's array on every core while later roots
+ * run; a root with a depth >= 127 is re-run with full arrays.
  * Per-iteration records are not kept.  stats (nullable) receives count entries. */
 int32_t dbfs_bfs_batch(dbfs_graph *g, const dbfs_bfs_options *opts, const int64_t *roots, int64_t count,
                        int32_t *const *levels_out, int64_t *const *parents_out, int32_t local, int32_t compact,

@@ -8,6 +8,7 @@
 //               used with one worker per process (torchrun, NCCL over NVLink).
 #include <algorithm>
 #include <cstdio>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -178,7 +179,10 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
                 if (a.parents) par = a.nparent[w][i];
             }
             a.glevel8[o] = pack_level(l, a.esc);
-            if (a.parents) a.gparent32[o] = (int32_t)par;
+            if (a.parents) {
+                if (a.gparent32) a.gparent32[o] = (int32_t)par;
+                else a.gparent[o] = par;
+            }
             continue;
         }
         if (di != 0xffffffffu) {
@@ -1208,9 +1212,9 @@ static AsmArgs batch_asm(Graph &g, bool parents, bool local) {
 
 // Host side of the compact transfer: int8 depth / int32 parent -> the caller's
 // int32 / int64 arrays (sign extension keeps -1), on every host core.
-static void widen_result(const int8_t *l8, const int32_t *p32, int64_t n, int32_t *lv, int64_t *pa) {
+static void widen_result(const int8_t *l8, const int32_t *p32, int64_t n, int32_t *lv, int64_t *pa, int nthreads) {
     const int64_t CH = 1 << 16, nch = (n + CH - 1) / CH;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(nthreads)
     for (int64_t c = 0; c < nch; c++) {
         const int64_t b = c * CH, e = std::min(n, b + CH);
         if (lv)
@@ -1369,54 +1373,63 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             stage_and_copy(k, g.dist ? &out_asm : nullptr);
         }
     } else {
-        // Compact transfers: depth as int8, parent as int32 on the wire (5 bytes per
-        // vertex instead of 12); the host widens them into the caller's arrays
+        // Compact transfers: the depth travels as int8 (9 bytes per vertex on the
+        // wire instead of 12; parents go straight into the caller's int64 array)
+        // and the host widens it into the caller's int32 array on every core
         // (sign extension restores -1) while the GPU runs later roots.  Three
-        // pinned host staging sets: root k's D2H lands in set k%3 once root k-3
-        // has been widened.  A root with a depth >= 127 is re-run with full
-        // arrays after the batch.
+        // pinned host staging sets: root k's D2H lands in set k%3, whose previous
+        // root (k-3) the host widened one iteration earlier.  A root with a depth
+        // >= 127 is re-run with full arrays after the batch.
         const int blocks = ctx.num_sms * 4;
+        // the host's cores shared by the ranks on it (launchers such as torchrun
+        // pin OMP_NUM_THREADS to 1, so the count is set here explicitly)
+        const int host_threads =
+            std::max(1, (int)std::thread::hardware_concurrency() / std::max(1, g.dist ? ctx.nranks : 1));
         for (int64_t k = 0; k < count + 2; k++) {
             if (k < count) {
                 const int b = (int)(k & 1);
                 enqueue_root(k, g.esc.p + b);
                 int8_t *l8 = reinterpret_cast<int8_t *>(g.stage_lv[b].p);
-                int32_t *p32 = reinterpret_cast<int32_t *>(g.stage_pv[b].p);
                 if (g.dist) {
                     AsmArgs ca = out_asm;
                     ca.glevel8 = l8;
-                    ca.gparent32 = want_par ? p32 : nullptr;
+                    ca.gparent32 = nullptr;  // parents travel as int64 (no host widening)
+                    ca.gparent = want_par ? g.stage_pv[b].p : nullptr;
                     ca.parents = want_par;
                     ca.esc = g.esc.p + b;
                     k_assemble<<<blocks, BT, 0, ctx.stream>>>(ca);
+                    DBFS_LAUNCHED();
                 } else {
-                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), want_par ? g.parents_dev() : nullptr,
-                                                                  nout, l8, p32, g.esc.p + b);
+                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), nullptr, nout, l8, nullptr,
+                                                                  g.esc.p + b);
+                    DBFS_LAUNCHED();
+                    if (want_par) {
+                        k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(),
+                                                                     (uint8_t *)g.stage_pv[b].p, 8 * nout);
+                        DBFS_LAUNCHED();
+                    }
                 }
-                DBFS_LAUNCHED();
                 DBFS_CUDA(cudaEventRecord(ctx.ev_ready[b], ctx.stream));
-            }
-            if (k >= 1 && k - 1 < count) {
-                const int64_t j = k - 1;
-                const int b = (int)(j & 1), hb = (int)(j % 3);
+                // root k's D2H is queued at once: the copy engine runs back to back
+                // while the host widens root k-2 (host set k%3 last held root k-3)
+                const int hb = (int)(k % 3);
                 DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
                 DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb], g.stage_lv[b].p, nout, cudaMemcpyDeviceToHost,
                                           ctx.copy_stream));
-                if (want_par)
-                    DBFS_CUDA(cudaMemcpyAsync(g.hstage32[hb], g.stage_pv[b].p, 4 * nout, cudaMemcpyDeviceToHost,
+                if (want_par && parents[k])  // straight into the caller's array
+                    DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * nout, cudaMemcpyDeviceToHost,
                                               ctx.copy_stream));
                 DBFS_CUDA(cudaMemcpyAsync(g.hesc + hb, g.esc.p + b, 4, cudaMemcpyDeviceToHost, ctx.copy_stream));
                 DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
                 DBFS_CUDA(cudaEventRecord(ctx.ev_hdone[hb], ctx.copy_stream));
-                if (st) st[j].d2h_bytes += nout + (want_par ? 4 * nout : 0) + 4;
+                if (st) st[k].d2h_bytes += nout + (want_par && parents[k] ? 8 * nout : 0) + 4;
             }
             if (k >= 2) {
                 const int64_t j = k - 2;
                 const int hb = (int)(j % 3);
                 DBFS_CUDA(cudaEventSynchronize(ctx.ev_hdone[hb]));
                 if (g.hesc[hb]) rerun.push_back(j);
-                else widen_result(g.hstage8[hb], want_par ? g.hstage32[hb] : nullptr, nout, levels[j],
-                                  want_par ? parents[j] : nullptr);
+                else widen_result(g.hstage8[hb], nullptr, nout, levels[j], nullptr, host_threads);
             }
         }
     }

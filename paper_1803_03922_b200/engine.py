@@ -253,7 +253,7 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
 
 
 def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
-              stats: bool = False, local: bool = False, compact: bool = False):
+              stats: bool = False, local: bool = False, compact: bool = True):
     """Graph500's multi-root loop in one call (``dbfs_bfs_batch``): returns one
     (depth, parent) pair per root.  The device-to-host copy of root k runs on a
     separate stream while root k+1 traverses, so PCIe time hides behind the
@@ -263,12 +263,11 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
     alternately, in which case each root's result is in its pair until root
     k+2 overwrites it.  ``local=True`` in a distributed run gives each rank
     only the vertices it owns (entry i = vertex rank + i*world), the
-    distributed Graph500 result.  ``compact`` sends depth as int8 and parent as
-    int32 over PCIe (5 instead of 12 bytes per vertex) and widens them on the
-    host's cores into ``outs`` (identical results; a root with a depth >= 127
-    is re-run with full arrays).  Off by default: on the B200 hosts measured,
-    widening 12 bytes per vertex on the CPU costs more than the PCIe bytes it
-    saves (s24: 45 vs 73 GTEPS e2e).  Per-iteration records are not kept.
+    distributed Graph500 result.  ``compact`` sends the depth as int8 over
+    PCIe (9 instead of 12 bytes per vertex; parents go straight into ``outs``)
+    and widens it on the host's cores while later roots traverse (identical
+    results; a root with a depth >= 127 is re-run with full arrays).
+    Per-iteration records are not kept.
     ``stats=True`` also returns the per-root C run-stats structs."""
     roots = np.ascontiguousarray([int(r) for r in roots], dtype=np.int64)
     for r in roots:
