@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <thread>
+
+#include <sched.h>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1224,6 +1226,15 @@ static void widen_result(const int8_t *l8, const int32_t *p32, int64_t n, int32_
     }
 }
 
+// CPUs this process may run on (its affinity mask, as nproc reports; the
+// machine's logical CPU count can be far larger inside a container).
+static int usable_cpus() {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, (int)CPU_COUNT(&set));
+    return std::max(1, (int)std::thread::hardware_concurrency());
+}
+
 static void ensure_compact_staging(Graph &g, int64_t nout) {
     if (g.hstage_n < nout) {
         for (int h = 0; h < 3; h++) {
@@ -1383,8 +1394,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         const int blocks = ctx.num_sms * 4;
         // the host's cores shared by the ranks on it (launchers such as torchrun
         // pin OMP_NUM_THREADS to 1, so the count is set here explicitly)
-        const int host_threads =
-            std::max(1, (int)std::thread::hardware_concurrency() / std::max(1, g.dist ? ctx.nranks : 1));
+        const int host_threads = std::max(1, std::min(16, usable_cpus() / std::max(1, g.dist ? ctx.nranks : 1)));
         for (int64_t k = 0; k < count + 2; k++) {
             if (k < count) {
                 const int b = (int)(k & 1);

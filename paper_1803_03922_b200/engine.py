@@ -17,6 +17,7 @@ import ctypes
 import dataclasses
 import hashlib
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -253,7 +254,7 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
 
 
 def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
-              stats: bool = False, local: bool = False, compact: bool = True):
+              stats: bool = False, local: bool = False, compact: bool | None = None):
     """Graph500's multi-root loop in one call (``dbfs_bfs_batch``): returns one
     (depth, parent) pair per root.  The device-to-host copy of root k runs on a
     separate stream while root k+1 traverses, so PCIe time hides behind the
@@ -266,8 +267,10 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
     distributed Graph500 result.  ``compact`` sends the depth as int8 over
     PCIe (9 instead of 12 bytes per vertex; parents go straight into ``outs``)
     and widens it on the host's cores while later roots traverse (identical
-    results; a root with a depth >= 127 is re-run with full arrays).
-    Per-iteration records are not kept.
+    results; a root with a depth >= 127 is re-run with full arrays).  None:
+    on for a single process, off when ranks share the host (their widening
+    competes for it); ``DBFS_COMPACT=0/1`` overrides.  Per-iteration records
+    are not kept.
     ``stats=True`` also returns the per-root C run-stats structs."""
     roots = np.ascontiguousarray([int(r) for r in roots], dtype=np.int64)
     for r in roots:
@@ -285,6 +288,9 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
             raise ValueError(f"levels buffers must be contiguous int32[{nout}]")
         if pa is not None and (pa.dtype != np.int64 or pa.size < nout or not pa.flags.c_contiguous):
             raise ValueError(f"parents buffers must be contiguous int64[{nout}]")
+    if compact is None:
+        env = os.environ.get("DBFS_COMPACT")
+        compact = (env == "1") if env in ("0", "1") else pg.nranks <= 1
     lv_ptrs = (_lib.vp * max(count, 1))(*[lv.ctypes.data if lv is not None else None for lv, _ in outs])
     pa_ptrs = (_lib.vp * max(count, 1))(*[pa.ctypes.data if pa is not None else None for _, pa in outs])
     st = (_lib.RunStatsC * max(count, 1))()
