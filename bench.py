@@ -303,7 +303,8 @@ def run_ours(args, world, rank, local_rank):
         "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h / args.steps),
                 "api": "bfs_batch: all steps in one call, D2H of step k overlapped with step k+1 (no L2 flush; graph > L2); "
-                       "depth sent as int8 and widened on the host, parents as int64"
+                       + ("depth sent as int8 and widened on the host, parents as int64" if not dist
+                          else "full int32 depth / int64 parent arrays")
                        + ("; each rank receives the depth/parent entries of the vertices it owns" if dist else ""),
                 "per_call_bfs": round(e2e_single, 4)},
         "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
