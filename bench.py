@@ -226,6 +226,7 @@ def run_ours(args, world, rank, local_rank):
     wall = time.perf_counter() - wall0
     launches = _lib.kernel_launches() - launches0
     engine_used = int(stats[-1].engine_used)
+    clocks = sampler.stop()  # the device-timed region ends here (nvidia-smi polling would perturb the e2e host loop)
 
     # e2e through the public API: depth + parent of every step to pinned host
     # buffers.  Headline: bfs_batch over the K roots (the D2H of step k overlaps
@@ -239,6 +240,9 @@ def run_ours(args, world, rank, local_rank):
     pairs = [(_lib.pinned_empty(nout, np.int32), _lib.pinned_empty(nout, np.int64)) for _ in range(2)]
     outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(args.steps)]
     step_roots = [roots[i % len(roots)] for i in range(args.steps)]
+    # untimed warm-up call: staging buffers and copy-stream events are allocated once
+    bfs_batch(pg, step_roots[: max(1, min(args.warmup, len(step_roots)))], outs=outs[: max(1, min(args.warmup,
+              len(step_roots)))], mode=args.mode, local=dist)
     if dist:
         ctx.barrier()
     t = time.perf_counter()
@@ -253,7 +257,6 @@ def run_ours(args, world, rank, local_rank):
         t = time.perf_counter()
         bfs(pg, roots[i % len(roots)], mode=args.mode, out=(lv_buf.array, pa_buf.array))
         e2e_s.append(time.perf_counter() - t)
-    clocks = sampler.stop()
 
     # max over ranks, per step
     if dist:

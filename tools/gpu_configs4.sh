@@ -16,3 +16,9 @@ run er_s28_bfs_4gpu 4 --graph er --mode bfs --scale 28 --scaling strong --theta 
 run s27_1gpu 1 --scale 27 --steps 32
 run s28_2gpu 2 --scale 27 --steps 32
 run s29_4gpu 4 --scale 27 --steps 32
+run er_s24_dobfs_1gpu 1 --graph er --scale 24 --steps 32
+run er_s25_dobfs_2gpu 2 --graph er --steps 32
+run er_s26_dobfs_4gpu 4 --graph er --steps 32
+run er_s24_bfs_1gpu 1 --graph er --mode bfs --scale 24 --steps 16
+run er_s25_bfs_2gpu 2 --graph er --mode bfs --steps 16
+run er_s26_bfs_4gpu 4 --graph er --mode bfs --steps 16

@@ -21,7 +21,7 @@ for k, t in rows:
 tot = sum(v[1] for v in agg.values())
 bfs = [t for k, t in rows if "k_bfs_persistent" in k]
 with open(os.path.join(out_dir, "ncu_launches_summary.txt"), "w") as f:
-    f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 4 --warmup 1 --no-cpu-baseline\n")
+    f.write("ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-alt-labeling\n")
     f.write("(cold-cache, serialised launches; compare shares, not absolutes)\n\n")
     f.write(f"{'kernel':60s} {'launches':>8s} {'total us':>12s} {'share':>7s}\n")
     for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
