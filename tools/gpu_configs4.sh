@@ -8,6 +8,7 @@ run() {  # name N args...
   echo "$name rc=$?"; python -c "
 import json; d=json.load(open('gpurun_out/cfg/$name.json')); print('  ', d['value'], d['e2e']['value'], d['ms_per_step'], d['config']['workload'])" 2>/dev/null
 }
+run s26_4gpu_peer 4 --steps 64
 run bfs_s26_1gpu 1 --mode bfs --scale 26 --scaling strong --steps 16
 run bfs_s26_2gpu 2 --mode bfs --scale 26 --scaling strong --steps 16
 run bfs_s26_4gpu 4 --mode bfs --scale 26 --scaling strong --steps 16
