@@ -1013,8 +1013,11 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         const bool nd_fwd = ex[KIND_ND] != BWD && S.fv[KIND_ND] > 0;
         const bool nd_cnt = ex[KIND_ND] == PUSHC && V.first[KIND_ND];
         const uint32_t *has_nn = V.src_bits[KIND_NN], *has_nd = V.src_bits[KIND_ND];
-        for (WarpChunks ch(S.nfront > (unsigned long long)TW ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW);
-             ch.valid(); ch.next()) {
+        // claim chunks dynamically only when the rows to push, not the bitmap
+        // scan, dominate (uniform frontier bits balance a static stride)
+        const unsigned long long t1_edges = S.fv[KIND_NN] + (nd_fwd ? S.fv[KIND_ND] : 0ull);
+        const bool t1_dyn = S.nfront > (unsigned long long)TW && t1_edges > (unsigned long long)V.t1_dyn_min * V.nw_n;
+        for (WarpChunks ch(t1_dyn ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
             // groups of 1024 normals without frontier bits (coarse fold of F(L-1)) are skipped
             if (DBFS_CWN == 32 && !__ldcg(&V.coarse_n[L & 1][ch.cur & (FW - 1)])) continue;
             const int64_t wi = ch.word(V.nw_n);
@@ -1399,7 +1402,7 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
     uint32_t *cur = V.nfront[L & 1];
     const uint32_t *nxt = V.nfront[(L + 1) & 1];
     const LevelSlot &A = V.ctl->s[L % 3];
-    const bool dyn = A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
+    const bool dyn = V.f3_dyn && A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
     uint32_t *cnt_dn = A.exec_dir[KIND_DN] == PUSHC ? V.first[KIND_DN] : nullptr;
     for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[5] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
         const int64_t base = ch.base();

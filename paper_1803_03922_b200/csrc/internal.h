@@ -96,7 +96,9 @@ struct View {
     int cand_all;                    // all workers' delegate candidates readable
     int P_sources;                   // mask sources for the OR
     int rec_cap;
-    int pad0, pad1, pad2;
+    int t1_dyn_min;                  // T1 claims chunks dynamically above this many pushed edges per bitmap word
+    int f3_dyn;                      // F3 claims chunks dynamically on heavy levels (0: static stride)
+    int pad2;
     PDiv pd;
     int64_t n, n_local, d, nw_n, nw_d;
     double f0[4], f1[4];
