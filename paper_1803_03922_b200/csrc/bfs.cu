@@ -466,6 +466,7 @@ static void ensure_resources(Graph &g) {
         V.rec_cap = g.rec_cap;
         V.t1_dyn_min = getenv("DBFS_T1_DYN_MIN") ? atoi(getenv("DBFS_T1_DYN_MIN")) : 4;
         V.f3_dyn = getenv("DBFS_F3_DYN") ? atoi(getenv("DBFS_F3_DYN")) : 1;
+        V.pull_dyn_min = getenv("DBFS_PULL_DYN_MIN") ? atoi(getenv("DBFS_PULL_DYN_MIN")) : 32;
         {
             // one 64-bit atomic reserves list slots and edge prefixes together:
             // edge bits for this worker's dn/dd totals, count bits for d

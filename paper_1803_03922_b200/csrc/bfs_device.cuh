@@ -903,7 +903,7 @@ __device__ __forceinline__ bool dyn_pull(const View &V, const unsigned long long
     unsigned long long U, Q, Sx;
     const unsigned long long q0[4] = {0, 0, 0, 0};
     level_inputs(V.total_src, cum, q0, k, U, Q, Sx);
-    return U > 32ull * (unsigned long long)TW;
+    return U > (unsigned long long)V.pull_dyn_min * (unsigned long long)TW;
 }
 
 // The record of level L made by one whole warp (the message flags and timers

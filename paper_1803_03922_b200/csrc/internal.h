@@ -98,7 +98,7 @@ struct View {
     int rec_cap;
     int t1_dyn_min;                  // T1 claims chunks dynamically above this many pushed edges per bitmap word
     int f3_dyn;                      // F3 claims chunks dynamically on heavy levels (0: static stride)
-    int pad2;
+    int pull_dyn_min;                // pulls claim chunks dynamically above this many candidates per warp
     PDiv pd;
     int64_t n, n_local, d, nw_n, nw_d;
     double f0[4], f1[4];
