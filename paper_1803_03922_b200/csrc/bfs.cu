@@ -58,6 +58,9 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
 // `cont_level` (over every worker's / rank's control block) once for the grid
 // and publishes it in cv->ctl->cont before releasing; `ts` gets its
 // local-complete / global-complete timestamps.
+#ifndef DBFS_BAR_SLEEP
+#define DBFS_BAR_SLEEP 64  // ns between a waiting block's polls of the barrier generation
+#endif
 __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBar *gbar = nullptr,
                                           unsigned nranks = 1, const View *cv = nullptr, int cont_level = 0,
                                           unsigned long long *ts = nullptr) {
@@ -110,7 +113,9 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBa
                     atomicExch(&bar->abort, 1u);
                     break;
                 }
-                __nanosleep(64);
+#if DBFS_BAR_SLEEP > 0
+                __nanosleep(DBFS_BAR_SLEEP);
+#endif
             }
         }
         if (gbar) __threadfence_system();
