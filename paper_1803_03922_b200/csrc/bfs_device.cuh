@@ -275,6 +275,15 @@ __host__ __device__ inline void make_record(const View &V, const Ctl &c, int L, 
 #define DBFS_UNR 4
 #endif
 constexpr int UNR = DBFS_UNR;    // independent column loads in flight per lane (push)
+#ifndef DBFS_ROWS_UNR
+#define DBFS_ROWS_UNR DBFS_UNR
+#endif
+#ifndef DBFS_LIST_UNR
+#define DBFS_LIST_UNR DBFS_UNR
+#endif
+constexpr int ROWS_UNR = DBFS_ROWS_UNR;  // normal-row pushes (nn, nd)
+constexpr int LIST_UNR = DBFS_LIST_UNR;  // delegate-list pushes (dn, dd)
+static_assert(ROWS_UNR <= UNR && LIST_UNR <= UNR, "send chunks are sized for UNR");
 constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
 constexpr int PROBE = 4;         // candidate groups whose first entry is probed together
 constexpr unsigned FULL = 0xffffffffu;
@@ -397,7 +406,7 @@ __device__ __forceinline__ unsigned long long *block_sendmask() {
     return &s_mask;
 }
 
-// Remote nn targets of one warp step (UNR slots, engine.py:207-222 ->
+// Remote nn targets of one warp step (U slots, engine.py:207-222 ->
 // comm.py:138-197), handled as one batch so the slots' memory round trips
 // overlap.  In-process peers are claimed directly in their bitmaps; a
 // distributed peer gets an 8-byte record in its inbox segment, unless this
@@ -406,17 +415,18 @@ __device__ __forceinline__ unsigned long long *block_sendmask() {
 // bit per global id (test, then set) keeps each remote target to a single
 // record per sender.  The reference counters see every record
 // (vc.records, the destination mask).
-__device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool (&need)[UNR], const uint32_t (&o)[UNR],
-                                                const uint32_t (&c)[UNR], const uint32_t (&parent)[UNR],
+template <int U>
+__device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool (&need)[U], const uint32_t (&o)[U],
+                                                const uint32_t (&c)[U], const uint32_t (&parent)[U],
                                                 VisitCounters &vc) {
     bool any = false;
 #pragma unroll
-    for (int u = 0; u < UNR; u++) any |= need[u];
+    for (int u = 0; u < U; u++) any |= need[u];
     if (!__any_sync(FULL, any)) return;
     {
         unsigned lo = 0, hi = 0;
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             if (need[u]) {
                 vc.records++;
                 if (o[u] < 32) lo |= 1u << o[u];
@@ -429,7 +439,7 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
     }
     if (!V.dist) {
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             if (!need[u]) continue;
             if (V.uniquify) {  // staging group of (sender, dest): comm.py:165-171
                 int grp = V.local_all2all ? (V.w % V.p_rank) + V.p_rank * ((int)o[u] / V.p_rank) : V.w;
@@ -442,31 +452,31 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
         }
         return;
     }
-    bool ship[UNR];
+    bool ship[U];
     if (V.sent) {
-        uint32_t w[UNR];
+        uint32_t w[U];
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {  // all tests in flight, then all sets
+        for (int u = 0; u < U; u++) {  // all tests in flight, then all sets
             const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
             w[u] = need[u] ? __ldcg(&V.sent[gv >> 5]) : 0xffffffffu;
         }
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
             const uint32_t bit = 1u << (gv & 31);
             ship[u] = need[u] && !(w[u] & bit);
             if (ship[u]) w[u] = atomicOr(&V.sent[gv >> 5], bit);
         }
 #pragma unroll
-        for (int u = 0; u < UNR; u++) ship[u] = ship[u] && !(w[u] & (1u << ((c[u] * (uint32_t)V.p + o[u]) & 31)));
+        for (int u = 0; u < U; u++) ship[u] = ship[u] && !(w[u] & (1u << ((c[u] * (uint32_t)V.p + o[u]) & 31)));
     } else {
 #pragma unroll
-        for (int u = 0; u < UNR; u++) ship[u] = need[u];
+        for (int u = 0; u < U; u++) ship[u] = need[u];
     }
     // destinations with records to ship, then one slot reservation per destination
     unsigned long long dm = 0;
 #pragma unroll
-    for (int u = 0; u < UNR; u++)
+    for (int u = 0; u < U; u++)
         if (ship[u]) dm |= 1ull << o[u];
     {
         const unsigned lo = __reduce_or_sync(FULL, (unsigned)dm);
@@ -477,9 +487,9 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
     while (dm) {
         const uint32_t dst = __ffsll(dm) - 1;
         dm &= dm - 1;
-        unsigned b[UNR], tot = 0;
+        unsigned b[U], tot = 0;
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             b[u] = __ballot_sync(FULL, ship[u] && o[u] == dst);
             tot += __popc(b[u]);
         }
@@ -494,7 +504,7 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
             }
             unsigned before = 0;
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
+            for (int u = 0; u < U; u++) {
                 if (ship[u] && o[u] == dst) {
                     const unsigned long long r = before + __popc(b[u] & lt);
                     V.sendbin[dst][r < rem ? cur + r : nb + (r - rem)] = make_uint2(c[u], parent[u]);
@@ -518,7 +528,7 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
         base = __shfl_sync(FULL, base, 0);
         unsigned before = 0;
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             if (ship[u] && o[u] == dst)
                 V.sendbin[dst][base + before + __popc(b[u] & lt)] = make_uint2(c[u], parent[u]);
             before += __popc(b[u]);
@@ -552,18 +562,18 @@ __device__ __forceinline__ bool push_edge(const View &V, int L, uint32_t col, in
     return false;
 }
 
-// Second stage of a push step: UNR columns per lane are resolved with all
+// Second stage of a push step: U columns per lane are resolved with all
 // status loads issued before any store (stores through the non-restrict state
 // pointers would otherwise serialise one L2 round trip per edge).
-template <int ACT, bool CNT>
-__device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t (&cc)[UNR], const uint32_t (&pp)[UNR],
-                                           const uint32_t (&tw)[UNR], uint32_t *first, const bool (&valid)[UNR],
+template <int ACT, bool CNT, int U>
+__device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t (&cc)[U], const uint32_t (&pp)[U],
+                                           const uint32_t (&tw)[U], uint32_t *first, const bool (&valid)[U],
                                            VisitCounters &vc) {
     // map the column to the (worker-local) vertex it names
-    uint32_t tgt[UNR];
-    bool local[UNR];
+    uint32_t tgt[U];
+    bool local[U];
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
+    for (int u = 0; u < U; u++) {
         local[u] = true;
         tgt[u] = cc[u];
         if (ACT == ACT_NN && V.p > 1) {
@@ -574,12 +584,12 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
     const uint32_t *vis = ACT == ACT_DELEG ? V.dvis : V.nvis;
     uint32_t *nxt = ACT == ACT_DELEG ? V.dnext[L & 1] : V.nfront[(L + 1) & 1];
     // stage 1: visited(<= L) words (read-only this phase: L1 is fine)
-    uint32_t s[UNR];
+    uint32_t s[U];
 #pragma unroll
-    for (int u = 0; u < UNR; u++) s[u] = (valid[u] && local[u]) ? __ldca(&vis[tgt[u] >> 5]) : 0xffffffffu;
+    for (int u = 0; u < U; u++) s[u] = (valid[u] && local[u]) ? __ldca(&vis[tgt[u] >> 5]) : 0xffffffffu;
     // stage 2: next-level words from L2 (written by other SMs this phase)
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
+    for (int u = 0; u < U; u++) {
         bool open = !((s[u] >> (tgt[u] & 31)) & 1u);
         if (ACT == ACT_DELEG && open) vc.dirty = 1;
         // counting push: every parent of an unvisited target bids its twin
@@ -590,7 +600,7 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
     // stage 3: fire-and-forget marks (RED.OR, no return value) and plain stores:
     // concurrent writers of one vertex store the same level and a valid parent.
 #pragma unroll
-    for (int u = 0; u < UNR; u++) {
+    for (int u = 0; u < U; u++) {
         const uint32_t x = tgt[u];
         if ((s[u] >> (x & 31)) & 1u) continue;
         atomicOr(&nxt[x >> 5], 1u << (x & 31));
@@ -601,10 +611,10 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         }
     }
     if (ACT == ACT_NN && V.p > 1) {
-        bool remote[UNR];
-        uint32_t own[UNR];
+        bool remote[U];
+        uint32_t own[U];
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             remote[u] = valid[u] && !local[u];
             own[u] = V.pd.mod(cc[u]);
         }
@@ -613,20 +623,20 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
 }
 
 // Expand <= 32 rows held one per lane (row start rb, length len, payload par)
-// with all lanes on consecutive edges and UNR independent loads per lane.
-template <int ACT, bool CNT = false>
+// with all lanes on consecutive edges and U independent loads per lane.
+template <int ACT, bool CNT = false, int U = ROWS_UNR>
 __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint32_t *__restrict__ col, int64_t rb,
                                                uint32_t len, uint32_t par, VisitCounters &vc,
                                                const uint32_t *__restrict__ twin = nullptr, uint32_t *first = nullptr) {
     unsigned tot;
     unsigned excl = warp_excl_scan(len, &tot);
     const unsigned lane = lane_id();
-    for (unsigned base = 0; base < tot; base += 32 * UNR) {
-        uint32_t cc[UNR];
-        uint32_t pp[UNR];
-        uint32_t tw[UNR];
+    for (unsigned base = 0; base < tot; base += 32 * U) {
+        uint32_t cc[U];
+        uint32_t pp[U];
+        uint32_t tw[U];
 #pragma unroll
-        for (int u = 0; u < UNR; u++) {
+        for (int u = 0; u < U; u++) {
             unsigned x = base + u * 32 + lane;
             int o = owner_search<unsigned>(excl, x);
             int64_t rbo = __shfl_sync(FULL, rb, o);
@@ -635,16 +645,16 @@ __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint3
             cc[u] = x < tot ? __ldg(&col[rbo + (x - eo)]) : 0u;
             tw[u] = (CNT && x < tot) ? __ldg(&twin[rbo + (x - eo)]) : 0u;
         }
-        bool valid[UNR];
+        bool valid[U];
 #pragma unroll
-        for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < tot;
-        push_stage<ACT, CNT>(V, L, cc, pp, tw, first, valid, vc);
+        for (int u = 0; u < U; u++) valid[u] = base + u * 32 + lane < tot;
+        push_stage<ACT, CNT, U>(V, L, cc, pp, tw, first, valid, vc);
     }
 }
 
 // Load-balanced push over a delegate frontier list (dlist, exclusive prefix
 // dpre, `cnt` rows, `total` edges): this warp handles edges [x0, x1).
-template <int ACT, bool CNT>
+template <int ACT, bool CNT, int U = LIST_UNR>
 __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *__restrict__ off,
                                           const uint32_t *__restrict__ col, const uint32_t *__restrict__ list,
                                           const int64_t *__restrict__ pre, int64_t cnt, int64_t total, int64_t x0,
@@ -680,12 +690,12 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
         if (lane == 0) wend = (i + 32 < cnt) ? pre[i + 32] : total;
         wend = __shfl_sync(FULL, wend, 0);
         int64_t lim = wend < x1 ? wend : x1;
-        for (int64_t base = x0; base < lim; base += 32 * UNR) {
-            uint32_t cc[UNR];
-            uint32_t pp[UNR];
-            uint32_t tw[UNR];
+        for (int64_t base = x0; base < lim; base += 32 * U) {
+            uint32_t cc[U];
+            uint32_t pp[U];
+            uint32_t tw[U];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) {
+            for (int u = 0; u < U; u++) {
                 int64_t x = base + u * 32 + lane;
                 int o = owner_search<int64_t>(pb, x);
                 int64_t rbo = __shfl_sync(FULL, rb, o);
@@ -694,10 +704,10 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
                 cc[u] = x < lim ? __ldg(&col[rbo + (x - pbo)]) : 0u;
                 tw[u] = (CNT && x < lim) ? __ldg(&twin[rbo + (x - pbo)]) : 0u;
             }
-            bool valid[UNR];
+            bool valid[U];
 #pragma unroll
-            for (int u = 0; u < UNR; u++) valid[u] = base + u * 32 + lane < lim;
-            push_stage<ACT, CNT>(V, L, cc, pp, tw, first, valid, vc);
+            for (int u = 0; u < U; u++) valid[u] = base + u * 32 + lane < lim;
+            push_stage<ACT, CNT, U>(V, L, cc, pp, tw, first, valid, vc);
         }
         x0 = lim;
         i += 32;
