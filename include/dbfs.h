@@ -86,7 +86,8 @@ typedef struct {
     double factor1[4];
     int32_t local_all2all;      /* accounting only (comm.py:138-197) */
     int32_t uniquify;           /* accounting only */
-    int32_t parent_mode;        /* 0 none, 1 any valid tree (timed), 2 min-ID */
+    int32_t parent_mode;        /* 0 none, 1 any valid tree (timed), 2 min-ID tree (computed on device after
+                                   the timed traversal; dbfs_bfs_batch: single-process graphs only) */
     int32_t engine;             /* 0 auto, 1 host-driven level loop, 2 persistent kernel, 3 peer (multi-GPU persistent over CUDA IPC) */
     int32_t record_iterations;  /* keep per-iteration records for dbfs_bfs_iteration */
     int32_t exec_policy;        /* 1: on symmetric graphs in dobfs mode, execute a FORWARD-reported

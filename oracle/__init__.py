@@ -57,6 +57,8 @@ def lib():
     sig = {
         "orc_rmat_edges": (c_int, [c_int, i64, c_double, c_double, c_double, u64, c_int, c_int, i64, i64, vp, vp]),
         "orc_hash_vertices": (c_int, [i64, u64, vp, vp, i64]),
+        "orc_rmat_summary": (c_int, [c_int, i64, c_double, c_double, c_double, u64, c_int, i64, vp,
+                                     ctypes.POINTER(i64), vp]),
         "orc_partition": (c_int, [vp, vp, i64, i64, i64, c_int, c_int, ctypes.POINTER(vp)]),
         "orc_partition_rmat": (c_int, [c_int, i64, c_double, c_double, c_double, u64, i64, c_int, c_int, ctypes.POINTER(vp)]),
         "orc_partition_rmat_flags": (c_int, [c_int, i64, c_double, c_double, c_double, u64, c_int, i64, c_int, c_int,
@@ -132,6 +134,20 @@ def rmat_edges(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=0, randomize=
                                 int(bool(randomize)) | (2 if scramble else 0),
                                 int(symmetrize), begin, end, _ptr(src), _ptr(dst)), "rmat")
     return src, dst
+
+
+def rmat_summary(scale, theta, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=0, scramble=False):
+    """(out-degree uint32[n], d, kind totals) of build_rmat_graph(params) with
+    threshold theta, streamed from the counter-based generator (no edge list is
+    stored, so scales 26-30 fit the host): partition.py:103-117 and the kind
+    totals of partition.py:312-318."""
+    n = 1 << scale
+    deg = np.empty(n, dtype=np.uint32)
+    d = i64()
+    kinds = np.zeros(4, dtype=np.int64)
+    _check(lib().orc_rmat_summary(scale, edge_factor, a, b, c, seed & (2**64 - 1), 3 if scramble else 1, theta,
+                                  _ptr(deg), ctypes.byref(d), _ptr(kinds)), "rmat_summary")
+    return deg, int(d.value), {k: int(kinds[i]) for i, k in enumerate(KINDS)}
 
 
 def hash_vertices(n, seed, ids):

@@ -204,6 +204,82 @@ int orc_rmat_edges(int scale, int64_t edge_factor, double a, double b, double c,
     return ORC_OK;
 }
 
+/* Graph summary straight from the counter-based generator, without storing
+ * the edge list: out-degrees (partition.py:103-104, bincount over the
+ * symmetrized list, i.e. deg(u)++ and deg(v)++ per original edge), the
+ * delegate count d = |{v : deg(v) > theta}| (partition.py:79-117) and the
+ * kind totals (partition.py:312-318; the kind of an edge depends only on its
+ * endpoints' classes).  Two multithreaded passes over the m0 original edges,
+ * so graphs far larger than the host could partition (scale 26-30) can be
+ * checked against the device build. */
+typedef struct {
+    const rmat_gen *g;
+    int64_t lo, hi;
+    uint32_t *deg;
+    const uint32_t *deg_ro;
+    int64_t theta;
+    int64_t kinds[4];
+} sum_job;
+
+static void *sum_deg_worker(void *arg) {
+    sum_job *j = (sum_job *)arg;
+    for (int64_t e = j->lo; e < j->hi; e++) {
+        uint64_t u, v;
+        rmat_edge(j->g, (uint64_t)e, &u, &v);
+        __atomic_fetch_add(&j->deg[u], 1u, __ATOMIC_RELAXED);
+        __atomic_fetch_add(&j->deg[v], 1u, __ATOMIC_RELAXED);
+    }
+    return NULL;
+}
+
+static void *sum_kind_worker(void *arg) {
+    sum_job *j = (sum_job *)arg;
+    int64_t k[4] = {0, 0, 0, 0};
+    for (int64_t e = j->lo; e < j->hi; e++) {
+        uint64_t u, v;
+        rmat_edge(j->g, (uint64_t)e, &u, &v);
+        int du = (int64_t)j->deg_ro[u] > j->theta, dv = (int64_t)j->deg_ro[v] > j->theta;
+        k[(du << 1) | dv]++;  /* original edge u->v */
+        k[(dv << 1) | du]++;  /* its reverse (symmetrize) */
+    }
+    for (int i = 0; i < 4; i++) j->kinds[i] = k[i];
+    return NULL;
+}
+
+int orc_rmat_summary(int scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int randomize, int64_t theta, uint32_t *deg_out, int64_t *d_out,
+                     int64_t *kind_totals) {
+    if (scale < 0 || scale > 40 || edge_factor < 1 || theta < 0) return ORC_EINVAL;
+    rmat_gen g;
+    rmat_gen_init(&g, scale, edge_factor, a, b, c, seed, randomize);
+    memset(deg_out, 0, sizeof(uint32_t) * (size_t)g.n);
+    int T = orc_threads();
+    if (g.m0 < (1 << 16)) T = 1;
+    pthread_t th[256];
+    sum_job jobs[256];
+    int64_t per = (g.m0 + T - 1) / T;
+    for (int pass = 0; pass < 2; pass++) {
+        for (int t = 0; t < T; t++) {
+            memset(&jobs[t], 0, sizeof(sum_job));
+            jobs[t].g = &g; jobs[t].deg = deg_out; jobs[t].deg_ro = deg_out; jobs[t].theta = theta;
+            jobs[t].lo = per * t < g.m0 ? per * t : g.m0;
+            jobs[t].hi = jobs[t].lo + per < g.m0 ? jobs[t].lo + per : g.m0;
+            void *(*fn)(void *) = pass == 0 ? sum_deg_worker : sum_kind_worker;
+            if (T > 1) pthread_create(&th[t], NULL, fn, &jobs[t]);
+            else fn(&jobs[t]);
+        }
+        if (T > 1) for (int t = 0; t < T; t++) pthread_join(th[t], NULL);
+    }
+    int64_t d = 0;
+    for (int64_t v = 0; v < g.n; v++) d += (int64_t)deg_out[v] > theta;
+    *d_out = d;
+    for (int i = 0; i < 4; i++) {
+        kind_totals[i] = 0;
+        for (int t = 0; t < T; t++) kind_totals[i] += jobs[t].kinds[i];
+    }
+    return ORC_OK;
+}
+
 /* hash_randomize_vertices on an arbitrary id array (rmat.py:153-182). */
 int orc_hash_vertices(int64_t n, uint64_t seed, const int64_t *in, int64_t *out,
                       int64_t count) {

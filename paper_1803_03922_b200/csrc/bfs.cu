@@ -861,8 +861,12 @@ static int configure_run(Graph &g, const dbfs_bfs_options &o) {
     return engine;
 }
 
+static void dist_assemble(Graph &g);
+void min_parents_device(Graph &g, int64_t root);
+
 void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     Ctx &ctx = *g.ctx;
+    DBFS_CHECK(o.parent_mode >= 0 && o.parent_mode <= 2, DBFS_EINVAL, "parent_mode must be 0, 1 or 2");
     DBFS_CHECK(o.mode == 0 || o.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
     DBFS_CHECK(0 <= o.source && o.source < g.n, DBFS_ERANGE,
                "source " + std::to_string(o.source) + " out of range [0, " + std::to_string(g.n) + ")");
@@ -1041,6 +1045,11 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     g.last_mode = o.mode;
     g.last_la = o.local_all2all;
     g.last_uq = o.uniquify;
+    if (o.parent_mode == 2) {  // deterministic min-ID tree, after the timed traversal
+        dist_assemble(g);
+        min_parents_device(g, o.source);
+        DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
     if (st) {
         memset(st, 0, sizeof(*st));
         st->iterations = iterations;
@@ -1271,6 +1280,9 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         DBFS_CHECK(0 <= roots[k] && roots[k] < g.n, DBFS_ERANGE,
                    "source " + std::to_string(roots[k]) + " out of range [0, " + std::to_string(g.n) + ")");
     if (count == 0) return;
+    DBFS_CHECK(o0.parent_mode >= 0 && o0.parent_mode <= 2, DBFS_EINVAL, "parent_mode must be 0, 1 or 2");
+    DBFS_CHECK(o0.parent_mode != 2 || !g.dist, DBFS_EINVAL,
+               "min-ID parents (parent_mode 2) are not available in distributed batches; use dbfs_bfs");
     ensure_copy_stream(ctx);
     const bool want_par = parents != nullptr && o0.parent_mode != 0;
     const int64_t nout = batch_output_count(g, local != 0);
@@ -1381,6 +1393,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                                               ctx.stream));
         DBFS_LAUNCHED();
         DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
+        if (o0.parent_mode == 2) min_parents_device(g, src);  // untimed: after the traversal's end event
         if (esc_k && k >= 2) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[k & 1], 0));
         k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k, esc_k);
         DBFS_LAUNCHED();
@@ -1514,6 +1527,13 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     for (auto &e : evs) cudaEventDestroy(e);
     if (aborted && peer) g.peer_state = -1;
     DBFS_CHECK(!aborted, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
+    if (!rerun.empty()) {
+        // a re-run root's result is what the device holds now: run_bfs set
+        // last_source / last_iterations / last_parent_mode for it
+        g.last_truncated = true;
+        g.last_rec.clear();
+        return;
+    }
     g.last_iterations = hi[count - 1].x;
     g.last_truncated = true;
     g.last_rec.clear();
@@ -1566,6 +1586,13 @@ __global__ void k_par_init(const int32_t *__restrict__ lv, int64_t n, unsigned l
         par[v] = lv[v] >= 0 ? 0x7fffffffffffffffull : 0xffffffffffffffffull;
 }
 
+// min-ID tree into the parent output: root -> root, unreached -> -1
+__global__ void k_par_final(const unsigned long long *__restrict__ par, const int32_t *__restrict__ lv, int64_t n,
+                            int64_t root, int64_t *__restrict__ out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = v == root ? root : (lv[v] < 0 ? -1 : (int64_t)par[v]);
+}
+
 static EdgeWalk walk_of(Graph &g, WorkerHost &Wk, int k) {
     EdgeWalk e;
     e.off = g.off_all.p + Wk.base[k];
@@ -1578,12 +1605,13 @@ static EdgeWalk walk_of(Graph &g, WorkerHost &Wk, int k) {
     return e;
 }
 
-void min_parents(Graph &g, int64_t *out) {
-    DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+// Replace the parent output of the last BFS (root) by the min-ID tree
+// (parent_mode 2): kernels only on ctx.stream (a batch enqueues it
+// between roots).  Distributed graphs min-reduce the candidates over ranks.
+void min_parents_device(Graph &g, int64_t root) {
     Ctx &ctx = *g.ctx;
-    dist_assemble(g);
-    DArray<unsigned long long> par;
-    par.alloc(std::max<int64_t>(g.n, 1));
+    DArray<unsigned long long> &par = g.minpar;
+    if (par.n < std::max<int64_t>(g.n, 1)) par.alloc(std::max<int64_t>(g.n, 1));
     const int32_t *lv = g.levels_dev();
     k_par_init<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(lv, g.n, par.p);
     DBFS_LAUNCHED();
@@ -1595,16 +1623,29 @@ void min_parents(Graph &g, int64_t *out) {
             DBFS_LAUNCHED();
         }
     if (g.dist) nccl_allreduce_i64(ctx, (int64_t *)par.p, g.n, 1);  // unsigned -1 stays max; reached < INT64_MAX
-    DBFS_CUDA(cudaMemcpyAsync(out, par.p, 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
-    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
-    int64_t root = g.last_source;
-    out[root] = root;
-    for (int64_t v = 0; v < g.n; v++)
-        if ((uint64_t)out[v] == 0xffffffffffffffffull) out[v] = -1;
+    k_par_final<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(par.p, lv, g.n, root, g.parents_dev());
+    DBFS_LAUNCHED();
 }
 
+void min_parents(Graph &g, int64_t *out) {
+    DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS result on device");
+    DBFS_CHECK(g.last_parent_mode != 0, DBFS_EINVAL, "last BFS ran without parents");
+    Ctx &ctx = *g.ctx;
+    dist_assemble(g);
+    if (g.last_parent_mode != 2) {
+        min_parents_device(g, g.last_source);
+        g.last_parent_mode = 2;
+    }
+    DBFS_CUDA(cudaMemcpyAsync(out, g.parents_dev(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+    DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+// Edge checks of the certificate.  On a symmetric graph every edge is
+// undirected: both ends reached or both unreached, levels at most one apart.
+// A directed graph (do_symmetrize=False, loaded edge lists) keeps only the
+// directed conditions: u reached => v reached, level[v] <= level[u] + 1.
 __global__ void k_validate_edges(EdgeWalk e, const int32_t *__restrict__ lv, const int64_t *__restrict__ par,
-                                 uint8_t *__restrict__ ok, unsigned int *__restrict__ bad) {
+                                 uint8_t *__restrict__ ok, unsigned int *__restrict__ bad, int symmetric) {
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, TW = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const unsigned lane = lane_id();
     unsigned b = 0;
@@ -1614,8 +1655,13 @@ __global__ void k_validate_edges(EdgeWalk e, const int32_t *__restrict__ lv, con
         for (int64_t j = e.off[r] + lane; j < e.off[r + 1]; j += 32) {
             int64_t v = col_gid(e, e.col[j]);
             int32_t lvv = lv[v];
-            if ((lu >= 0) != (lvv >= 0)) b |= 4;
-            else if (lu >= 0 && (lu - lvv > 1 || lvv - lu > 1)) b |= 2;
+            if (symmetric) {
+                if ((lu >= 0) != (lvv >= 0)) b |= 4;
+                else if (lu >= 0 && (lu - lvv > 1 || lvv - lu > 1)) b |= 2;
+            } else if (lu >= 0) {
+                if (lvv < 0) b |= 4;
+                else if (lvv - lu > 1) b |= 2;
+            }
             if (lvv >= 0 && par[v] == u) ok[v] = 1;
         }
     }
@@ -1684,7 +1730,7 @@ int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *paren
         for (int k = 0; k < 4; k++) {
             EdgeWalk e = walk_of(g, Wk, k);
             if (e.rows == 0) continue;
-            k_validate_edges<<<ctx.num_sms * 8, BT, 0, ctx.stream>>>(e, lv, pa, ok.p, bad.p);
+            k_validate_edges<<<ctx.num_sms * 8, BT, 0, ctx.stream>>>(e, lv, pa, ok.p, bad.p, g.symmetric ? 1 : 0);
             DBFS_LAUNCHED();
         }
     if (g.dist) nccl_allreduce_u8_max(ctx, ok.p, g.n);  // tree-edge marks OR-ed over ranks

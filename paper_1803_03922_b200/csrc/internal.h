@@ -292,6 +292,7 @@ struct Graph {
     int64_t hstage_n = 0;
     unsigned *hesc = nullptr;        // pinned: escape counts of the 3 host sets
     DArray<unsigned> esc;            // device escape counters (2 staging buffers)
+    DArray<unsigned long long> minpar;  // min-ID parent candidates (parent_mode 2)
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();

@@ -184,10 +184,8 @@ def run_bfs(pg: PartitionedGraph, opts: BfsOptions) -> BfsRun:
         raise ValueError(f"source {opts.source} out of range [0, {n})")
     levels = np.empty(n, dtype=np.int32)
     parents = np.empty(n, dtype=np.int64) if opts.parents else None
-    st = _bfs_raw(pg, opts, levels, parents)
+    st = _bfs_raw(pg, opts, levels, parents)  # parents="min": the C side replaces the tree by the min-ID one
     elapsed = time.perf_counter() - t0
-    if opts.parents == "min":
-        parents = min_parents(pg)
     per_it, comm = _per_iteration(pg, st.iterations)
     comm.wire_bytes = int(st.wire_bytes)
     insp = {k: {"forward": int(st.inspections[i][0]), "backward": int(st.inspections[i][1])}
@@ -241,16 +239,25 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
     ``stats=True`` also returns the C run-stats struct."""
     if not (0 <= root < pg.n):
         raise ValueError(f"source {root} out of range [0, {pg.n})")
-    opts = BfsOptions(mode=mode, source=int(root), parents="any")
+    if parents not in ("any", "min"):
+        raise ValueError("parents must be 'any' or 'min'")
+    opts = BfsOptions(mode=mode, source=int(root), parents=parents)
     if out is None:
         levels = np.empty(pg.n, dtype=np.int32)
         par = np.empty(pg.n, dtype=np.int64)
     else:
         levels, par = out
+        _check_host_array(levels, np.int32, pg.n, "levels")
+        _check_host_array(par, np.int64, pg.n, "parents")
     st = _bfs_raw(pg, opts, levels, par)
-    if parents == "min":
-        par = min_parents(pg)
     return (levels, par, st) if stats else (levels, par)
+
+
+def _check_host_array(a, dtype, n: int, what: str):
+    """Caller buffers handed to the C side as raw pointers: right dtype, >= n
+    entries, C-contiguous (the library writes 4n / 8n bytes)."""
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.size < n or not a.flags.c_contiguous:
+        raise ValueError(f"{what} must be a contiguous {np.dtype(dtype).name} array of >= {n} entries")
 
 
 def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
@@ -272,6 +279,8 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
     competes for it); ``DBFS_COMPACT=0/1`` overrides.  Per-iteration records
     are not kept.
     ``stats=True`` also returns the per-root C run-stats structs."""
+    if parents not in PARENT_MODES:
+        raise ValueError(f"parents must be one of {list(PARENT_MODES)}")
     roots = np.ascontiguousarray([int(r) for r in roots], dtype=np.int64)
     for r in roots:
         if not (0 <= r < pg.n):
@@ -326,10 +335,20 @@ def validate_bfs_tree(pg: PartitionedGraph, root: int, levels=None, parents=None
     """Graph500 certificate on the GPU.  0 = valid, else a bitmask:
     1 root, 2 edge spans > 1 level, 4 reached-unreached edge, 8 parent level,
     16 tree edge not in E, 32 parent of unreached / missing parent."""
+    if not (0 <= root < pg.n):
+        raise ValueError(f"root {root} out of range [0, {pg.n})")
     rep = ctypes.c_int32()
-    lv = np.ascontiguousarray(levels, dtype=np.int32).ctypes.data_as(_lib.vp) if levels is not None else None
-    pa = np.ascontiguousarray(parents, dtype=np.int64).ctypes.data_as(_lib.vp) if parents is not None else None
-    keep = (levels, parents)
+    lva = pa_ = None
+    if levels is not None:
+        lva = np.ascontiguousarray(levels, dtype=np.int32)
+        if lva.ndim != 1 or lva.size != pg.n:
+            raise ValueError(f"levels must hold exactly n = {pg.n} entries")
+    if parents is not None:
+        pa_ = np.ascontiguousarray(parents, dtype=np.int64)
+        if pa_.ndim != 1 or pa_.size != pg.n:
+            raise ValueError(f"parents must hold exactly n = {pg.n} entries")
+    lv = lva.ctypes.data_as(_lib.vp) if lva is not None else None
+    pa = pa_.ctypes.data_as(_lib.vp) if pa_ is not None else None
     _lib.check(_lib.load().dbfs_validate(pg.handle, int(root), lv, pa, ctypes.byref(rep)), "validate")
-    del keep
+    del lva, pa_  # the converted copies live until the call returned
     return int(rep.value)

@@ -1,6 +1,15 @@
-"""torchrun check of the one-worker-per-GPU NCCL path against the oracle.
+"""torchrun worker of tests/test_gpu_multi.py: the one-worker-per-GPU engines
+(peer persistent kernel over CUDA IPC, NCCL host level loop) against the
+oracle.  Prints "DIST CHECK PASS" on rank 0 when everything agrees.
 
-  torchrun --nproc-per-node N tools/dist_check.py [scale]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+      tests/dist_check_worker.py [scale] [engines|-] [er]
+
+Checked: levels digest, iterations and inspections of every engine x executor
+policy (cost, push) x mode against the oracle's run_bfs (engine.py:98-330 with
+comm.py:75-197 across ranks); the Graph500 certificate of every tree; per-rank
+records and comm accounting (uniquify, local_all2all) equal across engines;
+bfs_batch with full and per-rank (local) outputs; a DPG1 round trip.
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

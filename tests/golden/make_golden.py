@@ -39,6 +39,29 @@ def run_record(run) -> dict:
     return d
 
 
+def c1_roots(g) -> list:
+    """BASELINE configs[0] roots on the scale-16 graph: the 64 Graph500 roots
+    (first 64 distinct vertices with out-degree > 0 drawn from
+    default_rng(0).integers(0, n); the same rule as bench.py's
+    graph500_roots) followed by the reference CLI's own 64 draws
+    (cli.py:151-152, with replacement, degree 0 allowed) not already listed."""
+    deg = np.bincount(g.src, minlength=g.n)
+    rng = np.random.default_rng(0)
+    roots, seen = [], set()
+    while len(roots) < 64:
+        for v in rng.integers(0, g.n, size=4096).tolist():
+            if v not in seen and deg[v] > 0:
+                seen.add(v)
+                roots.append(v)
+                if len(roots) == 64:
+                    break
+    for v in np.random.default_rng(0).integers(0, g.n, size=64).tolist():
+        if v not in seen:
+            seen.add(v)
+            roots.append(v)
+    return [int(v) for v in roots]
+
+
 def main():
     sys.path.insert(0, REF)
     from delegate_bfs import rmat, storage
@@ -68,7 +91,7 @@ def main():
         (12, 21, 16, None, ["auto"], ["4x2"], [17]),
         (12, 0, 16, None, [16], ["2x2"], [3, 100, 999]),
         (11, 9, 8, (0.25, 0.25, 0.25, 0.25), [64, 16], ["1x1", "1x2"], [5, 1000]),
-        (16, 0, 16, None, [16], ["1x1"], [41743, 33497, 20173, 4930]),
+        (16, 0, 16, None, [16], ["1x1"], "C1"),
         (14, 0, 16, None, ["auto"], ["2x2"], [5, 77]),
     ]
     for scale, seed, ef, quads, thetas, shapes, sources in configs:
@@ -77,6 +100,9 @@ def main():
             kw = dict(a=quads[0], b=quads[1], c=quads[2], d_quad=quads[3])
         params = rmat.RmatParams(scale=scale, seed=seed, edge_factor=ef, **kw)
         g = rmat.build_rmat_graph(params)
+        if sources == "C1":
+            sources = c1_roots(g)
+            out["kats"]["c1_roots"] = sources
         gentry = {
             "scale": scale, "seed": seed, "edge_factor": ef,
             "quads": list(quads) if quads else [0.57, 0.19, 0.19, 0.05],

@@ -1,0 +1,121 @@
+"""The reference's acceptance grid, on the GPU, through the reference API.
+
+* Criterion 1 (``/root/reference/pkg/tests/test_acceptance.py:58-85``): RMAT
+  scales 10-16 (seed 0) x shapes 1x1x1 / 1x2x2 / 2x2x2 / 4x2x2 x theta
+  16 / 64 / 256 / auto x bfs / dobfs x local_all2all x uniquify x the 20
+  sources of ``default_rng(scale)``: every ``run_bfs`` level array equals the
+  sequential oracle's (``oracle.py:36-53``; here the C restatement
+  ``O.bfs_levels``, itself pinned to the reference by tests/golden).
+* BASELINE configs[0] (C1): scale 16, theta 16, one partition, all 64
+  Graph500 roots plus the reference CLI's own draws, bfs and dobfs: the whole
+  ``BfsRun.to_dict()`` (levels digest, iterations, per-iteration directions /
+  FV / BV / inspections, comm) equals the reference's recorded run
+  (``tests/golden/golden.json``, made by ``tests/golden/make_golden.py``).
+* Graph build at scale: the device build of RMAT scale 26 (BASELINE configs[2];
+  the builds of configs[3] use the same kernels) against the oracle's streaming
+  restatement of ``partition.py:103-117`` / ``312-318`` -- the whole degree
+  array, d and the kind totals -- and scale 22 with every CSR array
+  byte-compared to the oracle's own partition (``partition.py:295-340``).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from golden_utils import KINDS, load
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = {"1x1x1": (1, 1), "1x2x2": (2, 2), "2x2x2": (4, 2), "4x2x2": (8, 2)}
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_1803_03922_b200 as api
+    from paper_1803_03922_b200 import _lib
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible for a -m gpu test")
+    return api
+
+
+def _resolve_theta(spec, n):
+    from paper_1803_03922_b200.cli import resolve_theta
+    return resolve_theta(spec, n)
+
+
+@pytest.mark.parametrize("scale", list(range(10, 17)))
+def test_criterion_01_oracle_equivalence(api, scale):
+    el = api.build_rmat_graph(api.RmatParams(scale=scale, seed=0))
+    src, dst = O.rmat_edges(scale, seed=0)
+    n = 1 << scale
+    sources = np.random.default_rng(scale).integers(0, n, size=20)
+    ref = {int(s): O.bfs_levels(src, dst, n, int(s)) for s in set(sources.tolist())}
+    runs = mismatches = 0
+    for shape in SHAPES.values():
+        for theta_spec in (16, 64, 256, "auto"):
+            pg = api.partition_graph(el, _resolve_theta(theta_spec, n), api.ClusterShape(*shape))
+            for mode in ("bfs", "dobfs"):
+                for la in (False, True):
+                    for uq in (False, True):
+                        for s in sources:
+                            run = api.run_bfs(pg, api.BfsOptions(mode=mode, source=int(s), local_all2all=la,
+                                                                 uniquify=uq))
+                            runs += 1
+                            mismatches += not np.array_equal(run.levels, ref[int(s)])
+            pg.close()
+    assert runs == 4 * 4 * 2 * 2 * 2 * 20
+    assert mismatches == 0, f"scale {scale}: {mismatches} of {runs} runs differ from the oracle"
+
+
+def test_c1_all_roots_match_reference(api):
+    gold = load()
+    roots = gold["kats"]["c1_roots"]
+    assert len(roots) >= 64
+    g = next(g for g in gold["graphs"] if g["scale"] == 16 and g["seed"] == 0)
+    part = next(p for p in g["partitions"] if p["theta"] == 16 and p["p_rank"] * p["p_gpu"] == 1)
+    want = {(r["source"], r["mode"]): r["report"] for r in part["runs"]}
+    assert {s for s, _ in want} == set(roots)
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=16, seed=0)), 16, api.ClusterShape(1, 1))
+    # the bench's Graph500 root rule picks exactly the first 64 of them
+    from bench import graph500_roots
+    assert graph500_roots(pg.classification.out_degree, 64) == roots[:64]
+    for root in roots:
+        for mode in ("bfs", "dobfs"):
+            got = api.run_bfs(pg, api.BfsOptions(mode=mode, source=root)).to_dict()
+            ref = want[(root, mode)]
+            for key in ("levels_digest", "iterations", "inspections", "b_measured", "per_iteration", "comm"):
+                assert got[key] == ref[key], (root, mode, key)
+    # the reference's benchmark() over the 64 Graph500 roots: same runs kept
+    rep = api.benchmark(pg, roots[:64], api.BfsOptions(mode="dobfs"))
+    assert [r["levels_digest"] for r in rep["runs"]] == [want[(s, "dobfs")]["levels_digest"] for s in roots[:64]
+                                                         if want[(s, "dobfs")]["iterations"] > 1]
+
+
+def test_scale22_csr_equals_oracle_partition(api):
+    scale, theta = 22, 16
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40)), theta,
+                             api.ClusterShape(1, 1))
+    og = O.partition_rmat(scale, theta)
+    assert pg.classification.d == og.d
+    assert pg.kind_totals == og.kind_totals
+    assert np.array_equal(pg.classification.out_degree, og.degrees)
+    assert np.array_equal(pg.classification.delegate_global_ids, og.delegate_global_ids)
+    w, ow = pg.workers[0], og.workers[0]
+    for k in KINDS:
+        csr, ocsr = w.subgraph(k), getattr(ow, k)
+        assert np.array_equal(csr.row_offsets, ocsr.row_offsets), k
+        assert np.array_equal(csr.col_indices, ocsr.col_indices), k
+    pg.close()
+
+
+@pytest.mark.parametrize("scale,theta,scramble", [(26, 16, False), (25, 23, True)])
+def test_large_build_matches_streamed_oracle(api, scale, theta, scramble):
+    """Degrees, delegate count and kind totals of a benchmark-scale device
+    build against the oracle's generator, streamed on the host cores."""
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, scale_cap=40, scramble=scramble)),
+                             theta, api.ClusterShape(1, 1))
+    deg, d, kinds = O.rmat_summary(scale, theta, scramble=scramble)
+    assert pg.classification.d == d
+    assert pg.kind_totals == kinds
+    assert np.array_equal(pg.classification.out_degree, deg)
+    pg.close()
