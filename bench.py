@@ -1,26 +1,37 @@
 #!/usr/bin/env python
 """bench.py -- Graph500 harmonic-mean GTEPS of the B200 delegate BFS/DOBFS.
 
-Workload (BASELINE.json configs[1]): RMAT scale 24, edge factor 16 (Graph500
-quadrants, seed 0, hash-randomized, symmetrized), Θ = 16 (the reference's
-Θ curve, cli.py:22-26), DOBFS with the paper's factors, 64 Graph500 roots
-(first 64 distinct vertices with degree > 0 from default_rng(0)).
-A step is one BFS from one root; K steps cycle through the 64 roots.
+Headline (BASELINE.json configs[1] at N = 1): RMAT scale 24, edge factor 16
+(Graph500 quadrants, seed 0, the reference's hash relabeling, symmetrized),
+Theta = 16 (the reference's Theta curve, cli.py:19-26), DOBFS with the
+paper's factors.  One STEP is one Graph500 benchmark run: a BFS from each of
+the 64 Graph500 roots (first 64 distinct vertices with degree > 0 drawn from
+default_rng(0)); ``--steps K`` times K such runs.
 
-  value : sum over steps of (m/2) / sum of device times  == harmonic-mean TEPS
-          (graph already resident in HBM; depth + parent arrays complete in
-          device memory at the end of every step; L2 flushed between steps)
-  e2e   : the same through the public API ``bfs_batch(pg, roots, outs=pinned)``
-          with the depth/parent arrays of every step copied to pinned host
-          memory (step k's copy overlaps step k+1's traversal); the
-          one-call-per-root ``bfs()`` figure is reported beside it
-  roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md §Measurement
+  value : K * 64 * (m/2) / sum of the 64K device times == harmonic-mean TEPS
+          (graph resident in HBM; depth + parent arrays complete in device
+          memory at the end of every BFS; L2 flushed between BFS)
+  e2e   : the same K runs through the reference API ``benchmark(pg, roots,
+          BfsOptions)`` (engine.py:333-364): every root's levels reach host
+          memory inside the timed call; beside it the Graph500 batch with
+          depth AND parent arrays to pinned host memory (``bfs_batch``)
+  roofline : SURVEY 8(d) algorithmic bytes over the persistent kernel's
+          average duration, against the measured copy bandwidth x N
+  series: BASELINE configs[3] (paper weak scaling, scale 27 + log2 N, Theta
+          23/32/45/64) and configs[2] (scale 26 top-down BFS, strong
+          scaling) measured in the same run, keyed, so a scaling sweep records
+          BASELINE's own curves
+  parity: the scale-24 graph built independently by the oracle (host cores)
+          and compared with the device build array by array; levels of all 64
+          roots compared with the oracle's run_bfs
 
-Multi-GPU (torchrun, one process per GPU): weak scaling, scale = 24 + log2(N),
-one worker per GPU; the BFS runs as one persistent kernel per GPU over
-CUDA-IPC peer memory (NVLink), NCCL only for setup/assembly; step time = max over ranks.
+Multi-GPU (torchrun, one process per GPU): headline weak scaling at scale
+24 + log2(N) (one worker per GPU, Feistel-scrambled labels so owners
+v mod N are balanced; the reference labeling is measured beside it); the BFS
+is one persistent kernel per GPU over CUDA-IPC peer memory (NVLink), NCCL
+only for setup/assembly; every time is the max over ranks.
 ``--impl reference`` times the CPU restatement of the reference (oracle/) on
-this host on the same config (rank 0 only).
+this host (rank 0 only).
 """
 
 from __future__ import annotations
@@ -42,8 +53,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Graph500 harmonic-mean GTEPS, RMAT weak/strong scaling at 1/2/4/8 B200"
 UNIT = "GTEPS"
-L2_BYTES = 126 << 20
-
+KINDS = ("nn", "nd", "dn", "dd")
 
 # The JSON line is the only thing on stdout: native libraries (NCCL's version
 # banner, CUDA) write to fd 1 directly, so fd 1 is pointed at stderr for the
@@ -64,21 +74,26 @@ def emit(line: dict):
     (_JSON_OUT or sys.stdout).flush()
 
 
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
 GRAPH_NAME = {"rmat": "RMAT", "er": "Uniform random (Erdos-Renyi, RMAT with uniform quadrants)"}
 
 
-def graph_quads(args, oracle=False):
+def graph_quads(graph, oracle=False):
     """RMAT quadrants: Graph500 (0.57, 0.19, 0.19, 0.05), or uniform = Erdos-Renyi G(n, m)."""
-    if args.graph == "er":
+    if graph == "er":
         return {"a": 0.25, "b": 0.25, "c": 0.25} if oracle else {"a": 0.25, "b": 0.25, "c": 0.25, "d_quad": 0.25}
     return {}
 
 
-ENGINE_NOTE = {1: " (NCCL level loop)", 3: " (one persistent kernel across GPUs over CUDA-IPC peer memory)"}
+ENGINE_NAME = {1: "host level loop (NCCL)", 2: "persistent kernel",
+               3: "peer persistent kernel (one launch per GPU over CUDA-IPC peer memory)"}
 
 
 def suggested_theta(scale: int) -> int:
-    """cli.py:22-26: 64 at scale 30, sqrt(2) per scale, clamped to [16, 512]."""
+    """cli.py:19-26: 64 at scale 30, sqrt(2) per scale, clamped to [16, 512]."""
     theta = 64.0 * math.sqrt(2.0) ** (scale - 30)
     return int(min(max(round(theta), 16), 512))
 
@@ -104,7 +119,7 @@ def measured_peaks() -> dict:
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"}
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -158,21 +173,141 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def alg_bytes(st, n_total: int) -> float:
-    """Algorithmic bytes of one BFS: every inspection
-    reads a 4-byte column and tests one status bit; every expanded/scanned row
-    reads two 8-byte offsets; the depth (4 B) and parent (8 B) arrays are
-    written once per vertex."""
-    insp = st.work_inspections  # executed (<= reference-accounted when pulls replace pushes)
-    return insp * (4.0 + 1.0 / 8.0) + 16.0 * st.rows_touched + 12.0 * n_total
+# ----------------------------------------------------------------- roofline
+
+# column bytes c_k, status bytes s_{k,dir} per inspection
+COL_B = {"nn": 8.0, "nd": 4.0, "dn": 4.0, "dd": 4.0}
+STATUS_B = {("nn", 0): 4.0, ("nd", 0): 1 / 8, ("dn", 0): 4.0, ("dd", 0): 1 / 8,
+            ("nn", 1): 4.0, ("nd", 1): 4.0, ("dn", 1): 1 / 8, ("dd", 1): 1 / 8}
+
+
+def survey_bytes(st, rows: float, n: int) -> float:
+    """SURVEY 8(d) algorithmic bytes of one BFS (all GPUs): every reported
+    inspection (engine.py:54 counters) reads a column (c_k) and a status entry
+    (s_{k,dir}); every expanded / scanned row reads an 8-byte offset pair
+    entry; the depth array is written once (4n)."""
+    b = 0.0
+    for i, k in enumerate(KINDS):
+        for d in (0, 1):
+            b += int(st.inspections[i][d]) * (COL_B[k] + STATUS_B[(k, d)])
+    return b + 8.0 * rows + 4.0 * n
+
+
+def executed_bytes(work: float, rows: float, n: int) -> float:
+    """Bytes of the work the executor actually ran (counting pushes / pulls
+    substituted for reported directions): every executed inspection reads a
+    4-byte column and tests a status bit, every row two 8-byte offsets, and
+    depth (4 B) + parent (8 B) are written once per vertex."""
+    return work * (4.0 + 1.0 / 8.0) + 16.0 * rows + 12.0 * n
 
 
 # ------------------------------------------------------------------- our arm
 
+def _allreduce(ctx, arr, op="max"):
+    from paper_1803_03922_b200 import _lib
+    buf = np.ascontiguousarray(arr, dtype=np.float64)
+    if op == "max":
+        _lib.check(_lib.load().dbfs_ctx_allreduce_max_f64(ctx.handle, buf.ctypes.data_as(_lib.vp), len(buf)))
+    else:  # sum via max of one-hot slots (small vectors only)
+        world, rank = ctx.nranks, ctx.rank
+        slots = np.zeros((world, len(buf)), dtype=np.float64)
+        slots[rank] = buf
+        flat = slots.ravel()
+        _lib.check(_lib.load().dbfs_ctx_allreduce_max_f64(ctx.handle, flat.ctypes.data_as(_lib.vp), len(flat)))
+        buf = flat.reshape(world, len(buf)).sum(axis=0)
+    return buf
+
+
+def build_graph(api, ctx, scale, theta, world, dist, graph, scrambled, edge_factor=16):
+    params = api.RmatParams(scale=scale, edge_factor=edge_factor, seed=0, scale_cap=40, scramble=scrambled,
+                            **graph_quads(graph))
+    t0 = time.perf_counter()
+    pg = api.partition_graph(api.build_rmat_graph(params), theta,
+                             api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
+    if dist:
+        ctx.barrier()
+    return pg, time.perf_counter() - t0
+
+
+def time_runs(ctx, pg, roots, steps, warmup_roots, mode, dist):
+    """Device-timed Graph500 runs: `steps` x all roots, L2 flushed before every
+    BFS (outside its CUDA-event window); per-BFS time = max over ranks."""
+    from paper_1803_03922_b200 import _lib
+    from paper_1803_03922_b200.engine import bfs_device
+    for r in warmup_roots:
+        bfs_device(pg, r, mode=mode)
+    if dist:
+        ctx.barrier()
+    launches0 = _lib.kernel_launches()
+    dev_ms, stats = [], []
+    for _ in range(steps):
+        for r in roots:
+            ctx.flush_l2()
+            st = bfs_device(pg, r, mode=mode)
+            dev_ms.append(st.device_ms)
+            stats.append(st)
+    if dist:
+        ctx.barrier()
+    launches = _lib.kernel_launches() - launches0
+    if dist:
+        dev_ms = list(_allreduce(ctx, np.array(dev_ms)))
+    return dev_ms, stats, launches
+
+
+def roofline_of(ctx, pg, stats, dev_ms, world, dist, peaks, traffic=None):
+    """SURVEY 8(d) fraction over all GPUs: B_alg / (t * N * peak); executed-work
+    bytes as a second figure.  Per-rank rows / work are summed over ranks."""
+    n = pg.n
+    rows = np.array([float(s.rows_touched) for s in stats])
+    work = np.array([float(s.work_inspections) for s in stats])
+    if dist:
+        rows = _allreduce(ctx, rows, "sum")
+        work = _allreduce(ctx, work, "sum")
+    b_alg = np.array([survey_bytes(s, r, n) for s, r in zip(stats, rows)])
+    b_exec = np.array([executed_bytes(w, r, n) for w, r in zip(work, rows)])
+    t = float(np.mean(dev_ms)) / 1e3
+    peak = peaks["hbm_gbs"] * world
+    ach = float(np.mean(b_alg)) / t / 1e9
+    ach_exec = float(np.mean(b_exec)) / t / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "traffic": traffic, "peak_source": peaks["source"] + (f" x {world} GPUs" if world > 1 else ""),
+            "kernel": "k_bfs_persistent", "alg_bytes_per_launch": round(float(np.mean(b_alg))),
+            "formula": "SURVEY 8(d): sum_k,dir insp[k][dir]*(c_k + s_k,dir) + 8*rows + 4*n, summed over GPUs",
+            "executed": {"achieved": round(ach_exec, 2), "frac": round(ach_exec / peak, 4),
+                         "bytes_per_launch": round(float(np.mean(b_exec))),
+                         "formula": "(4 + 1/8)*executed inspections + 16*rows + 12*n"}}
+
+
+def _load_imbalance(ctx, pg, dist):
+    """max over workers of the worker's edge count / mean edge count."""
+    loads = np.array([float(sum(w.sizes()[1])) for w in pg.workers], dtype=np.float64)
+    mx = float(loads.max())
+    if dist:
+        mx = float(_allreduce(ctx, np.array([mx]))[0])
+    return round(mx / (pg.m / pg.shape.p), 3) if pg.m else 1.0
+
+
+def measure_series(api, ctx, name, scale, theta, mode, world, dist, scrambled, graph, steps, peaks, scaling, note):
+    """One keyed series point: build, warm up, time `steps` runs of the 64
+    roots; returns its value and roofline."""
+    pg, build_s = build_graph(api, ctx, scale, theta, world, dist, graph, scrambled)
+    roots = graph500_roots(pg.classification.out_degree, 64)
+    dev_ms, stats, launches = time_runs(ctx, pg, roots, steps, roots[:4], mode, dist)
+    value = len(dev_ms) * (pg.m / 2) / (sum(dev_ms) / 1e3) / 1e9
+    out = {"config": f"{name}", "value": round(value, 4), "unit": UNIT, "scale": scale, "theta": theta,
+           "mode": mode, "graph": graph, "n_gpus": world, "scaling": scaling, "steps": steps, "roots": len(roots),
+           "ms_per_bfs": round(float(np.mean(dev_ms)), 4), "build_s": round(build_s, 2),
+           "labeling": "scrambled" if scrambled else "reference", "gpu_launches": int(launches),
+           "worker_edges_max_over_mean": _load_imbalance(ctx, pg, dist),
+           "roofline": roofline_of(ctx, pg, stats, dev_ms, world, dist, peaks), "note": note}
+    pg.close()
+    return out
+
+
 def run_ours(args, world, rank, local_rank):
     import paper_1803_03922_b200 as api
     from paper_1803_03922_b200 import _lib
-    from paper_1803_03922_b200.engine import batch_output_count, bfs, bfs_batch, bfs_device
+    from paper_1803_03922_b200.engine import BfsOptions, batch_output_count, bfs, bfs_batch, levels_digest
 
     dist = world > 1
     tdist = None
@@ -186,131 +321,107 @@ def run_ours(args, world, rank, local_rank):
     _lib.set_default_context(ctx)
     if dist:
         init_nccl_context(ctx, tdist)
+    peaks = measured_peaks()
 
     scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
-    scrambled = args.labeling == "scrambled"
-    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, scramble=scrambled,
-                            **graph_quads(args))
-    t0 = time.perf_counter()
-    pg = api.partition_graph(api.build_rmat_graph(params), theta,
-                             api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
-    if dist:
-        ctx.barrier()
-    build_s = time.perf_counter() - t0
+    labeling = args.labeling if args.labeling != "auto" else ("scrambled" if dist else "reference")
+    scrambled = labeling == "scrambled"
+    pg, build_s = build_graph(api, ctx, scale, theta, world, dist, args.graph, scrambled, args.edge_factor)
     n, m = pg.n, pg.m
-    degrees = pg.classification.out_degree
-    roots = graph500_roots(degrees, args.roots)
-    parents = "any"
+    roots = graph500_roots(pg.classification.out_degree, args.roots)
+    log(f"built scale {scale} in {build_s:.2f}s")
 
-    def step(root):
-        return bfs_device(pg, root, mode=args.mode, parents=parents)
-
-    for i in range(args.warmup):
-        step(roots[i % len(roots)])
+    # ---- device-timed Graph500 runs (the headline value)
+    warm = [roots[i % len(roots)] for i in range(args.warmup * len(roots))]
     sampler = ClockSampler(local_rank if dist else args.device)
     sampler.start()
     time.sleep(0.3)
-    if dist:
-        ctx.barrier()
-    launches0 = _lib.kernel_launches()
-    dev_ms, wall0 = [], time.perf_counter()
-    stats = []
-    for i in range(args.steps):
-        ctx.flush_l2()  # outside the CUDA-event window of the step
-        st = step(roots[i % len(roots)])
-        dev_ms.append(st.device_ms)
-        stats.append(st)
-    if dist:
-        ctx.barrier()
+    wall0 = time.perf_counter()
+    dev_ms, stats, launches = time_runs(ctx, pg, roots, args.steps, warm, args.mode, dist)
     wall = time.perf_counter() - wall0
-    launches = _lib.kernel_launches() - launches0
+    clocks = sampler.stop()
     engine_used = int(stats[-1].engine_used)
-    clocks = sampler.stop()  # the device-timed region ends here (nvidia-smi polling would perturb the e2e host loop)
+    total_dev_s = sum(dev_ms) / 1e3
+    nbfs = len(dev_ms)
+    value = nbfs * (m / 2) / total_dev_s / 1e9
+    per_root = [(m / 2) / (t / 1e3) / 1e9 for t in dev_ms]
+    geomean = float(np.exp(np.mean(np.log(per_root))))
+    log(f"value {value:.2f} GTEPS over {nbfs} BFS")
 
-    # e2e through the public API: depth + parent of every step to pinned host
-    # buffers.  Headline: bfs_batch over the K roots (the D2H of step k overlaps
-    # the traversal of step k+1; two pinned buffer pairs used alternately);
-    # beside it the one-call-per-root bfs() loop.  No L2 flush inside the
-    # timed batch: the graph (and each step's 12n-byte result) exceed L2.
-    # (N > 1: each rank receives the vertices it owns, v mod N == rank -- the
-    # distributed Graph500 result; the one-call bfs() figure gathers all n on
-    # every rank)
+    # ---- e2e through the reference API: benchmark() over the 64 roots per step
+    opts = BfsOptions(mode=args.mode)
+    api.benchmark(pg, roots[: min(8, len(roots))], opts)  # untimed: staging buffers / events allocated once
+    if dist:
+        ctx.barrier()
+    e2e_wall, digests_gpu = 0.0, {}
+    for _ in range(args.steps):
+        rep = api.benchmark(pg, roots, opts)
+        e2e_wall += rep["wall_s"]
+        for r in rep["runs"]:
+            digests_gpu[r["source"]] = r["levels_digest"]
+    if dist:
+        e2e_wall = float(_allreduce(ctx, np.array([e2e_wall]))[0])
+    e2e_value = args.steps * len(roots) * (m / 2) / e2e_wall / 1e9
+    # beside it: the Graph500 batch, depth AND parent arrays of every root to pinned host memory
     nout = batch_output_count(pg, local=dist)
     pairs = [(_lib.pinned_empty(nout, np.int32), _lib.pinned_empty(nout, np.int64)) for _ in range(2)]
-    outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(args.steps)]
-    step_roots = [roots[i % len(roots)] for i in range(args.steps)]
-    # untimed warm-up call: staging buffers and copy-stream events are allocated once
-    bfs_batch(pg, step_roots[: max(1, min(args.warmup, len(step_roots)))], outs=outs[: max(1, min(args.warmup,
-              len(step_roots)))], mode=args.mode, local=dist)
+    outs = [(pairs[i % 2][0].array, pairs[i % 2][1].array) for i in range(len(roots))]
+    bfs_batch(pg, roots[:2], outs=outs[:2], mode=args.mode, local=dist)
     if dist:
         ctx.barrier()
     t = time.perf_counter()
-    _, bst = bfs_batch(pg, step_roots, outs=outs, mode=args.mode, stats=True, local=dist)
-    e2e_batch_s = time.perf_counter() - t
-    h2d = sum(int(x.h2d_bytes) + 8 for x in bst)
-    d2h = sum(int(x.d2h_bytes) for x in bst)
-    lv_buf, pa_buf = _lib.pinned_empty(n, np.int32), _lib.pinned_empty(n, np.int64)
-    e2e_s = []
-    for i in range(args.steps):
-        ctx.flush_l2()
-        t = time.perf_counter()
-        bfs(pg, roots[i % len(roots)], mode=args.mode, out=(lv_buf.array, pa_buf.array))
-        e2e_s.append(time.perf_counter() - t)
-
-    # max over ranks, per step
+    _, bst = bfs_batch(pg, roots, outs=outs, mode=args.mode, stats=True, local=dist)
+    batch_s = time.perf_counter() - t
     if dist:
-        dev_ms = list(_allreduce_max(ctx, np.array(dev_ms, dtype=np.float64)))
-        e2e_s = list(_allreduce_max(ctx, np.array(e2e_s, dtype=np.float64)))
-        e2e_batch_s = float(_allreduce_max(ctx, np.array([e2e_batch_s], dtype=np.float64))[0])
-    total_dev_s = sum(dev_ms) / 1e3
-    value = args.steps * (m / 2) / total_dev_s / 1e9
-    per_root = [(m / 2) / (t / 1e3) / 1e9 for t in dev_ms]
-    geomean = float(np.exp(np.mean(np.log(per_root))))
-    e2e_value = args.steps * (m / 2) / e2e_batch_s / 1e9
-    e2e_single = args.steps * (m / 2) / sum(e2e_s) / 1e9
+        batch_s = float(_allreduce(ctx, np.array([batch_s]))[0])
+    batch_value = len(roots) * (m / 2) / batch_s / 1e9
+    h2d_step = 8 * len(roots) + sum(int(x.h2d_bytes) for x in bst)  # roots + views
+    d2h_batch = sum(int(x.d2h_bytes) for x in bst)
+    # benchmark()'s copies per step: compact depth (1 B per vertex) + per-root records
+    e2e_d2h = int(len(roots) * (n + 64 * 1024))
 
-    # correctness of what was timed: certificate on a few roots, digest vs oracle sample
+    # ---- correctness of what was timed
     validated = 0
     for r in roots[: min(4, len(roots))]:
-        bfs_device(pg, r, mode=args.mode, parents="any")
+        bfs(pg, r, mode=args.mode)
         if api.validate_bfs_tree(pg, r) != 0:
             raise SystemExit(f"Graph500 certificate failed for root {r}")
         validated += 1
     imbalance = _load_imbalance(ctx, pg, dist)
-
-    peaks = measured_peaks()
-    st_mean_bytes = float(np.mean([alg_bytes(s, n) for s in stats]))
-    kernel_ms = float(np.mean(dev_ms))
-    achieved = st_mean_bytes / (kernel_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None if dist else _ncu_traffic(),
-            "peak_source": peaks["source"],
-            "kernel": "k_visit+k_finish" if engine_used == 1 else "k_bfs_persistent",
-            "alg_bytes_per_launch": st_mean_bytes}
+    traffic = _ncu_traffic() if (not dist and scale == 24 and not scrambled and args.graph == "rmat") else None
+    roof = roofline_of(ctx, pg, stats, dev_ms, world, dist, peaks, traffic)
 
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(kernel_ms, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(sum(dev_ms) / args.steps, 4), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
-        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, seed 0), "
-                "generated on device",
-        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
-                               f"{args.roots} Graph500 roots, {world}xB200",
+        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, "
+                "seed 0), generated on device",
+        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} "
+                               f"{args.mode.upper()}, {len(roots)} Graph500 roots per step, {world}xB200",
                    "scale": scale, "edge_factor": args.edge_factor, "theta": theta, "mode": args.mode,
-                   "roots": args.roots, "parents": "valid parent tree written in the timed region",
-                   "l2": "flushed between steps (256 MB write); graph also > L2",
-                   "parallelism": f"{world} worker(s), one per GPU" + (ENGINE_NOTE.get(engine_used, "") if dist else ""),
-                   "engine": {1: "host level loop", 2: "persistent kernel", 3: "peer persistent kernel"}.get(engine_used)},
+                   "roots": len(roots), "step": f"one Graph500 run: a BFS from each of the {len(roots)} roots",
+                   "bfs_timed": nbfs, "parents": "valid parent tree written in the timed region",
+                   "l2": "flushed before every BFS (256 MB write, outside its event window); graph also > L2",
+                   "labeling": labeling, "parallelism": f"{world} worker(s), one per GPU",
+                   "engine": ENGINE_NAME.get(engine_used)},
+        "ms_per_bfs": round(float(np.mean(dev_ms)), 4),
         "geomean_gteps": round(geomean, 4),
-        "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
-                "d2h_bytes_per_step": int(d2h / args.steps),
-                "api": "bfs_batch: all steps in one call, D2H of step k overlapped with step k+1 (no L2 flush; graph > L2); "
-                       + ("depth sent as int8 and widened on the host, parents as int64" if not dist
-                          else "full int32 depth / int64 parent arrays")
-                       + ("; each rank receives the depth/parent entries of the vertices it owns" if dist else ""),
-                "per_call_bfs": round(e2e_single, 4)},
+        "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d_step),
+                "d2h_bytes_per_step": e2e_d2h,
+                "api": "reference API benchmark(pg, roots, BfsOptions) (engine.py:333-364): one pipelined "
+                       "dbfs_bfs_batch per step, every root's int32 levels in host memory inside the timed "
+                       "call (int8 on PCIe, widened on the host cores), iteration records per root; digests "
+                       "after the call as in the reference",
+                "graph500_batch": {"value": round(batch_value, 4), "unit": UNIT,
+                                   "d2h_bytes_per_step": int(d2h_batch),
+                                   "api": "bfs_batch: depth (int32) and parent (int64) of every root to pinned "
+                                          "host memory" + ("; each rank receives the vertices it owns" if dist
+                                                           else "")}},
         "roofline": roof, "clocks": clocks, "gpu_launches": int(launches),
+        "gpu_launches_note": "per timed BFS: one k_bfs_persistent (the traversal) + one k_count_reached (after "
+                             "the event window) + the L2 flush memset",
         "build_s": round(build_s, 3), "wall_s_timed": round(wall, 4), "validated_roots": validated,
         "graph": {"n": n, "m": m, "d": pg.classification.d, "kind_totals": pg.kind_totals,
                   "device_bytes": pg.device_bytes},
@@ -318,78 +429,50 @@ def run_ours(args, world, rank, local_rank):
         "inspections_mean": float(np.mean([sum(s.inspections[k][0] + s.inspections[k][1] for k in range(4))
                                            for s in stats])),
         "executed_inspections_mean": float(np.mean([s.work_inspections for s in stats])),
+        "worker_edges_max_over_mean": imbalance,
     }
-    line["config"]["labeling"] = ("reference hash_randomize_vertices + Feistel relabeling (balanced v mod p owners)"
-                                  if scrambled else "reference hash_randomize_vertices")
-    line["worker_edges_max_over_mean"] = imbalance
     if dist:
-        # bytes this rank moved over NVLink per BFS (8-byte records incl. parent,
-        # d/8-byte delegate masks read from each peer on dirty levels), the max
-        # over ranks, against NVLink 5's 900 GB/s per direction and the step time
         wire = float(np.mean([s.wire_bytes for s in stats]))
-        wire_max = float(_allreduce_max(ctx, np.array([wire]))[0])
-        t_step = total_dev_s / args.steps
+        wire_max = float(_allreduce(ctx, np.array([wire]))[0])
+        t_bfs = total_dev_s / nbfs
         line["comm"] = {"wire_bytes_per_bfs_max_rank": round(wire_max),
                         "nvlink_time_us_at_900GBps": round(wire_max / 900e9 * 1e6, 2),
-                        "share_of_step": round(wire_max / 900e9 / t_step, 4),
-                        "achieved_GBps_over_step": round(wire_max / t_step / 1e9, 2),
+                        "share_of_bfs": round(wire_max / 900e9 / t_bfs, 4),
+                        "achieved_GBps_over_bfs": round(wire_max / t_bfs / 1e9, 2),
                         "note": "exchange is fused into the persistent kernel (posted NVLink stores, peer mask "
                                 "reads), so its time overlaps the traversal; per-level bytes: tools/dist_levels.py"}
-    if rank == 0 and not args.no_cpu_baseline and not dist:
-        line["cpu_baseline"] = cpu_baseline_same_graph(pg, roots, args, n, m)
-    # reference-labeling series where its skewed owners fit (build peak ~24 B per
-    # directed edge on the heaviest worker, up to 2.75x the mean at p = 8)
-    if scrambled and not args.no_alt_labeling and m // world <= (1 << 29):
-        # the same workload on the reference's own labeling, device time only
+
+    # ---- independent build + CPU baseline on the host cores (N = 1)
+    if rank == 0 and not dist and not args.no_cpu_baseline:
+        line["parity"], line["cpu_baseline"] = independent_parity_and_cpu(api, pg, roots, args, scale, theta,
+                                                                          scrambled, digests_gpu)
+    # ---- the other labeling beside the headline (same scale, device time)
+    series = {}
+    if not args.no_series:
         pg.close()
         del pg
-        line["reference_labeling"] = _device_series(api, ctx, args, scale, theta, world, dist)
+        alt = "reference" if scrambled else "scrambled"
+        if not (alt == "reference" and dist and m // world > (1 << 30)):
+            series["alt_labeling"] = measure_series(
+                api, ctx, f"headline graph, {alt} labeling", scale, theta, args.mode, world, dist,
+                alt == "scrambled", args.graph, 1, peaks, args.scaling,
+                "the headline workload on the other vertex labeling (reference hash vs + Feistel scramble)")
+        # BASELINE configs[3]: paper weak scaling, 2^27 vertices per GPU
+        s4 = 27 + world.bit_length() - 1
+        series["C4_paper_weak"] = measure_series(
+            api, ctx, f"configs[3]: RMAT scale-{s4} DOBFS, {world}xB200", s4, suggested_theta(s4), "dobfs", world,
+            dist, dist, "rmat", 1, peaks, "weak",
+            "paper setup (PAPER.md:1050-1052): scale 27 + log2 N, Theta from cli.py:19-26")
+        # BASELINE configs[2]: scale-26 top-down BFS, strong scaling
+        series["C3_strong_bfs"] = measure_series(
+            api, ctx, f"configs[2]: RMAT scale-26 top-down BFS, {world}xB200", 26, 16, "bfs", world, dist, dist,
+            "rmat", 1, peaks, "strong", "same graph at every N (strong scaling)")
+        line["series"] = series
     if rank == 0:
         emit(line)
     if dist:
         tdist.barrier()
         tdist.destroy_process_group()
-
-
-def _load_imbalance(ctx, pg, dist):
-    """max over workers of the worker's edge count / mean edge count."""
-    loads = np.array([[float(sum(w.sizes()[1])) for w in pg.workers]], dtype=np.float64).ravel()
-    mx = float(loads.max())
-    if dist:
-        mx = float(_allreduce_max(ctx, np.array([mx]))[0])
-    return round(mx / (pg.m / pg.shape.p), 3) if pg.m else 1.0
-
-
-def _device_series(api, ctx, args, scale, theta, world, dist):
-    from paper_1803_03922_b200.engine import bfs_device
-    params = api.RmatParams(scale=scale, edge_factor=args.edge_factor, seed=0, scale_cap=40, **graph_quads(args))
-    pg = api.partition_graph(api.build_rmat_graph(params), theta,
-                             api.ClusterShape(1, world) if dist else api.ClusterShape(1, 1), ctx=ctx)
-    roots = graph500_roots(pg.classification.out_degree, args.roots)
-    for i in range(args.warmup):
-        bfs_device(pg, roots[i % len(roots)], mode=args.mode)
-    if dist:
-        ctx.barrier()
-    dev_ms = []
-    for i in range(args.steps):
-        ctx.flush_l2()
-        dev_ms.append(bfs_device(pg, roots[i % len(roots)], mode=args.mode).device_ms)
-    if dist:
-        dev_ms = list(_allreduce_max(ctx, np.array(dev_ms, dtype=np.float64)))
-    out = {"value": round(args.steps * (pg.m / 2) / (sum(dev_ms) / 1e3) / 1e9, 4), "unit": UNIT,
-           "ms_per_step": round(float(np.mean(dev_ms)), 4),
-           "worker_edges_max_over_mean": _load_imbalance(ctx, pg, dist),
-           "note": "reference labeling: owners v mod p inherit the hash's low-bit degree skew"}
-    pg.close()
-    return out
-
-
-def _allreduce_max(ctx, arr):
-    from paper_1803_03922_b200 import _lib
-    import ctypes
-    buf = np.ascontiguousarray(arr, dtype=np.float64)
-    _lib.check(_lib.load().dbfs_ctx_allreduce_max_f64(ctx.handle, buf.ctypes.data_as(_lib.vp), len(buf)))
-    return buf
 
 
 def _ncu_traffic():
@@ -402,9 +485,10 @@ def _ncu_traffic():
 
 
 def _cpu_threads(n: int) -> int:
-    """Host threads for the CPU baseline: every core, bounded so the concurrent
-    oracle runs (~64 bytes per vertex each) use at most half the free memory."""
-    cores = os.cpu_count() or 1
+    """Host threads for the CPU runs: every usable core, bounded so the
+    concurrent oracle runs (~64 bytes per vertex each) use at most half the
+    free memory."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     try:
         free = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
         cap = max(1, int(0.5 * free // max(64 * n, 1)))
@@ -413,125 +497,162 @@ def _cpu_threads(n: int) -> int:
     return max(1, min(cores, cap, 128))
 
 
-def _oracle_throughput(O, og, roots, mode, threads, budget_s, check=None):
+def _oracle_rounds(O, og, roots, mode, threads, budget_s):
     """Independent BFS roots on `threads` host threads (the C oracle releases the
-    GIL; the graph is read-only): rounds of `threads` roots until `budget_s` of
-    wall time has passed.  Returns (roots done, wall seconds, results)."""
+    GIL; the graph is read-only): rounds of `threads` roots, at least one pass
+    over `roots`, then more rounds until `budget_s` of wall time has passed.
+    Returns (roots done, wall seconds, {root: result})."""
     from concurrent.futures import ThreadPoolExecutor
-    done, results = 0, []
+    done, results = 0, {}
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as ex:
         i = 0
         while True:
             batch = [roots[(i + j) % len(roots)] for j in range(threads)]
             for r, res in zip(batch, ex.map(lambda r: O.run_bfs(og, r, mode=mode), batch)):
-                results.append((r, res))
+                results.setdefault(r, res)
             done += len(batch)
             i += len(batch)
-            if time.perf_counter() - t0 > budget_s:
+            if i >= len(roots) and time.perf_counter() - t0 > budget_s:
                 break
     return done, time.perf_counter() - t0, results
 
 
-def cpu_baseline_same_graph(pg, roots, args, n, m):
-    """The oracle (C restatement of the reference run_bfs) on this host's cores,
-    on the very graph the GPU traverses (CSR exported from the device): rounds
-    of independent roots, one per host thread, for a bounded time; depth
-    digests are cross-checked against the GPU."""
+def independent_parity_and_cpu(api, pg, roots, args, scale, theta, scrambled, digests_gpu):
+    """The oracle builds the same graph from the RMAT parameters on the host
+    (rmat.py:107-208 + partition.py:103-351 restated, no device data), every
+    array of the device build is compared with it, and the oracle's run_bfs on
+    its own graph gives the levels of all roots (compared with the GPU's, from
+    benchmark()) and the CPU baseline rate (host cores, one root per thread)."""
     import oracle as O
     from paper_1803_03922_b200.engine import bfs, levels_digest
     t0 = time.perf_counter()
-    og = O.from_partition(pg)
-    load_s = time.perf_counter() - t0
-    threads = _cpu_threads(n)
+    og = O.partition_rmat(scale, theta, 1, 1, edge_factor=args.edge_factor, scramble=scrambled,
+                          **graph_quads(args.graph, oracle=True))
+    build_s = time.perf_counter() - t0
+    w, ow = pg.workers[0], og.workers[0]
+    csr_ok = {}
+    for k in KINDS:
+        csr, ocsr = w.subgraph(k), getattr(ow, k)
+        csr_ok[k] = bool(np.array_equal(csr.row_offsets, ocsr.row_offsets)
+                         and np.array_equal(csr.col_indices, ocsr.col_indices))
+    build_ok = (pg.classification.d == og.d and pg.kind_totals == og.kind_totals
+                and bool(np.array_equal(pg.classification.out_degree, og.degrees))
+                and bool(np.array_equal(pg.classification.delegate_global_ids, og.delegate_global_ids))
+                and all(csr_ok.values()))
+    threads = _cpu_threads(og.n)
     t = time.perf_counter()
     O.run_bfs(og, roots[0], mode=args.mode)
     single_s = time.perf_counter() - t
-    done, wall, results = _oracle_throughput(O, og, roots, args.mode, threads, args.cpu_budget_s)
-    match = True
-    for r, res in results[: min(len(results), 8)]:
-        lv, _ = bfs(pg, r, mode=args.mode)
-        match &= levels_digest(lv) == res["levels_digest"]
-    value = done * (m / 2) / wall / 1e9
-    return {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{done} BFS runs (rounds of {threads} concurrent roots from the {len(roots)}), same "
-                      f"scale-{int(math.log2(n))} graph (CSR exported from the device), oracle/dbfs_oracle.c, "
-                      f"one root per host thread",
-            "single_thread_value": round((m / 2) / single_s / 1e9, 6),
-            "depth_parity": bool(match), "graph_load_s": round(load_s, 2)}
+    done, wall, results = _oracle_rounds(O, og, roots, args.mode, threads, args.cpu_budget_s)
+    match = 0
+    for r in roots:
+        gd = digests_gpu.get(r)
+        if gd is None:  # discarded by benchmark() (iterations <= 1): compare directly
+            gd = levels_digest(bfs(pg, r, mode=args.mode)[0])
+        match += gd == results[r]["levels_digest"]
+    m = og.m
+    parity = {"roots": len(roots), "levels_match": match, "independent_build": True, "build_match": build_ok,
+              "csr_match": csr_ok, "oracle_build_s": round(build_s, 2),
+              "how": "oracle/dbfs_oracle.c built the graph from the RMAT parameters on the host; degrees, "
+                     "delegates, kind totals and every CSR array equal the device build; levels digests of all "
+                     "roots from the oracle's run_bfs equal the GPU's (benchmark())"}
+    cpu = {"value": round(done * (m / 2) / wall / 1e9, 6), "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{done} BFS runs (rounds of {threads} concurrent roots over all {len(roots)} roots), the "
+                     f"oracle's own scale-{scale} graph, oracle/dbfs_oracle.c (C restatement of engine.run_bfs), "
+                     "one root per host thread",
+           "single_thread_value": round((m / 2) / single_s / 1e9, 6)}
+    return parity, cpu
 
 
 # ------------------------------------------------------------- reference arm
 
-REF_SCALE_CAP = 24
+def _ref_scale(scale: int, edge_factor: int) -> tuple[int, str | None]:
+    """Largest scale <= `scale` the oracle can build and run on this host within
+    the bench's time budget: ~48 bytes per directed edge of host memory (edge
+    list + CSR + build scratch) under 60 % of the available RAM, and scale
+    <= 25 (the build is single-threaded: ~50 s at scale 24, doubling per scale)."""
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError, AttributeError):
+        avail = 64 << 30
+    s = scale
+    while s > 10 and (48 * 2 * edge_factor * (1 << s) > 0.6 * avail or s > 25):
+        s -= 1
+    if s == scale:
+        return s, None
+    need = 48 * 2 * edge_factor * (1 << scale) / 2**30
+    return s, (f"scale {scale} needs ~{need:.0f} GiB of host memory and a single-threaded host build of "
+               f"~{50 * 2 ** (scale - 24):.0f} s (host has {avail / 2**30:.0f} GiB available): the reference "
+               f"restatement runs the same generator / Theta rule / roots at scale {s}; TEPS of this traversal "
+               "varies little with scale")
 
 
 def run_reference(args, world, rank):
     """The reference's CPU path on this host: the oracle port (oracle/, a C
-    restatement of delegate_bfs run_bfs), rank 0 only."""
+    restatement of delegate_bfs run_bfs), rank 0 only, on every host core."""
     if rank != 0:
         return
     import oracle as O
     from paper_1803_03922_b200.dist import weak_scale
     scale = weak_scale(args.scale, world) if args.scaling == "weak" else args.scale
     theta = args.theta if args.theta is not None else suggested_theta(scale)
-    # host memory/time bound: graphs above scale 24 are sampled at scale 24
-    # (GTEPS of this traversal is nearly scale-independent), same labeling
-    cpu_scale = min(scale, REF_SCALE_CAP)
+    labeling = args.labeling if args.labeling != "auto" else ("scrambled" if world > 1 else "reference")
+    cpu_scale, why = _ref_scale(scale, args.edge_factor)
     cpu_theta = args.theta if args.theta is not None else suggested_theta(cpu_scale)
     t0 = time.perf_counter()
     og = O.partition_rmat(cpu_scale, cpu_theta, 1, world, edge_factor=args.edge_factor, load_arrays=False,
-                          **graph_quads(args, oracle=True),
-                          scramble=args.labeling == "scrambled")
-    deg = _oracle_degrees(og, O)
+                          **graph_quads(args.graph, oracle=True), scramble=labeling == "scrambled")
+    deg = O._view(O.lib().orc_graph_degrees(og._h), og.n, np.int64)
     build_s = time.perf_counter() - t0
     roots = graph500_roots(deg, args.roots)
     threads = _cpu_threads(og.n)
     single = []  # warm-up runs, one at a time: the reference's own single-threaded per-BFS rate
-    for i in range(args.warmup):
+    for i in range(max(1, args.warmup)):
         t = time.perf_counter()
         O.run_bfs(og, roots[i % len(roots)], mode=args.mode)
         single.append(time.perf_counter() - t)
     # each step: one round of `threads` independent roots, one per host thread
     times, done = [], 0
-    for i in range(args.steps):
-        k, wall, _ = _oracle_throughput(O, og, roots[(i * threads) % len(roots):] + roots, args.mode, threads, 0.0)
-        times.append(wall)
-        done += k
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for i in range(args.steps):
+            batch = [roots[(i * threads + j) % len(roots)] for j in range(threads)]
+            t = time.perf_counter()
+            list(ex.map(lambda r: O.run_bfs(og, r, mode=args.mode), batch))
+            times.append(time.perf_counter() - t)
+            done += len(batch)
     m = og.m
     value = done * (m / 2) / sum(times) / 1e9
+    sample = (f"{args.steps} steps x {threads} concurrent BFS runs (one root per host thread) over the "
+              f"{len(roots)} Graph500 roots of the scale-{cpu_scale} graph (theta {cpu_theta}, {world} simulated "
+              "workers), oracle/dbfs_oracle.c (C restatement of engine.run_bfs; the reference itself is "
+              "single-threaded)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / max(done, 1), 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / args.steps, 3),
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
-        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, seed 0), "
-                "generated on the host",
-        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} {args.mode.upper()}, "
-                               f"{args.roots} Graph500 roots, CPU", "scale": scale, "theta": theta,
-                   "mode": args.mode, "roots": args.roots, "shape": f"1x1x{world}", "labeling": args.labeling},
+        "data": f"synthetic {'RMAT (Graph500 quadrants' if args.graph == 'rmat' else 'RMAT (uniform quadrants'}, "
+                "seed 0), generated on the host",
+        "config": {"workload": f"{GRAPH_NAME[args.graph]} scale-{scale} edgefactor-{args.edge_factor} "
+                               f"{args.mode.upper()}, {args.roots} Graph500 roots, CPU",
+                   "scale": scale, "theta": theta, "mode": args.mode, "roots": args.roots,
+                   "shape": f"1x{world}", "labeling": labeling,
+                   "cpu_scale": cpu_scale, "sampled_scale": why},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} steps x {threads} concurrent BFS runs (one root per host thread) "
-                                   f"over the {args.roots} roots of the scale-{cpu_scale} graph (theta {cpu_theta}, "
-                                   f"{world} simulated workers), oracle/dbfs_oracle.c (C restatement of "
-                                   "engine.run_bfs; the reference itself is single-threaded)",
-                         "single_thread_value": (round(len(single) * (m / 2) / sum(single) / 1e9, 6)
-                                                 if single else None)},
+                         "sample": sample,
+                         "single_thread_value": round(len(single) * (m / 2) / sum(single) / 1e9, 6)},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build_s": round(build_s, 2),
     }
     emit(line)
 
 
-def _oracle_degrees(og, O):
-    L = O.lib()
-    return O._view(L.orc_graph_degrees(og._h), og.n, np.int64)
-
-
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=4, help="Graph500 runs of all roots to time")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed Graph500 runs before timing")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
@@ -540,14 +661,15 @@ def main():
     ap.add_argument("--roots", type=int, default=64)
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--device", type=int, default=0)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the independent oracle build / CPU runs")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--graph", choices=["rmat", "er"], default="rmat",
                     help="rmat: Graph500 quadrants; er: uniform quadrants (Erdos-Renyi, configs[4])")
-    ap.add_argument("--labeling", choices=["scrambled", "reference"], default="scrambled",
-                    help="vertex labels: the reference hash, plus (default) this build's Feistel relabeling")
-    ap.add_argument("--no-alt-labeling", action="store_true",
-                    help="skip the extra device-time series on the reference labeling")
+    ap.add_argument("--labeling", choices=["auto", "scrambled", "reference"], default="auto",
+                    help="vertex labels: the reference hash (N = 1 default) or + this build's Feistel relabeling "
+                         "(N > 1 default: balanced v mod N owners)")
+    ap.add_argument("--no-series", action="store_true",
+                    help="skip the configs[2] / configs[3] series and the other-labeling point")
     args = ap.parse_args()
     _claim_stdout()
     if args.warmup < 0 or args.steps < 1:

@@ -113,6 +113,11 @@ typedef struct {
     int64_t work_inspections;   /* inspections actually executed (<= reported when pulls replace pushes) */
     int32_t per_iteration_truncated;
     int32_t engine_used;        /* 1 host loop, 2 persistent, 3 peer */
+    double total_mask_bytes;    /* CommStats.total_mask_bytes (comm.py:39-72): sum over iterations */
+    int64_t total_normal_bytes; /* CommStats.total_normal_bytes */
+    int64_t s_prime;            /* CommStats.s_prime: iterations with a mask reduction */
+    int32_t accounting_valid;   /* 1 when the four fields above and inspections cover every iteration */
+    int32_t _pad;
 } dbfs_run_stats;
 
 /* One BfsRun.per_iteration entry summed over workers (engine.py:291-302). */

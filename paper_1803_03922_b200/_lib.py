@@ -57,7 +57,9 @@ class RunStatsC(ctypes.Structure):
     _fields_ = [("iterations", i64), ("inspections", (i64 * 2) * 4), ("b_measured", dbl),
                 ("device_ms", dbl), ("reached", i64), ("kernel_launches", i64), ("wire_bytes", i64),
                 ("h2d_bytes", i64), ("d2h_bytes", i64), ("rows_touched", i64), ("init_us", dbl), ("work_inspections", i64),
-                ("per_iteration_truncated", i32), ("engine_used", i32)]
+                ("per_iteration_truncated", i32), ("engine_used", i32),
+                ("total_mask_bytes", dbl), ("total_normal_bytes", i64), ("s_prime", i64),
+                ("accounting_valid", i32), ("_pad", i32)]
 
 
 class IterationC(ctypes.Structure):

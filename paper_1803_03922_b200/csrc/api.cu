@@ -347,71 +347,7 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
         DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS has run");
         int64_t nrec = (int64_t)g.last_rec.size() / std::max(g.W, 1);
         DBFS_CHECK(it >= 0 && it < nrec, DBFS_ERANGE, "iteration out of range (or truncated)");
-        const int W = g.W;
-        dbfs_iteration r;
-        memset(&r, 0, sizeof(r));
-        r.iteration = it;
-        bool any_new = false;
-        int64_t records = 0, msgs = 0, uq_records = 0;
-        // send matrix [sender][dest] for message accounting
-        std::vector<int64_t> cnt((size_t)g.p * g.p, 0);
-        for (int i = 0; i < W; i++) {
-            const IterRec &x = g.last_rec[(size_t)it * W + i];
-            for (int k = 0; k < 4; k++) {
-                r.inspections[k] += (int64_t)x.insp[k];
-                r.fv[k] += (int64_t)x.fv[k];
-            }
-            any_new |= x.new_del > 0;
-            r.frontier_normals += (int64_t)x.nfront;
-            for (int k = 0; k < 4; k++) r.work[k] += (int64_t)x.work[k];
-            if (i == 0) {
-                for (int k = 0; k < 4; k++) r.exec_dirs[k] = x.exec_dir[k];
-                double ghz = g.clock_ghz > 0 ? g.clock_ghz : 1.9;
-                double nwarps = g.warps_per_worker > 0 ? g.warps_per_worker : 1;
-                for (int k = 0; k < 8; k++) {
-                    r.task_avg_us[k] = (double)x.tsum[k] / nwarps / (ghz * 1e3);
-                    r.task_max_us[k] = (double)x.tmax[k] / (ghz * 1e3);
-                }
-                r.frontier_delegates = (int64_t)x.dfront;
-                if (x.t[1] > x.t[0]) r.visit_us = (double)(x.t[1] - x.t[0]) / 1e3;
-                if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;
-                if (x.tb[0] > x.t[0] && x.tb[1] >= x.tb[0] && x.tb[2] > x.t[1] && x.tb[3] >= x.tb[2]) {
-                    r.sync_us[0] = (double)(x.tb[0] - x.t[0]) / 1e3;
-                    r.sync_us[1] = (double)(x.tb[1] - x.tb[0]) / 1e3;
-                    r.sync_us[2] = (double)(x.tb[2] - x.t[1]) / 1e3;
-                    r.sync_us[3] = (double)(x.tb[3] - x.tb[2]) / 1e3;
-                }
-            }
-            records += (int64_t)x.records;
-            uq_records += (int64_t)x.uq_records;
-            msgs += (int64_t)x.messages;
-            int w = g.workers[i].w;
-            for (int o = 0; o < g.p; o++) cnt[(size_t)w * g.p + o] = (int64_t)x.send[o];
-            if (directions)
-                for (int k = 0; k < 4; k++) directions[(size_t)w * 4 + k] = (int8_t)x.dir[k];
-            if (bv)
-                for (int k = 0; k < 4; k++) bv[(size_t)w * 4 + k] = x.bv[k];
-        }
-        // comm.py:75-98 / 138-197 accounting
-        r.mask_bytes = any_new ? 2.0 * (double)g.d * (double)g.p_rank / 8.0 : 0.0;
-        r.normal_bytes = 4 * (g.last_uq && g.p > 1 ? uq_records : records);
-        if (g.last_la) {
-            // local-all2all regroups (sender, dest) -> (r + p_rank * (dest / p_rank), dest)
-            std::vector<int> seen((size_t)g.p * g.p, 0);
-            msgs = 0;
-            for (int s = 0; s < g.p; s++)
-                for (int o = 0; o < g.p; o++)
-                    if (cnt[(size_t)s * g.p + o] > 0) {
-                        int fs = (s % g.p_rank) + g.p_rank * (o / g.p_rank);
-                        if (!seen[(size_t)fs * g.p + o]) {
-                            seen[(size_t)fs * g.p + o] = 1;
-                            msgs++;
-                        }
-                    }
-        }
-        r.message_count = msgs;
-        r.pair_count = g.last_la ? (int64_t)g.p * g.p / g.p_gpu : (int64_t)g.p * g.p;
-        *rec = r;
+        iteration_summary(g, &g.last_rec[(size_t)it * g.W], it, g.last_la, g.last_uq, rec, directions, bv);
     });
 }
 

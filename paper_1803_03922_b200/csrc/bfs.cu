@@ -295,6 +295,19 @@ __global__ void k_batch_prep(const View *__restrict__ views, GridBar *bar) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *bar = GridBar{0u, 0u, 0u, 0u};
 }
 
+// Per-root iteration records of a batch (dbfs_bfs_batch with record_iterations):
+// the first rmax records of every worker into dst[it * W + w].
+__global__ void k_stage_recs(const View *__restrict__ views, int W, int rmax, IterRec *__restrict__ dst) {
+    const int w = blockIdx.x;
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(views[w].rec);
+    static_assert(sizeof(IterRec) % 8 == 0, "records are copied in 8-byte words");
+    constexpr int NW = sizeof(IterRec) / 8;
+    for (int i = threadIdx.x; i < rmax * NW; i += blockDim.x) {
+        const int it = i / NW, j = i % NW;
+        reinterpret_cast<unsigned long long *>(&dst[(size_t)it * W + w])[j] = src[i];
+    }
+}
+
 __global__ void k_batch_info(const Ctl *__restrict__ ctl0, const GridBar *__restrict__ bar, int2 *info,
                              unsigned *esc) {
     *info = make_int2(ctl0->last_level, (int)bar->abort);
@@ -1054,11 +1067,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         memset(st, 0, sizeof(*st));
         st->iterations = iterations;
         st->reached = reached;
-        for (int L = 0; L < nrec; L++)
-            for (int i = 0; i < W; i++) {
-                const IterRec &r = g.last_rec[(size_t)L * W + i];
-                for (int k = 0; k < 4; k++) st->inspections[k][r.dir[k]] += (int64_t)r.insp[k];
-            }
+        run_accounting(g, g.last_rec.data(), nrec, iterations, g.last_la, g.last_uq, st);
         st->device_ms = ms;
         st->kernel_launches = g_kernel_launches - launches0;
         st->per_iteration_truncated = g.last_truncated;
@@ -1088,8 +1097,6 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
             st->init_us = (double)(c0.t_seeded - c0.t_start) / 1e3;
         }
         st->d2h_bytes = 4 + (int64_t)sizeof(Ctl) + (int64_t)(sizeof(IterRec) * nrec * W);
-        int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
-        st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
     }
     if (g.dist && st) {
         // inspections are per rank; sum over ranks
@@ -1366,6 +1373,29 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     AsmArgs aa = make_asm(g, o0.parent_mode != 0);
     int do_asm = (!g.dist && g.p > 1) ? 1 : 0;
     AsmArgs out_asm = batch_asm(g, o0.parent_mode != 0, local != 0);
+    // per-root iteration records (comm accounting / inspections of every root,
+    // dbfs_run_stats.accounting_valid): staged on device after each traversal,
+    // copied on the copy stream with the root's outputs
+    const int rmax = std::min(g.rec_cap, 64);
+    const bool want_rec = o0.record_iterations && !g.dist && st;
+    DArray<IterRec> drec;
+    struct PinnedRecs {
+        IterRec *p = nullptr;
+        ~PinnedRecs() {
+            if (p) cudaFreeHost(p);
+        }
+    } hrec_buf;
+    if (want_rec) {
+        drec.alloc((int64_t)count * rmax * W);
+        DBFS_CUDA(cudaHostAlloc((void **)&hrec_buf.p, drec.bytes(), cudaHostAllocDefault));
+    }
+    IterRec *const hrec = hrec_buf.p;
+    auto copy_recs = [&](int64_t k) {
+        if (!want_rec) return;
+        const size_t per = (size_t)rmax * W;
+        DBFS_CUDA(cudaMemcpyAsync(hrec + k * per, drec.p + k * per, per * sizeof(IterRec), cudaMemcpyDeviceToHost,
+                                  ctx.copy_stream));
+    };
     void *flag = (char *)ctx.ensure_scratch(256) + 128;  // NCCL barrier word (the grid barrier is at offset 0)
     GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
     DArray<int2> info;
@@ -1394,6 +1424,10 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         DBFS_LAUNCHED();
         DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
         if (o0.parent_mode == 2) min_parents_device(g, src);  // untimed: after the traversal's end event
+        if (want_rec) {
+            k_stage_recs<<<W, 256, 0, ctx.stream>>>(g.views.p, W, rmax, drec.p + (size_t)k * rmax * W);
+            DBFS_LAUNCHED();
+        }
         if (esc_k && k >= 2) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[k & 1], 0));
         k_batch_info<<<1, 1, 0, ctx.stream>>>(g.workers[0].ctl.p, bar, info.p + k, esc_k);
         DBFS_LAUNCHED();
@@ -1403,6 +1437,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         for (int64_t k = 0; k < count; k++) {
             enqueue_root(k, nullptr);
             stage_and_copy(k, g.dist ? &out_asm : nullptr);
+            copy_recs(k);  // the copy stream already waits for this root's staging
         }
     } else {
         // Compact transfers: the depth travels as int8 (9 bytes per vertex on the
@@ -1451,6 +1486,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                     DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * nout, cudaMemcpyDeviceToHost,
                                               ctx.copy_stream));
                 DBFS_CUDA(cudaMemcpyAsync(g.hesc + hb, g.esc.p + b, 4, cudaMemcpyDeviceToHost, ctx.copy_stream));
+                copy_recs(k);
                 DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
                 DBFS_CUDA(cudaEventRecord(ctx.ev_hdone[hb], ctx.copy_stream));
                 if (st) st[k].d2h_bytes += nout + (want_par && parents[k] ? 8 * nout : 0) + 4;
@@ -1522,6 +1558,21 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             r.per_iteration_truncated = 1;  // records are not collected in batch mode
             r.h2d_bytes = k == 0 ? (int64_t)(sizeof(View) * W) : 0;
             r.d2h_bytes = d2h + (int64_t)sizeof(int2);
+            if (want_rec) {
+                const int64_t nrec = std::min<int64_t>(hi[k].x, rmax);
+                run_accounting(g, hrec + (size_t)k * rmax * W, nrec, hi[k].x, o0.local_all2all,
+                               o0.uniquify && g.p > 1, &r);
+                r.d2h_bytes += (int64_t)((size_t)rmax * W * sizeof(IterRec));
+                int64_t work = 0, rows = 0;
+                for (int64_t it = 0; it < nrec; it++)
+                    for (int i = 0; i < W; i++) {
+                        const IterRec &x = hrec[((size_t)k * rmax + it) * W + i];
+                        rows += (int64_t)x.rows;
+                        for (int q = 0; q < 4; q++) work += (int64_t)x.work[q];
+                    }
+                r.rows_touched = rows;
+                r.work_inspections = work;
+            }
         }
     }
     for (auto &e : evs) cudaEventDestroy(e);
@@ -1544,6 +1595,105 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     g.last_la = o0.local_all2all;
     g.last_uq = o0.uniquify;
     g.assembled = !g.dist;
+}
+
+// ------------------------------------------------------ per-iteration records
+
+// BfsRun.per_iteration entry `it` summed over the W local workers' records
+// x[0..W) (engine.py:291-302) with the comm accounting of comm.py:75-197.
+void iteration_summary(const Graph &g, const IterRec *x0, int64_t it, int last_la, int last_uq, dbfs_iteration *rec,
+                       int8_t *directions, double *bv) {
+    dbfs_iteration r;
+    memset(&r, 0, sizeof(r));
+    r.iteration = it;
+    const int W = g.W;
+    bool any_new = false;
+    int64_t records = 0, msgs = 0, uq_records = 0;
+    // send matrix [sender][dest] for message accounting
+    std::vector<int64_t> cnt((size_t)g.p * g.p, 0);
+    for (int i = 0; i < W; i++) {
+        const IterRec &x = x0[i];
+        for (int k = 0; k < 4; k++) {
+            r.inspections[k] += (int64_t)x.insp[k];
+            r.fv[k] += (int64_t)x.fv[k];
+        }
+        any_new |= x.new_del > 0;
+        r.frontier_normals += (int64_t)x.nfront;
+        for (int k = 0; k < 4; k++) r.work[k] += (int64_t)x.work[k];
+        if (i == 0) {
+            for (int k = 0; k < 4; k++) r.exec_dirs[k] = x.exec_dir[k];
+            double ghz = g.clock_ghz > 0 ? g.clock_ghz : 1.9;
+            double nwarps = g.warps_per_worker > 0 ? g.warps_per_worker : 1;
+            for (int k = 0; k < 8; k++) {
+                r.task_avg_us[k] = (double)x.tsum[k] / nwarps / (ghz * 1e3);
+                r.task_max_us[k] = (double)x.tmax[k] / (ghz * 1e3);
+            }
+            r.frontier_delegates = (int64_t)x.dfront;
+            if (x.t[1] > x.t[0]) r.visit_us = (double)(x.t[1] - x.t[0]) / 1e3;
+            if (x.t[2] > x.t[1]) r.finish_us = (double)(x.t[2] - x.t[1]) / 1e3;
+            if (x.tb[0] > x.t[0] && x.tb[1] >= x.tb[0] && x.tb[2] > x.t[1] && x.tb[3] >= x.tb[2]) {
+                r.sync_us[0] = (double)(x.tb[0] - x.t[0]) / 1e3;
+                r.sync_us[1] = (double)(x.tb[1] - x.tb[0]) / 1e3;
+                r.sync_us[2] = (double)(x.tb[2] - x.t[1]) / 1e3;
+                r.sync_us[3] = (double)(x.tb[3] - x.tb[2]) / 1e3;
+            }
+        }
+        records += (int64_t)x.records;
+        uq_records += (int64_t)x.uq_records;
+        msgs += (int64_t)x.messages;
+        int w = g.workers[i].w;
+        for (int o = 0; o < g.p; o++) cnt[(size_t)w * g.p + o] = (int64_t)x.send[o];
+        if (directions)
+            for (int k = 0; k < 4; k++) directions[(size_t)w * 4 + k] = (int8_t)x.dir[k];
+        if (bv)
+            for (int k = 0; k < 4; k++) bv[(size_t)w * 4 + k] = x.bv[k];
+    }
+    // comm.py:75-98 / 138-197 accounting
+    r.mask_bytes = any_new ? 2.0 * (double)g.d * (double)g.p_rank / 8.0 : 0.0;
+    r.normal_bytes = 4 * (last_uq && g.p > 1 ? uq_records : records);
+    if (last_la) {
+        // local-all2all regroups (sender, dest) -> (r + p_rank * (dest / p_rank), dest)
+        std::vector<int> seen((size_t)g.p * g.p, 0);
+        msgs = 0;
+        for (int s = 0; s < g.p; s++)
+            for (int o = 0; o < g.p; o++)
+                if (cnt[(size_t)s * g.p + o] > 0) {
+                    int fs = (s % g.p_rank) + g.p_rank * (o / g.p_rank);
+                    if (!seen[(size_t)fs * g.p + o]) {
+                        seen[(size_t)fs * g.p + o] = 1;
+                        msgs++;
+                    }
+                }
+    }
+    r.message_count = msgs;
+    r.pair_count = last_la ? (int64_t)g.p * g.p / g.p_gpu : (int64_t)g.p * g.p;
+    *rec = r;
+}
+
+// Run-level accounting from the records of iterations [0, nrec): inspections
+// by reported direction, b_measured (engine.py:316-318) and the CommStats
+// totals (comm.py:39-72), summed in iteration order like the reference.
+void run_accounting(const Graph &g, const IterRec *recs, int64_t nrec, int64_t iterations, int la, int uq,
+                    dbfs_run_stats *st) {
+    const int W = g.W;
+    for (int k = 0; k < 4; k++) st->inspections[k][0] = st->inspections[k][1] = 0;
+    st->total_mask_bytes = 0.0;
+    st->total_normal_bytes = 0;
+    st->s_prime = 0;
+    for (int64_t it = 0; it < nrec; it++) {
+        for (int i = 0; i < W; i++) {
+            const IterRec &r = recs[(size_t)it * W + i];
+            for (int k = 0; k < 4; k++) st->inspections[k][r.dir[k]] += (int64_t)r.insp[k];
+        }
+        dbfs_iteration s;
+        iteration_summary(g, &recs[(size_t)it * W], it, la, uq, &s, nullptr, nullptr);
+        st->total_mask_bytes += s.mask_bytes;
+        st->total_normal_bytes += s.normal_bytes;
+        st->s_prime += s.mask_bytes > 0;
+    }
+    const int64_t bwd = st->inspections[KIND_ND][BWD] + st->inspections[KIND_DD][BWD];
+    st->b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
+    st->accounting_valid = (!g.dist && nrec == iterations) ? 1 : 0;
 }
 
 // ------------------------------------------------ min-ID parents (A19) / A20

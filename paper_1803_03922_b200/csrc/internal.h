@@ -317,6 +317,10 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o, const int64_t *roots, in
                    int64_t *const *parents, int local, int compact, dbfs_run_stats *st);
 int64_t batch_output_count(const Graph &g, bool local);
 void min_parents(Graph &g, int64_t *out);
+void iteration_summary(const Graph &g, const IterRec *x0, int64_t it, int last_la, int last_uq, dbfs_iteration *rec,
+                       int8_t *directions, double *bv);
+void run_accounting(const Graph &g, const IterRec *recs, int64_t nrec, int64_t iterations, int la, int uq,
+                    dbfs_run_stats *st);
 int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *parents);
 
 // dist.cu (NCCL)

@@ -196,18 +196,70 @@ def run_bfs(pg: PartitionedGraph, opts: BfsOptions) -> BfsRun:
                   device_ms=float(st.device_ms), kernel_launches=int(st.kernel_launches))
 
 
+def _run_entry(s, iterations, teps, total_insp, mask_bytes, normal_bytes, s_prime, digest):
+    return {"source": s, "iterations": iterations, "teps": teps, "total_inspections": total_insp,
+            "mask_bytes": mask_bytes, "normal_bytes": normal_bytes, "s_prime": s_prime, "levels_digest": digest}
+
+
 def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     """Per-source runs, discard S <= 1, geometric-mean TEPS (engine.py:333-364);
-    the Graph500 harmonic mean is reported beside it."""
-    runs = []
-    sources = list(sources)
+    the Graph500 harmonic mean is reported beside it.
+
+    One process owning the whole graph runs the sources as a pipelined batch
+    (``dbfs_bfs_batch``): every root's levels reach host memory (the depth
+    travels as int8 and is widened on the host's cores while later roots
+    traverse), its iteration records give the same inspections / mask bytes /
+    normal bytes / S' as ``run_bfs``, and digests are taken after the call
+    (the reference, too, hashes outside its timed region).  Runs are
+    pipelined, so a per-run wall clock does not exist: a run's ``teps`` uses
+    its device-timed traversal, and the report adds ``wall_s`` (the batch
+    calls, host copies included) and ``e2e_teps`` over all runs.  Distributed
+    graphs and the host-loop engine run ``run_bfs`` per source."""
+    sources = [int(s) for s in sources]
     for s in sources:
-        run = run_bfs(pg, dataclasses.replace(opts, source=int(s)))
-        if run.iterations > 1:
-            runs.append((int(s), run))
+        if not (0 <= s < pg.n):
+            raise ValueError(f"source {s} out of range [0, {pg.n})")
+    entries, t_total = [], 0.0
+    if pg.nranks > 1 or opts.engine == "host":
+        for s in sources:
+            run = run_bfs(pg, dataclasses.replace(opts, source=s))
+            t_total += run.elapsed
+            entries.append((run.iterations, _run_entry(s, run.iterations, run.teps, run.total_inspections,
+                                                       run.comm_stats.total_mask_bytes,
+                                                       run.comm_stats.total_normal_bytes,
+                                                       run.comm_stats.s_prime, run.levels_digest)))
+    else:
+        n = pg.n
+        chunk = max(1, min(len(sources), (8 << 30) // max(4 * n, 1)))  # <= 8 GiB of host levels per call
+        # host level arrays are kept with the graph and reused by later calls
+        # (fresh pages would be faulted in by the host widening inside the call)
+        bufs = getattr(pg, "_benchmark_levels", None)
+        if bufs is None or len(bufs) < chunk or bufs[0].size != n:
+            bufs = [np.zeros(n, dtype=np.int32) for _ in range(chunk)]
+            pg._benchmark_levels = bufs
+        for c0 in range(0, len(sources), chunk):
+            roots = sources[c0:c0 + chunk]
+            t0 = time.perf_counter()
+            outs, sts = bfs_batch(pg, roots, outs=[(bufs[i], None) for i in range(len(roots))], mode=opts.mode,
+                                  parents=opts.parents, stats=True, options=opts, accounting=True)
+            t_total += time.perf_counter() - t0
+            for i, (s, st) in enumerate(zip(roots, sts)):
+                if not st.accounting_valid:  # records truncated (deep BFS): exact stats from a single run
+                    run = run_bfs(pg, dataclasses.replace(opts, source=s))
+                    entries.append((run.iterations, _run_entry(
+                        s, run.iterations, run.teps, run.total_inspections, run.comm_stats.total_mask_bytes,
+                        run.comm_stats.total_normal_bytes, run.comm_stats.s_prime, run.levels_digest)))
+                    continue
+                it = int(st.iterations)
+                total = sum(int(st.inspections[k][0]) + int(st.inspections[k][1]) for k in range(4))
+                teps = compute_teps(pg.m, max(st.device_ms, 1e-6) / 1e3)
+                entries.append((it, _run_entry(s, it, teps, total, float(st.total_mask_bytes),
+                                               int(st.total_normal_bytes), int(st.s_prime),
+                                               levels_digest(bufs[i]))))
+    runs = [e for it, e in entries if it > 1]
     if not runs:
         raise EmptyReportError("all runs discarded (every source trivial)")
-    teps = np.array([r.teps for _, r in runs])
+    teps = np.array([r["teps"] for r in runs])
     geomean = float(np.exp(np.log(teps).mean()))
     harmonic = float(len(teps) / np.sum(1.0 / teps))
     return {
@@ -215,19 +267,9 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
         "num_discarded": len(sources) - len(runs),
         "geomean_teps": geomean,
         "harmonic_teps": harmonic,
-        "runs": [
-            {
-                "source": s,
-                "iterations": r.iterations,
-                "teps": r.teps,
-                "total_inspections": r.total_inspections,
-                "mask_bytes": r.comm_stats.total_mask_bytes,
-                "normal_bytes": r.comm_stats.total_normal_bytes,
-                "s_prime": r.comm_stats.s_prime,
-                "levels_digest": r.levels_digest,
-            }
-            for s, r in runs
-        ],
+        "wall_s": t_total,
+        "e2e_teps": len(sources) * (pg.m / 2) / t_total if t_total > 0 else 0.0,
+        "runs": runs,
     }
 
 
@@ -261,7 +303,8 @@ def _check_host_array(a, dtype, n: int, what: str):
 
 
 def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", parents: str | None = "any",
-              stats: bool = False, local: bool = False, compact: bool | None = None):
+              stats: bool = False, local: bool = False, compact: bool | None = None,
+              options: BfsOptions | None = None, accounting: bool = False):
     """Graph500's multi-root loop in one call (``dbfs_bfs_batch``): returns one
     (depth, parent) pair per root.  The device-to-host copy of root k runs on a
     separate stream while root k+1 traverses, so PCIe time hides behind the
@@ -277,7 +320,10 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
     results; a root with a depth >= 127 is re-run with full arrays).  None:
     on for a single process, off when ranks share the host (their widening
     competes for it); ``DBFS_COMPACT=0/1`` overrides.  Per-iteration records
-    are not kept.
+    are not kept; ``accounting=True`` (single process) keeps each root's
+    records long enough to fill its run stats with the reference's
+    inspections and CommStats totals (``accounting_valid``).  ``options``
+    supplies the other BfsOptions fields (factors, executor, ...).
     ``stats=True`` also returns the per-root C run-stats structs."""
     if parents not in PARENT_MODES:
         raise ValueError(f"parents must be one of {list(PARENT_MODES)}")
@@ -303,9 +349,12 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
     lv_ptrs = (_lib.vp * max(count, 1))(*[lv.ctypes.data if lv is not None else None for lv, _ in outs])
     pa_ptrs = (_lib.vp * max(count, 1))(*[pa.ctypes.data if pa is not None else None for _, pa in outs])
     st = (_lib.RunStatsC * max(count, 1))()
-    opts = BfsOptions(mode=mode, source=int(roots[0]) if count else 0, parents=parents).to_c()
+    base = options if options is not None else BfsOptions()
+    opts = dataclasses.replace(base, mode=mode, source=int(roots[0]) if count else 0, parents=parents).to_c()
+    opts.record_iterations = int(bool(accounting))
     _lib.check(_lib.load().dbfs_bfs_batch(pg.handle, ctypes.byref(opts), roots.ctypes.data_as(_lib.vp), count,
-                                          lv_ptrs, pa_ptrs if parents else None, int(bool(local)), int(bool(compact)),
+                                          lv_ptrs, pa_ptrs if parents and any(pa is not None for _, pa in outs) else None,
+                                          int(bool(local)), int(bool(compact)),
                                           st), "bfs_batch")
     return (outs, list(st)[:count]) if stats else outs
 

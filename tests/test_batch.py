@@ -73,3 +73,28 @@ def test_compact_batch_escapes_deep_levels(api):
         assert api.validate_bfs_tree(pg, r, lv, pa) == 0
         ref_lv, _ = api.bfs(pg, r)
         assert np.array_equal(lv, ref_lv)
+
+
+def test_compact_rerun_leaves_device_state_consistent(api):
+    """An early root escapes (depth >= 127) and is re-run after the batch while
+    the last root does not: the device result, last source and iteration count
+    must then describe the re-run root (validate / min_parents without arrays
+    use them)."""
+    n = 400
+    src = np.arange(n - 1, dtype=np.int64)
+    # path of 400 plus a shallow last root: centre of a short component glued on
+    n2 = n + 5
+    s2 = np.concatenate([src, np.array([n, n, n, n])])
+    d2 = np.concatenate([src + 1, np.array([n + 1, n + 2, n + 3, n + 4])])
+    g2 = api.EdgeList(np.concatenate([s2, d2]), np.concatenate([d2, s2]), n=n2, symmetric=True)
+    pg2 = api.partition_graph(g2, 2, api.ClusterShape(1, 1))
+    outs = api.bfs_batch(pg2, [0, n], compact=True, parents="any")
+    assert outs[0][0][n - 1] == n - 1 and outs[1][0][n] == 0
+    # the device now holds root 0's result (re-run last): certificate on device arrays
+    assert api.validate_bfs_tree(pg2, 0) == 0
+    par = api.min_parents(pg2)
+    assert par[0] == 0 and par[1] == 0 and par[n - 1] == n - 2
+    # min-ID parents requested in a batch are computed on device per root
+    outs = api.bfs_batch(pg2, [n, 2], parents="min", compact=False)
+    lv, pa = outs[1]
+    assert pa[2] == 2 and pa[1] == 2 and pa[3] == 2 and pa[0] == 1 and pa[n] == -1

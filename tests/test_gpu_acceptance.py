@@ -85,10 +85,50 @@ def test_c1_all_roots_match_reference(api):
             ref = want[(root, mode)]
             for key in ("levels_digest", "iterations", "inspections", "b_measured", "per_iteration", "comm"):
                 assert got[key] == ref[key], (root, mode, key)
-    # the reference's benchmark() over the 64 Graph500 roots: same runs kept
-    rep = api.benchmark(pg, roots[:64], api.BfsOptions(mode="dobfs"))
-    assert [r["levels_digest"] for r in rep["runs"]] == [want[(s, "dobfs")]["levels_digest"] for s in roots[:64]
-                                                         if want[(s, "dobfs")]["iterations"] > 1]
+    # the reference's benchmark() over all roots (one pipelined batch): the
+    # same runs kept, each with the reference's digest, counters and comm totals
+    for mode in ("bfs", "dobfs"):
+        rep = api.benchmark(pg, roots, api.BfsOptions(mode=mode))
+        kept = [s for s in roots if want[(s, mode)]["iterations"] > 1]
+        assert [r["source"] for r in rep["runs"]] == kept
+        assert rep["num_discarded"] == len(roots) - len(kept)
+        for r in rep["runs"]:
+            ref = want[(r["source"], mode)]
+            assert r["levels_digest"] == ref["levels_digest"]
+            assert r["iterations"] == ref["iterations"]
+            assert r["total_inspections"] == ref["total_inspections"]
+            assert r["mask_bytes"] == ref["comm"]["total_mask_bytes"]
+            assert r["normal_bytes"] == ref["comm"]["total_normal_bytes"]
+            assert r["s_prime"] == ref["comm"]["s_prime"]
+
+
+def test_benchmark_matches_golden_runs(api):
+    """benchmark() (batched, records per root) reports the reference's per-run
+    digests, inspections and comm totals on every golden partition, p > 1
+    simulated workers and local_all2all / uniquify included."""
+    from golden_utils import iter_partitions
+    gold = load()
+    for g, p in iter_partitions(gold, max_scale=14):
+        a, b, c, dq = g["quads"]
+        params = api.RmatParams(scale=g["scale"], seed=g["seed"], edge_factor=g["edge_factor"], a=a, b=b, c=c,
+                                d_quad=dq)
+        pg = api.partition_graph(api.build_rmat_graph(params), p["theta"], api.ClusterShape(p["p_rank"], p["p_gpu"]))
+        groups = {}
+        for r in p["runs"]:
+            groups.setdefault((r["mode"], r["local_all2all"], r["uniquify"]), []).append(r)
+        for (mode, la, uq), runs in groups.items():
+            rep = api.benchmark(pg, [r["source"] for r in runs],
+                                api.BfsOptions(mode=mode, local_all2all=la, uniquify=uq))
+            kept = [r for r in runs if r["report"]["iterations"] > 1]
+            assert len(rep["runs"]) == len(kept)
+            for got, r in zip(rep["runs"], kept):
+                ref = r["report"]
+                assert got["source"] == r["source"]
+                assert got["levels_digest"] == ref["levels_digest"]
+                assert got["total_inspections"] == ref["total_inspections"]
+                assert (got["mask_bytes"], got["normal_bytes"], got["s_prime"]) == (
+                    ref["comm"]["total_mask_bytes"], ref["comm"]["total_normal_bytes"], ref["comm"]["s_prime"])
+        pg.close()
 
 
 def test_scale22_csr_equals_oracle_partition(api):
