@@ -7,6 +7,7 @@
 //   host loop : one launch per phase with the NCCL exchange between V and F;
 //               used with one worker per process (torchrun, NCCL over NVLink).
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <thread>
 
@@ -376,6 +377,8 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 
 Graph::~Graph() {
     if (h_ctl) cudaFreeHost(h_ctl);
+    if (batch_hrec) cudaFreeHost(batch_hrec);
+    for (cudaEvent_t e : batch_evs) cudaEventDestroy(e);
     for (int h = 0; h < 3; h++) {
         if (hstage8[h]) cudaFreeHost(hstage8[h]);
         if (hstage32[h]) cudaFreeHost(hstage32[h]);
@@ -1282,6 +1285,8 @@ int64_t batch_output_count(const Graph &g, bool local) { return (local && g.dist
 void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, int64_t count, int32_t *const *levels,
                    int64_t *const *parents, int local, int compact_req, dbfs_run_stats *st) {
     Ctx &ctx = *g.ctx;
+    const double tentry =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     DBFS_CHECK(o0.mode == 0 || o0.mode == 1, DBFS_EINVAL, "mode must be one of ('bfs', 'dobfs')");
     for (int64_t k = 0; k < count; k++)
         DBFS_CHECK(0 <= roots[k] && roots[k] < g.n, DBFS_ERANGE,
@@ -1362,6 +1367,12 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     const int W = g.W;
     const bool peer = engine == 3;
     const bool compact = compact_req && levels && g.n < ((int64_t)1 << 31);
+    const bool btrace = getenv("DBFS_BATCH_TRACE") != nullptr;
+    auto now_ms = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double tb0 = now_ms();
+    double t_wait = 0, t_widen = 0;
     if (compact) ensure_compact_staging(g, nout);
     set_smem_attrs();
     if (g.pgrid <= 0) {
@@ -1378,18 +1389,16 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     // copied on the copy stream with the root's outputs
     const int rmax = std::min(g.rec_cap, 64);
     const bool want_rec = o0.record_iterations && !g.dist && st;
-    DArray<IterRec> drec;
-    struct PinnedRecs {
-        IterRec *p = nullptr;
-        ~PinnedRecs() {
-            if (p) cudaFreeHost(p);
-        }
-    } hrec_buf;
-    if (want_rec) {
+    // batch scratch is kept with the graph and only grows: cudaMalloc /
+    // cudaHostAlloc / cudaFree inside the call would synchronise and stall
+    DArray<IterRec> &drec = g.batch_drec;
+    if (want_rec && drec.n < (int64_t)count * rmax * W) {
         drec.alloc((int64_t)count * rmax * W);
-        DBFS_CUDA(cudaHostAlloc((void **)&hrec_buf.p, drec.bytes(), cudaHostAllocDefault));
+        if (g.batch_hrec) cudaFreeHost(g.batch_hrec);
+        g.batch_hrec = nullptr;
+        DBFS_CUDA(cudaHostAlloc((void **)&g.batch_hrec, drec.bytes(), cudaHostAllocDefault));
     }
-    IterRec *const hrec = hrec_buf.p;
+    IterRec *const hrec = g.batch_hrec;
     auto copy_recs = [&](int64_t k) {
         if (!want_rec) return;
         const size_t per = (size_t)rmax * W;
@@ -1398,10 +1407,14 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     };
     void *flag = (char *)ctx.ensure_scratch(256) + 128;  // NCCL barrier word (the grid barrier is at offset 0)
     GridBar *bar = (GridBar *)ctx.ensure_scratch(sizeof(GridBar));
-    DArray<int2> info;
-    info.alloc(count);
-    std::vector<cudaEvent_t> evs(2 * count, nullptr);
-    for (auto &e : evs) DBFS_CUDA(cudaEventCreate(&e));
+    DArray<int2> &info = g.batch_info;
+    if (info.n < count) info.alloc(count);
+    while ((int64_t)g.batch_evs.size() < 2 * count) {
+        cudaEvent_t e;
+        DBFS_CUDA(cudaEventCreate(&e));
+        g.batch_evs.push_back(e);
+    }
+    const std::vector<cudaEvent_t> &evs = g.batch_evs;
     if (peer) nccl_barrier(ctx);
     const int64_t launches0 = g_kernel_launches;
     const View *vp = peer ? g.peer_view.p : g.views.p;
@@ -1494,9 +1507,15 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             if (k >= 2) {
                 const int64_t j = k - 2;
                 const int hb = (int)(j % 3);
+                const double tw0 = btrace ? now_ms() : 0;
                 DBFS_CUDA(cudaEventSynchronize(ctx.ev_hdone[hb]));
+                const double tw1 = btrace ? now_ms() : 0;
                 if (g.hesc[hb]) rerun.push_back(j);
                 else widen_result(g.hstage8[hb], nullptr, nout, levels[j], nullptr, host_threads);
+                if (btrace) {
+                    t_wait += tw1 - tw0;
+                    t_widen += now_ms() - tw1;
+                }
             }
         }
     }
@@ -1538,6 +1557,9 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             }
         }
     }
+    if (btrace)
+        fprintf(stderr, "[batch] %lld roots: setup %.2f ms, loop+sync %.2f ms (waits %.2f, widening %.2f)\n",
+                (long long)count, tb0 - tentry, now_ms() - tb0, t_wait, t_widen);
     std::vector<int2> hi(count);
     DBFS_CUDA(cudaMemcpy(hi.data(), info.p, sizeof(int2) * count, cudaMemcpyDeviceToHost));
     const int64_t launches = g_kernel_launches - launches0;
@@ -1575,7 +1597,6 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             }
         }
     }
-    for (auto &e : evs) cudaEventDestroy(e);
     if (aborted && peer) g.peer_state = -1;
     DBFS_CHECK(!aborted, DBFS_ETIMEOUT, "device watchdog fired in the persistent BFS kernel");
     if (!rerun.empty()) {
@@ -1585,6 +1606,10 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         g.last_rec.clear();
         return;
     }
+    if (btrace)
+        fprintf(stderr, "[batch] done at %.2f ms after entry\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() -
+                    tentry);
     g.last_iterations = hi[count - 1].x;
     g.last_truncated = true;
     g.last_rec.clear();

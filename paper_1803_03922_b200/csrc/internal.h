@@ -293,6 +293,10 @@ struct Graph {
     unsigned *hesc = nullptr;        // pinned: escape counts of the 3 host sets
     DArray<unsigned> esc;            // device escape counters (2 staging buffers)
     DArray<unsigned long long> minpar;  // min-ID parent candidates (parent_mode 2)
+    DArray<IterRec> batch_drec;      // dbfs_bfs_batch scratch (grow-only): per-root records,
+    IterRec *batch_hrec = nullptr;   //   their pinned host copy,
+    DArray<int2> batch_info;         //   per-root (iterations, watchdog),
+    std::vector<cudaEvent_t> batch_evs;  // and per-root timing events
     ~Graph();
     int32_t *levels_dev();
     int64_t *parents_dev();

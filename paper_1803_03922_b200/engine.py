@@ -231,18 +231,24 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     else:
         n = pg.n
         chunk = max(1, min(len(sources), (8 << 30) // max(4 * n, 1)))  # <= 8 GiB of host levels per call
-        # host level arrays are kept with the graph and reused by later calls
-        # (fresh pages would be faulted in by the host widening inside the call)
-        bufs = getattr(pg, "_benchmark_levels", None)
-        if bufs is None or len(bufs) < chunk or bufs[0].size != n:
-            bufs = [np.zeros(n, dtype=np.int32) for _ in range(chunk)]
-            pg._benchmark_levels = bufs
+        # host level arrays: page-locked, kept with the graph and reused by later
+        # calls (pageable pages are faulted in -- or NUMA-migrated -- while the
+        # host widens the depths inside the call)
+        held = getattr(pg, "_benchmark_levels", None)
+        if held is None or len(held) < chunk or held[0].array.size != n:
+            pg._benchmark_levels = None
+            held = [_lib.pinned_empty(n, np.int32) for _ in range(chunk)]
+            pg._benchmark_levels = held
+        bufs = [h.array for h in held]
         for c0 in range(0, len(sources), chunk):
             roots = sources[c0:c0 + chunk]
             t0 = time.perf_counter()
             outs, sts = bfs_batch(pg, roots, outs=[(bufs[i], None) for i in range(len(roots))], mode=opts.mode,
                                   parents=opts.parents, stats=True, options=opts, accounting=True)
             t_total += time.perf_counter() - t0
+            from concurrent.futures import ThreadPoolExecutor  # digests after the timed call (hashlib drops the GIL)
+            with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+                digests = list(ex.map(levels_digest, bufs[:len(roots)]))
             for i, (s, st) in enumerate(zip(roots, sts)):
                 if not st.accounting_valid:  # records truncated (deep BFS): exact stats from a single run
                     run = run_bfs(pg, dataclasses.replace(opts, source=s))
@@ -254,8 +260,7 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
                 total = sum(int(st.inspections[k][0]) + int(st.inspections[k][1]) for k in range(4))
                 teps = compute_teps(pg.m, max(st.device_ms, 1e-6) / 1e3)
                 entries.append((it, _run_entry(s, it, teps, total, float(st.total_mask_bytes),
-                                               int(st.total_normal_bytes), int(st.s_prime),
-                                               levels_digest(bufs[i]))))
+                                               int(st.total_normal_bytes), int(st.s_prime), digests[i])))
     runs = [e for it, e in entries if it > 1]
     if not runs:
         raise EmptyReportError("all runs discarded (every source trivial)")
