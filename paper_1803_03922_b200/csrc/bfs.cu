@@ -227,7 +227,14 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
     extern __shared__ uint4 dsm[];
     Smem &sm = *reinterpret_cast<Smem *>(dsm);
     const int wsel = blockIdx.x % W, wb = blockIdx.x / W, nb = gridDim.x / W;
-    const View &V = views[wsel];
+    {
+        static_assert(sizeof(View) % 16 == 0, "View is copied in 16-byte words");
+        const uint4 *src = reinterpret_cast<const uint4 *>(&views[wsel]);
+        uint4 *dst = reinterpret_cast<uint4 *>(&sm.view);
+        for (int i = threadIdx.x; i < (int)(sizeof(View) / 16); i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
+    const View &V = sm.view;
     const unsigned nblocks = gridDim.x;
     const bool timer = wb == 0 && threadIdx.x == 0;
     if (timer) V.ctl->t_start = globaltimer_ns();
@@ -433,6 +440,8 @@ static void ensure_resources(Graph &g) {
         Wk.dparent.alloc(std::max<int64_t>(g.d, 1));
         Wk.dcand.alloc(std::max<int64_t>(g.d, 1));
         Wk.nvis.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.nseen.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.dseen.alloc(std::max<int64_t>(nw_d, 1));
         Wk.nfront0.alloc(std::max<int64_t>(nw_n, 1));
         Wk.nfront1.alloc(std::max<int64_t>(nw_n, 1));
         Wk.dvis.alloc(std::max<int64_t>(nw_d, 1));
@@ -528,6 +537,8 @@ static void ensure_resources(Graph &g) {
         V.dparent = Wk.dparent.p;
         V.dcand = Wk.dcand.p;
         V.nvis = Wk.nvis.p;
+        V.nseen = Wk.nseen.p;
+        V.dseen = Wk.dseen.p;
         V.nfront[0] = Wk.nfront0.p;
         V.nfront[1] = Wk.nfront1.p;
         V.dvis = Wk.dvis.p;
@@ -559,10 +570,9 @@ static void ensure_resources(Graph &g) {
             for (int j = 0; j < W; j++) {
                 WorkerHost &Wj = g.workers[j];
                 V.ctl_all[j] = Wj.ctl.p;
-                V.nvis_all[j] = Wj.nvis.p;
+                V.nseen_all[j] = Wj.nseen.p;
                 V.nfront_all[0][j] = Wj.nfront0.p;
                 V.nfront_all[1][j] = Wj.nfront1.p;
-                V.nlevel_all[j] = Wj.nlevel.p;
                 V.nparent_all[j] = Wj.nparent.p;
                 V.mask_src[0][j] = Wj.dnext0.p;
                 V.mask_src[1][j] = Wj.dnext1.p;

@@ -41,6 +41,8 @@ constexpr int FW = 8192;       // words of the coarse frontier filter (32 KB, 2^
 #endif
 
 struct Smem {
+    View view;                 // this block's worker View (global copies would be re-fetched from L2
+                               // after every grid barrier's acquire)
     uint32_t list[WPB][LIST];
 #if DBFS_FILTER
     uint32_t filt[FW];         // coarse filter of the pull frontier (when sparse)
@@ -368,30 +370,21 @@ struct VisitCounters {
 };
 
 // Claim normal c of worker `wv` (this worker, or an in-process peer) for
-// level L+1: pre-state check on visited(<= L), then fire-and-forget.
-__device__ __forceinline__ void claim_on(uint32_t *__restrict__ nvis, uint32_t *__restrict__ nx,
-                                         int32_t *__restrict__ nlevel, int64_t *__restrict__ nparent, int parents,
-                                         int L, uint32_t c, int64_t parent, bool check) {
+// level L+1, fire-and-forget.  `seen` is visited(<= L) plus the pushes' claims
+// made so far at level L (the eager copy of the visited bitmap, see
+// push_stage): one L2 test decides; a claim sets it and the next-frontier bit.
+// F copies the folded visited bitmap back into it (pull finds included).
+__device__ __forceinline__ void claim_on(uint32_t *__restrict__ seen, uint32_t *__restrict__ nx,
+                                         int64_t *__restrict__ nparent, int parents, uint32_t c, int64_t parent) {
     const uint32_t wd = c >> 5, bit = 1u << (c & 31);
-    if (check && (nvis[wd] & bit)) return;
-    if (nx[wd] & bit) return;  // already claimed this level (possibly stale: then harmless)
-    atomicOr(&nx[wd], bit);    // result unused -> RED.OR
-    if (parents) nparent[c] = parent;  // the level is written by F3 (word order, coalesced)
+    if (__ldcg(&seen[wd]) & bit) return;  // visited, or claimed this level (possibly stale: then harmless)
+    atomicOr(&seen[wd], bit);             // results unused -> RED.OR
+    atomicOr(&nx[wd], bit);
+    if (parents) nparent[c] = parent;     // the level is written by F3 (word order, coalesced)
 }
 
-__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool check) {
-    claim_on(V.nvis, V.nfront[(L + 1) & 1], V.nlevel, V.nparent, V.parents, L, c, parent, check);
-}
-
-// Mark delegate x found at level L by this worker (delegate mask, comm.py:33-36).
-__device__ __forceinline__ void find_delegate(const View &V, int L, uint32_t x, int64_t parent,
-                                              unsigned long long &dirty) {
-    const uint32_t wd = x >> 5, bit = 1u << (x & 31);
-    uint32_t *dn = V.dnext[L & 1];
-    dirty = 1;
-    if (dn[wd] & bit) return;
-    atomicOr(&dn[wd], bit);
-    if (V.parents) V.dcand[x] = parent;
+__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent) {
+    claim_on(V.nseen, V.nfront[(L + 1) & 1], V.nparent, V.parents, c, parent);
 }
 
 // Remote nn records of one warp step (engine.py:207-222 -> comm.py:138-197):
@@ -447,8 +440,8 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
                 uint32_t old = atomicOr(&V.uq_all[o[u]][(int64_t)grp * nwo + (c[u] >> 5)], 1u << (c[u] & 31));
                 if (!(old & (1u << (c[u] & 31)))) vc.uq++;
             }
-            claim_on(V.nvis_all[o[u]], V.nfront_all[(L + 1) & 1][o[u]], V.nlevel_all[o[u]], V.nparent_all[o[u]],
-                     V.parents, L, c[u], parent[u], true);
+            claim_on(V.nseen_all[o[u]], V.nfront_all[(L + 1) & 1][o[u]], V.nparent_all[o[u]], V.parents, c[u],
+                     parent[u]);
         }
         return;
     }
@@ -538,30 +531,6 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
 
 enum { ACT_NN = 0, ACT_DELEG = 1, ACT_NORMAL = 2 };
 
-// One pushed edge; returns true (with owner/local) when an nn edge is remote.
-template <int ACT>
-__device__ __forceinline__ bool push_edge(const View &V, int L, uint32_t col, int64_t parent, VisitCounters &vc,
-                                          uint32_t &o, uint32_t &c) {
-    if (ACT == ACT_NN) {
-        if (V.p == 1) {
-            claim_normal(V, L, col, parent, true);
-            return false;
-        }
-        o = V.pd.mod(col);
-        c = V.pd.div(col);
-        if ((int)o == V.w) {
-            claim_normal(V, L, c, parent, true);
-            return false;
-        }
-        return true;
-    } else if (ACT == ACT_DELEG) {  // nd / dd: delegate mask (engine.py:225-228, 253-256)
-        if (!tbit(V.dvis, col)) find_delegate(V, L, col, parent, vc.dirty);
-    } else {  // dn: local normal (engine.py:238-241)
-        claim_normal(V, L, col, parent, true);
-    }
-    return false;
-}
-
 // Second stage of a push step: U columns per lane are resolved with all
 // status loads issued before any store (stores through the non-restrict state
 // pointers would otherwise serialise one L2 round trip per edge).
@@ -583,26 +552,37 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
     }
     const uint32_t *vis = ACT == ACT_DELEG ? V.dvis : V.nvis;
     uint32_t *nxt = ACT == ACT_DELEG ? V.dnext[L & 1] : V.nfront[(L + 1) & 1];
-    // stage 1: visited(<= L) words (read-only this phase: L1 is fine)
+    uint32_t *seen = ACT == ACT_DELEG ? V.dseen : V.nseen;
     uint32_t s[U];
+    if (!CNT) {
+        // one L2 test per edge: `seen` = visited(<= L) + the claims of this level
+        // (kept separately from the pre-state `vis`, which pulls and counters
+        // need; F leaves seen == vis for the next level)
 #pragma unroll
-    for (int u = 0; u < U; u++) s[u] = (valid[u] && local[u]) ? __ldca(&vis[tgt[u] >> 5]) : 0xffffffffu;
-    // stage 2: next-level words from L2 (written by other SMs this phase)
+        for (int u = 0; u < U; u++) s[u] = (valid[u] && local[u]) ? __ldcg(&seen[tgt[u] >> 5]) : 0xffffffffu;
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-        bool open = !((s[u] >> (tgt[u] & 31)) & 1u);
-        if (ACT == ACT_DELEG && open) vc.dirty = 1;
-        // counting push: every parent of an unvisited target bids its twin
-        // position, claimed this level or not (the pull stops at the first)
-        if (CNT && open) atomicMin(&first[tgt[u]], tw[u]);
-        s[u] = open ? __ldcg(&nxt[tgt[u] >> 5]) : 0xffffffffu;
+        for (int u = 0; u < U; u++)
+            if (ACT == ACT_DELEG && !((s[u] >> (tgt[u] & 31)) & 1u)) vc.dirty = 1;
+    } else {
+        // counting push: every parent of a target unvisited at level L bids its
+        // twin position, claimed this level or not (the pull stops at the first)
+#pragma unroll
+        for (int u = 0; u < U; u++) s[u] = (valid[u] && local[u]) ? __ldca(&vis[tgt[u] >> 5]) : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            bool open = !((s[u] >> (tgt[u] & 31)) & 1u);
+            if (ACT == ACT_DELEG && open) vc.dirty = 1;
+            if (open) atomicMin(&first[tgt[u]], tw[u]);
+            s[u] = open ? __ldcg(&seen[tgt[u] >> 5]) : 0xffffffffu;
+        }
     }
-    // stage 3: fire-and-forget marks (RED.OR, no return value) and plain stores:
+    // fire-and-forget marks (RED.OR, no return value) and plain stores:
     // concurrent writers of one vertex store the same level and a valid parent.
 #pragma unroll
     for (int u = 0; u < U; u++) {
         const uint32_t x = tgt[u];
         if ((s[u] >> (x & 31)) & 1u) continue;
+        atomicOr(&seen[x >> 5], 1u << (x & 31));
         atomicOr(&nxt[x >> 5], 1u << (x & 31));
         if (ACT == ACT_DELEG) {
             if (V.parents) V.dcand[x] = pp[u];
@@ -1289,7 +1269,10 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
             nw = r & ~dv;
             next_mask[wi] = 0u;
             V.dfront[wi] = nw;
-            if (nw) V.dvis[wi] = dv | nw;
+            if (nw) {
+                V.dvis[wi] = dv | nw;
+                V.dseen[wi] = dv | nw;  // + the other workers' finds (own claims are in it already)
+            }
         }
         {
             uint32_t fold = nw;
@@ -1380,7 +1363,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
                     uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
                     if (!(old & (1u << (rec.x & 31)))) uq++;
                 }
-                claim_normal(V, L, rec.x, (int64_t)rec.y, true);
+                claim_normal(V, L, rec.x, (int64_t)rec.y);
             }
         }
         uq = warp_sum(uq);
@@ -1399,7 +1382,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
             uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
             if (!(old & (1u << (rec.x & 31)))) uq++;
         }
-        claim_normal(V, L, rec.x, (int64_t)rec.y, true);
+        claim_normal(V, L, rec.x, (int64_t)rec.y);
     }
     uq = warp_sum(uq);
     if (lane_id() == 0 && uq) atomicAdd(&V.ctl->s[L % 3].uq_records, uq);
@@ -1421,7 +1404,12 @@ __device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uin
         if (wi >= 0) {
             if (cur[wi]) cur[wi] = 0u;
             nw = nxt[wi];
-            if (nw) V.nvis[wi] |= nw;
+            if (nw) {
+                const uint32_t vis = V.nvis[wi] | nw;
+                V.nvis[wi] = vis;
+                V.nseen[wi] = vis;  // + the pulls' finds (pulls do not mark seen: a push claiming the
+                                    // same vertex again only repeats an idempotent mark)
+            }
         }
         if (!__any_sync(FULL, nw != 0u)) continue;
         {
@@ -1516,6 +1504,7 @@ __device__ void phase_init(const View &V, int wb, int nb) {
     for (int64_t i = tid; i < V.d; i += nth) V.dlevel[i] = -1;
     for (int64_t i = tid; i < V.nw_n; i += nth) {
         V.nvis[i] = 0u;
+        V.nseen[i] = 0u;
         V.nfront[0][i] = 0u;
         V.nfront[1][i] = 0u;
     }
@@ -1529,6 +1518,7 @@ __device__ void phase_init(const View &V, int wb, int nb) {
         for (int64_t i = tid; i < V.nw_g; i += nth) V.sent[i] = 0u;
     for (int64_t i = tid; i < V.nw_d; i += nth) {
         V.dvis[i] = 0u;
+        V.dseen[i] = 0u;
         V.dfront[i] = 0u;
         V.dnext[0][i] = 0u;
         V.dnext[1][i] = 0u;
@@ -1543,6 +1533,7 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         uint32_t x = del_id;
         V.dlevel[x] = 0;
         V.dvis[x >> 5] |= 1u << (x & 31);
+        V.dseen[x >> 5] |= 1u << (x & 31);
         V.dfront[x >> 5] |= 1u << (x & 31);
         V.coarse_d[0][(x >> 10) & (FW - 1)] |= 1u << (x & 31);
         if (V.parents) V.dparent[x] = source;
@@ -1573,6 +1564,7 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         if (V.parents) V.nparent[c] = source;
         V.nfront[0][c >> 5] |= 1u << (c & 31);
         V.nvis[c >> 5] |= 1u << (c & 31);
+        V.nseen[c >> 5] |= 1u << (c & 31);
         V.coarse_n[0][(c >> 10) & (FW - 1)] |= 1u << (c & 31);
         int64_t dnd = V.off[KIND_ND][c + 1] - V.off[KIND_ND][c];
         S.fv[KIND_ND] = dnd;

@@ -79,7 +79,7 @@ struct IterRec {
 };
 
 // Device-visible description of one worker (lives in device memory).
-struct View {
+struct alignas(16) View {
     int w, W, p, p_rank, dist;       // global index, local worker count, shape
     int mode, allow_back, parents;
     int symmetric, exec_policy;      // executor may pull a FORWARD-reported kind (dobfs, symmetric graphs)
@@ -118,6 +118,8 @@ struct View {
     int64_t *dparent;
     int64_t *dcand;
     uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
+    uint32_t *nseen, *dseen;         // visited(<= L) + claims of level L: the push's single test
+    uint32_t *nseen_all[MAXW];       // in-process: peers' seen bits (direct remote claims)
     uint32_t *coarse_d[2], *coarse_n[2];  // coarse frontier filters by level parity
     uint32_t *dlist[2][2];           // delegate frontier per push kind (0 dn, 1 dd) and parity
     int64_t *dpre[2][2];             // exclusive edge prefix of dlist rows
@@ -127,9 +129,7 @@ struct View {
     int64_t sendcap[MAXW];
     Ctl *ctl;
     Ctl *ctl_all[MAXW];              // in-process: every worker's control block
-    uint32_t *nvis_all[MAXW];        // in-process: peers' normal state (direct remote claims)
     uint32_t *nfront_all[2][MAXW];
-    int32_t *nlevel_all[MAXW];
     int64_t *nparent_all[MAXW];
     const uint32_t *mask_src[2][MAXW];
     const int64_t *cand_src[MAXW];
@@ -222,6 +222,7 @@ struct WorkerHost {
     DArray<int32_t> nlevel, dlevel;
     DArray<int64_t> nparent, dparent, dcand;
     DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
+    DArray<uint32_t> nseen, dseen;   // visited + claims of the running level (push test)
     DArray<uint32_t> coarse;         // 4 x 8192 words: coarse_d[0..1], coarse_n[0..1]
     DArray<uint32_t> dlist[4];       // [kind*2 + parity]
     DArray<int64_t> dpre[4];
