@@ -1398,7 +1398,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
     // dbfs_run_stats.accounting_valid): staged on device after each traversal,
     // copied on the copy stream with the root's outputs
     const int rmax = std::min(g.rec_cap, 64);
-    const bool want_rec = o0.record_iterations && !g.dist && st;
+    const bool want_rec = o0.record_iterations && st;
     // batch scratch is kept with the graph and only grows: cudaMalloc /
     // cudaHostAlloc / cudaFree inside the call would synchronise and stall
     DArray<IterRec> &drec = g.batch_drec;
@@ -1605,6 +1605,40 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 r.rows_touched = rows;
                 r.work_inspections = work;
             }
+        }
+    }
+    if (want_rec && g.dist && !aborted) {
+        // one worker per rank: inspections and normal-record bytes are per-rank
+        // partial sums (mask bytes and S' follow the replicated delegate finds)
+        constexpr int F = 11;
+        std::vector<int64_t> h((size_t)count * F, 0);
+        for (int64_t k = 0; k < count; k++) {
+            const dbfs_run_stats &r = st[k];
+            for (int q = 0; q < 4; q++) {
+                h[k * F + 2 * q] = r.inspections[q][0];
+                h[k * F + 2 * q + 1] = r.inspections[q][1];
+            }
+            h[k * F + 8] = r.total_normal_bytes;
+            h[k * F + 9] = r.rows_touched;
+            h[k * F + 10] = r.work_inspections;
+        }
+        DArray<int64_t> t;
+        t.alloc((int64_t)h.size());
+        DBFS_CUDA(cudaMemcpy(t.p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice));
+        nccl_allreduce_i64(ctx, t.p, (int64_t)h.size(), 0);
+        DBFS_CUDA(cudaMemcpy(h.data(), t.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < count; k++) {
+            dbfs_run_stats &r = st[k];
+            for (int q = 0; q < 4; q++) {
+                r.inspections[q][0] = h[k * F + 2 * q];
+                r.inspections[q][1] = h[k * F + 2 * q + 1];
+            }
+            r.total_normal_bytes = h[k * F + 8];
+            r.rows_touched = h[k * F + 9];
+            r.work_inspections = h[k * F + 10];
+            const int64_t bwd = r.inspections[KIND_ND][BWD] + r.inspections[KIND_DD][BWD];
+            r.b_measured = g.d ? (double)bwd / (double)(g.d * g.p) : 0.0;
+            r.accounting_valid = r.iterations <= rmax ? 1 : 0;
         }
     }
     if (aborted && peer) g.peer_state = -1;

@@ -213,14 +213,17 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     (the reference, too, hashes outside its timed region).  Runs are
     pipelined, so a per-run wall clock does not exist: a run's ``teps`` uses
     its device-timed traversal, and the report adds ``wall_s`` (the batch
-    calls, host copies included) and ``e2e_teps`` over all runs.  Distributed
-    graphs and the host-loop engine run ``run_bfs`` per source."""
+    calls, host copies included) and ``e2e_teps`` over all runs.  With one
+    worker per GPU (torchrun) every rank receives the whole level array of
+    every root (assembled over NVLink) and the per-rank counters are summed
+    over ranks after the call.  The host-loop engine runs ``run_bfs`` per
+    source."""
     sources = [int(s) for s in sources]
     for s in sources:
         if not (0 <= s < pg.n):
             raise ValueError(f"source {s} out of range [0, {pg.n})")
     entries, t_total = [], 0.0
-    if pg.nranks > 1 or opts.engine == "host":
+    if opts.engine == "host":
         for s in sources:
             run = run_bfs(pg, dataclasses.replace(opts, source=s))
             t_total += run.elapsed

@@ -92,6 +92,12 @@ for r in roots[:2]:
             local_ok = False
             print(f"rank {rank}: DPG1 round trip differs on {key} for root {r}", flush=True)
 back.close()
+# the reference API benchmark() across ranks (pipelined batch, counters summed over ranks)
+bench_rep = {}
+for opts in (dict(), dict(uniquify=True)):
+    for mode in ("dobfs", "bfs"):
+        rep = api.benchmark(pg, roots, BfsOptions(mode=mode, **opts))
+        bench_rep[(mode, tuple(opts))] = rep["runs"]
 flags = [None] * world
 tdist.all_gather_object(flags, local_ok)
 ok = all(flags)
@@ -106,6 +112,16 @@ if rank == 0:
         print(f"{engine}({used}) {mode} root {r}: digest {'OK' if dg == ref['levels_digest'] else 'MISMATCH'} "
               f"iters {it}/{ref['iterations']} insp {'OK' if insp == ri else (insp, ri)} certificate {bad} "
               f"device {ms:.2f} ms", flush=True)
+    for (mode, opt), runs in bench_rep.items():
+        for run in runs:
+            ref = O.run_bfs(og, run["source"], mode=mode, uniquify="uniquify" in opt)
+            got = (run["levels_digest"], run["iterations"], run["total_inspections"], run["mask_bytes"],
+                   run["normal_bytes"], run["s_prime"])
+            want = (ref["levels_digest"], ref["iterations"], ref["total_inspections"], ref["comm"]["total_mask_bytes"],
+                    ref["comm"]["total_normal_bytes"], ref["comm"]["s_prime"])
+            if got != want:
+                ok = False
+                print(f"benchmark() {mode} {opt} root {run['source']}: {got} != {want}", flush=True)
     print("DIST CHECK", "PASS" if ok else "FAIL", flush=True)
 tdist.barrier()
 tdist.destroy_process_group()
