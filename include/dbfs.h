@@ -14,6 +14,7 @@
  *   dbfs_rmat_generate        <- rmat.generate_rmat / build_rmat_graph   (rmat.py:125-208)
  *   dbfs_graph_build_rmat     <- partition_graph(build_rmat_graph(...))  (partition.py:343-351)
  *   dbfs_graph_build_edges    <- partition_graph(EdgeList, theta, shape) (partition.py:343-351)
+ *   dbfs_graph_upload_partitioned <- a reference PartitionedGraph as is    (partition.py:263-292)
  *   dbfs_graph_export_*       <- PartitionedGraph / WorkerGraph fields    (partition.py:263-292)
  *   dbfs_bfs                  <- engine.run_bfs                           (engine.py:98-330)
  *   dbfs_bfs_batch            <- engine.benchmark's per-source loop       (engine.py:333-364)
@@ -156,6 +157,14 @@ int32_t dbfs_ctx_create(int32_t device, dbfs_ctx **out);
 int32_t dbfs_ctx_destroy(dbfs_ctx *ctx);
 int32_t dbfs_nccl_unique_id(uint8_t *out, int64_t len);       /* len >= 128 */
 int32_t dbfs_ctx_init_dist(dbfs_ctx *ctx, const uint8_t *uid, int64_t len, int32_t nranks, int32_t rank);
+/* One worker per GPU inside ONE process (the reference's ClusterShape(1, P)
+ * partition_graph in one process, partition.py:47-76 / engine.py:149-164): each
+ * rank is a host thread driving its own context; like dbfs_ctx_init_dist, but
+ * the peers' arrays are mapped by pointer with peer access instead of CUDA IPC. */
+int32_t dbfs_ctx_init_local_group(dbfs_ctx *ctx, const uint8_t *uid, int64_t len, int32_t nranks, int32_t rank);
+/* Abort the context's NCCL communicator (another rank of a device group failed):
+ * collectives pending on it return; the context keeps its device but no comm. */
+int32_t dbfs_ctx_abort(dbfs_ctx *ctx);
 int32_t dbfs_ctx_barrier(dbfs_ctx *ctx);
 int32_t dbfs_ctx_flush_l2(dbfs_ctx *ctx);                     /* write 256 MB on the ctx stream, sync */                      /* NCCL all-reduce barrier + stream sync */
 int32_t dbfs_ctx_allreduce_max_f64(dbfs_ctx *ctx, double *inout, int64_t count);
@@ -177,6 +186,20 @@ int32_t dbfs_graph_build_rmat(dbfs_ctx *ctx, const dbfs_rmat_params *params, int
 int32_t dbfs_graph_build_edges(dbfs_ctx *ctx, const int64_t *src, const int64_t *dst, int64_t m,
                                int64_t n, int64_t theta, int32_t p_rank, int32_t p_gpu,
                                dbfs_graph **out);
+/* A partition built elsewhere -- the reference's PartitionedGraph
+ * (partition.py:263-292), e.g. from its partition_graph or load_partitioned_graph
+ * (partition.py:343-351, 424-464) -- uploaded as is (single process, the p
+ * workers on this device): for worker w and kind k in (nn, nd, dn, dd),
+ * row_offsets[w*4+k] is int64[rows+1] (rows = n_local(w) for nn/nd, d for
+ * dn/dd) and col_indices[w*4+k] is int64 (nn) or uint32 (others), the
+ * reference's CsrSubgraph arrays; out_degree int64[n] and the ascending
+ * delegate_global_ids int64[d] are the VertexClassification.  Rows keep their
+ * neighbour order (the BFS counters depend on it).  symmetric: every edge's
+ * reverse is present (graphs from build_rmat_graph with symmetrize). */
+int32_t dbfs_graph_upload_partitioned(dbfs_ctx *ctx, int64_t n, int64_t m, int64_t theta, int32_t p_rank,
+                                      int32_t p_gpu, int64_t d, const int64_t *delegate_global_ids,
+                                      const int64_t *out_degree, const int64_t *const *row_offsets,
+                                      const void *const *col_indices, int32_t symmetric, dbfs_graph **out);
 int32_t dbfs_graph_free(dbfs_graph *g);
 /* Declare the edge multiset symmetric (every (u,v) has its (v,u)); RMAT builds with
  * symmetrize set are symmetric by construction. */
@@ -220,6 +243,10 @@ int32_t dbfs_bfs_batch_output_count(const dbfs_graph *g, int32_t local, int64_t 
 int32_t dbfs_bfs_iteration(const dbfs_graph *g, int64_t it, dbfs_iteration *rec, int8_t *directions,
                            double *bv);
 /* Min-ID parents from the last run's levels, computed on device. */
+/* Send flags of iteration `it` of the last BFS: out[i * p + o] != 0 when local
+ * worker i sent >= 1 normal record to worker o (comm.py:138-197 message
+ * accounting across one-worker-per-GPU ranks). */
+int32_t dbfs_bfs_iteration_sends(const dbfs_graph *g, int64_t it, int64_t *out);
 int32_t dbfs_min_parents(dbfs_graph *g, int64_t *parents_out);
 /* Graph500 certificate over the partitioned edges for the last run's
  * device-resident levels/parents, or for host arrays when given.  *report = 0 when valid,

@@ -105,6 +105,10 @@ SIGNATURES = {
     "dbfs_bfs_batch_output_count": (i32, [vp, i32, P(i64)]),
     "dbfs_bfs_iteration": (i32, [vp, i64, P(IterationC), vp, vp]),
     "dbfs_min_parents": (i32, [vp, vp]),
+    "dbfs_bfs_iteration_sends": (i32, [vp, i64, vp]),
+    "dbfs_ctx_init_local_group": (i32, [vp, vp, i64, i32, i32]),
+    "dbfs_ctx_abort": (i32, [vp]),
+    "dbfs_graph_upload_partitioned": (i32, [vp, i64, i64, i64, i32, i32, i64, vp, vp, vp, vp, i32, P(vp)]),
     "dbfs_validate": (i32, [vp, i64, vp, vp, P(i32)]),
     "dbfs_edges_text_capacity": (i32, [vp, i64, P(i64)]),
     "dbfs_edges_parse_text": (i32, [vp, i64, i64, vp, vp, P(i64), P(i64)]),
@@ -190,6 +194,12 @@ class Context:
         check(load().dbfs_ctx_init_dist(self._h, buf, len(uid), nranks, rank), "init_dist")
         self.nranks, self.rank = nranks, rank
 
+    def init_local_group(self, uid: bytes, nranks: int, rank: int):
+        """Rank `rank` of a one-process device group (dbfs_ctx_init_local_group)."""
+        buf = ctypes.create_string_buffer(uid, len(uid))
+        check(load().dbfs_ctx_init_local_group(self._h, buf, len(uid), nranks, rank), "init_local_group")
+        self.nranks, self.rank = nranks, rank
+
     def barrier(self):
         check(load().dbfs_ctx_barrier(self._h))
 
@@ -198,7 +208,7 @@ class Context:
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:
-            _lib.dbfs_ctx_destroy(self._h)
+            release(_lib.dbfs_ctx_destroy, self._h)
             self._h = None
 
     def __del__(self):
@@ -223,6 +233,57 @@ def default_context() -> Context:
 def set_default_context(ctx: Context):
     global _default_ctx
     _default_ctx = ctx
+
+
+# Releases of device / pinned memory synchronise the GPU(s).  A finalizer can
+# run on whatever thread the garbage collector happens to run on -- including
+# a device-group rank thread (group.py) while the other ranks wait for it in a
+# collective, which would then never finish.  Finalizers therefore release
+# immediately only on the main thread outside device-group calls; otherwise
+# the release is queued and done at the next safe point (drain_releases).
+_deferred = []
+_deferred_lock = threading.Lock()
+_group_depth = 0  # device-group calls in flight (main thread waits inside them)
+
+
+def release(fn, handle):
+    """Call fn(handle) now if that cannot stall a device group, else later."""
+    if threading.current_thread() is threading.main_thread() and _group_depth == 0:
+        fn(handle)
+    else:
+        with _deferred_lock:
+            _deferred.append((fn, handle))
+
+
+def drain_releases():
+    """Run the queued releases (main thread, no device-group call in flight)."""
+    while True:
+        with _deferred_lock:
+            if not _deferred:
+                return
+            items = list(_deferred)
+            _deferred.clear()
+        for fn, handle in items:
+            try:
+                fn(handle)
+            except Exception:
+                pass
+
+
+class group_call:
+    """Context manager around a device-group call (see release)."""
+
+    def __enter__(self):
+        global _group_depth
+        drain_releases()
+        _group_depth += 1
+
+    def __exit__(self, *exc):
+        global _group_depth
+        _group_depth -= 1
+        if _group_depth == 0:
+            drain_releases()
+        return False
 
 
 def nccl_unique_id() -> bytes:
@@ -251,7 +312,7 @@ class PinnedArray:
     def __del__(self):
         try:
             if self._p and _lib is not None:
-                _lib.dbfs_host_free(self._p)
+                release(_lib.dbfs_host_free, self._p)
                 self._p = None
         except Exception:
             pass

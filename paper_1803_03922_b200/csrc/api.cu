@@ -6,7 +6,7 @@
 #include "internal.h"
 
 namespace dbfs {
-int64_t g_kernel_launches = 0;
+std::atomic<int64_t> g_kernel_launches{0};
 
 void *Ctx::ensure_scratch(size_t bytes) {
     if ((size_t)scratch.n < bytes) {
@@ -49,7 +49,7 @@ extern "C" {
 
 const char *dbfs_last_error(void) { return t_err.c_str(); }
 int32_t dbfs_abi_version(void) { return DBFS_ABI_VERSION; }
-int64_t dbfs_kernel_launch_counter(void) { return g_kernel_launches; }
+int64_t dbfs_kernel_launch_counter(void) { return g_kernel_launches.load(); }
 
 int32_t dbfs_device_count(int32_t *out) {
     return guard([&] {
@@ -141,6 +141,18 @@ int32_t dbfs_ctx_init_dist(dbfs_ctx *ctx, const uint8_t *uid, int64_t len, int32
     });
 }
 
+int32_t dbfs_ctx_init_local_group(dbfs_ctx *ctx, const uint8_t *uid, int64_t len, int32_t nranks, int32_t rank) {
+    return guard([&] {
+        DBFS_CHECK(len >= 128 && nranks >= 1 && rank >= 0 && rank < nranks, DBFS_EINVAL, "bad group args");
+        nccl_init(ctx->c, uid, nranks, rank);
+        ctx->c.local_group = 1;
+    });
+}
+
+int32_t dbfs_ctx_abort(dbfs_ctx *ctx) {
+    return guard([&] { nccl_abort(ctx->c); });
+}
+
 int32_t dbfs_ctx_barrier(dbfs_ctx *ctx) {
     return guard([&] {
         DBFS_CUDA(cudaSetDevice(ctx->c.device));
@@ -227,6 +239,28 @@ int32_t dbfs_graph_build_edges(dbfs_ctx *ctx, const int64_t *src, const int64_t 
         init_graph(g->g, ctx, theta, p_rank, p_gpu);
         g->g.n = n;
         build_graph_edges(g->g, src, dst, m);
+    });
+    if (rc) delete g;
+    else *out = g;
+    return rc;
+}
+
+int32_t dbfs_graph_upload_partitioned(dbfs_ctx *ctx, int64_t n, int64_t m, int64_t theta, int32_t p_rank,
+                                      int32_t p_gpu, int64_t d, const int64_t *delegate_global_ids,
+                                      const int64_t *out_degree, const int64_t *const *row_offsets,
+                                      const void *const *col_indices, int32_t symmetric, dbfs_graph **out) {
+    *out = nullptr;
+    dbfs_graph *g = new dbfs_graph();
+    int32_t rc = guard([&] {
+        DBFS_CHECK(n >= 0 && m >= 0 && d >= 0 && d <= n && out_degree && row_offsets && col_indices &&
+                       (delegate_global_ids || d == 0),
+                   DBFS_EINVAL, "bad arguments");
+        init_graph(g->g, ctx, theta, p_rank, p_gpu);
+        g->g.n = n;
+        g->g.m = m;
+        g->g.d = d;
+        upload_partitioned(g->g, out_degree, delegate_global_ids, row_offsets, col_indices);
+        g->g.symmetric = symmetric != 0;
     });
     if (rc) delete g;
     else *out = g;
@@ -348,6 +382,18 @@ int32_t dbfs_bfs_iteration(const dbfs_graph *gg, int64_t it, dbfs_iteration *rec
         int64_t nrec = (int64_t)g.last_rec.size() / std::max(g.W, 1);
         DBFS_CHECK(it >= 0 && it < nrec, DBFS_ERANGE, "iteration out of range (or truncated)");
         iteration_summary(g, &g.last_rec[(size_t)it * g.W], it, g.last_la, g.last_uq, rec, directions, bv);
+    });
+}
+
+int32_t dbfs_bfs_iteration_sends(const dbfs_graph *gg, int64_t it, int64_t *out) {
+    return guard([&] {
+        const Graph &g = gg->g;
+        DBFS_CHECK(g.last_valid, DBFS_EINVAL, "no BFS has run");
+        int64_t nrec = (int64_t)g.last_rec.size() / std::max(g.W, 1);
+        DBFS_CHECK(it >= 0 && it < nrec, DBFS_ERANGE, "iteration out of range (or truncated)");
+        for (int i = 0; i < g.W; i++)
+            for (int o = 0; o < g.p; o++)
+                out[(size_t)i * g.p + o] = (int64_t)g.last_rec[(size_t)it * g.W + i].send[o];
     });
 }
 

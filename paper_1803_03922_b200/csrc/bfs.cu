@@ -8,6 +8,7 @@
 //               used with one worker per process (torchrun, NCCL over NVLink).
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <thread>
 
@@ -595,13 +596,20 @@ static void ensure_resources(Graph &g) {
     (void)ctx;
 }
 
+// Dynamic shared-memory limits are per device: a process may drive several
+// GPUs (group.py runs one host thread per device).
 static void set_smem_attrs() {
-    static bool done = false;
-    if (done) return;
+    static std::mutex mu;
+    static std::vector<char> done;
+    int dev = 0;
+    DBFS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if ((int)done.size() <= dev) done.resize(dev + 1, 0);
+    if (done[dev]) return;
     DBFS_CUDA(cudaFuncSetAttribute(k_bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
     DBFS_CUDA(cudaFuncSetAttribute(k_visit, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
     DBFS_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(Smem)));
-    done = true;
+    done[dev] = 1;
 }
 
 static int persistent_grid(Graph &g, int *blocks_per_sm) {
@@ -719,6 +727,8 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
 // stored into fixed per-sender segments of the owner's inbox, and levels are
 // separated by a system-scope barrier in rank 0's memory.  Collective; every
 // rank agrees on the outcome (the host-loop NCCL engine is the fallback).
+static void finish_peer_setup(Graph &g, const std::vector<void *> &ptr);
+
 static void setup_peer(Graph &g) {
     if (g.peer_state) return;
     g.peer_state = -1;
@@ -732,6 +742,49 @@ static void setup_peer(Graph &g) {
     constexpr int NH = 9;
     void *bases[NH] = {Wk.ctl.p,    Wk.dnext0.p,  Wk.dnext1.p,  Wk.dcand.p,    Wk.inbox0.p,
                        Wk.nlevel.p, Wk.nparent.p, Wk.dparent.p, g.gbar_mem.p};
+    if (ctx.local_group) {
+        // ranks are threads of this process: exchange raw device pointers (and
+        // device ordinals) and enable peer access instead of CUDA IPC
+        struct Rec {
+            void *ptr[NH];
+            int64_t dev;
+        } me_rec{}, *all_rec = nullptr;
+        for (int i = 0; i < NH; i++) me_rec.ptr[i] = bases[i];
+        me_rec.dev = ctx.device;
+        std::vector<Rec> recs(p);
+        DArray<uint8_t> hs, hr;
+        hs.alloc(sizeof(Rec));
+        hr.alloc(sizeof(Rec) * p);
+        DBFS_CUDA(cudaMemcpy(hs.p, &me_rec, sizeof(Rec), cudaMemcpyHostToDevice));
+        nccl_allgather_bytes(ctx, hs.p, hr.p, sizeof(Rec));
+        DBFS_CUDA(cudaMemcpy(recs.data(), hr.p, sizeof(Rec) * p, cudaMemcpyDeviceToHost));
+        all_rec = recs.data();
+        int lok = ok;
+        for (int j = 0; j < p && lok; j++) {
+            if (j == me) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, ctx.device, (int)all_rec[j].dev) != cudaSuccess || !can) {
+                cudaGetLastError();
+                lok = 0;
+                break;
+            }
+            cudaError_t e = cudaDeviceEnablePeerAccess((int)all_rec[j].dev, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) lok = 0;
+            cudaGetLastError();
+        }
+        DArray<uint32_t> f;
+        f.alloc(1);
+        uint32_t h = lok ? 1u : 0u;
+        DBFS_CUDA(cudaMemcpy(f.p, &h, 4, cudaMemcpyHostToDevice));
+        nccl_allreduce_u32_sum(ctx, f.p, 1);
+        DBFS_CUDA(cudaMemcpy(&h, f.p, 4, cudaMemcpyDeviceToHost));
+        if ((int)h != p) return;
+        std::vector<void *> ptr((size_t)NH * p, nullptr);
+        for (int j = 0; j < p; j++)
+            for (int i = 0; i < NH; i++) ptr[(size_t)j * NH + i] = all_rec[j].ptr[i];
+        finish_peer_setup(g, ptr);
+        return;
+    }
     std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * p);
     for (int i = 0; i < NH && ok; i++)
         if (cudaIpcGetMemHandle(&mine[i], bases[i]) != cudaSuccess) {
@@ -777,6 +830,16 @@ static void setup_peer(Graph &g) {
         g.peer_opened.clear();
         return;
     }
+    finish_peer_setup(g, ptr);
+}
+
+// Peer engine view from every rank's mapped arrays ptr[rank * 9 + i] (i: ctl,
+// dnext0, dnext1, dcand, inbox0, nlevel, nparent, dparent, barrier).
+static void finish_peer_setup(Graph &g, const std::vector<void *> &ptr) {
+    Ctx &ctx = *g.ctx;
+    const int p = g.p, me = ctx.rank;
+    constexpr int NH = 9;
+    WorkerHost &Wk = g.workers[0];
     View V = g.views_h[0];
     V.peer = 1;
     V.dist = 1;
@@ -1521,7 +1584,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 DBFS_CUDA(cudaEventSynchronize(ctx.ev_hdone[hb]));
                 const double tw1 = btrace ? now_ms() : 0;
                 if (g.hesc[hb]) rerun.push_back(j);
-                else widen_result(g.hstage8[hb], nullptr, nout, levels[j], nullptr, host_threads);
+                else if (levels[j]) widen_result(g.hstage8[hb], nullptr, nout, levels[j], nullptr, host_threads);
                 if (btrace) {
                     t_wait += tw1 - tw0;
                     t_widen += now_ms() - tw1;

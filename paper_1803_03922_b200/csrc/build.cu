@@ -511,6 +511,94 @@ static void classify(Graph &g) {
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
+// A partition built elsewhere (the reference's PartitionedGraph,
+// partition.py:263-292, or a DPG1 file set) straight into the device layout:
+// per worker the four CSRs (int64 offsets; int64 nn / uint32 other columns),
+// concatenated in the composite row order [w][nn | nd | dn | dd] with absolute
+// offsets, then the same per-worker aids (source bitmaps, row lengths) the
+// device build derives.  No edge list, no re-sort: the rows keep the caller's
+// neighbour order, which the BFS counters depend on.
+void upload_partitioned(Graph &g, const int64_t *degree, const int64_t *dgid, const int64_t *const *off,
+                        const void *const *cols) {
+    Ctx &ctx = *g.ctx;
+    const int p = g.p;
+    const int64_t n = g.n, d = g.d;
+    DBFS_CHECK(ctx.nranks == 1, DBFS_EINVAL, "upload builds a single-process partition");
+    DBFS_CHECK(p >= 1 && p <= MAXW, DBFS_ECAPACITY, "at most 64 workers");
+    DBFS_CHECK(ceil_div(n, p) < ((int64_t)1 << 32) && d < ((int64_t)1 << 32) - 1, DBFS_ECAPACITY,
+               "local id space exceeds 32 bits");
+    // classification: degrees, delegate ids (ascending global ids)
+    {
+        std::vector<uint32_t> h((size_t)std::max<int64_t>(n, 1), 0);
+        for (int64_t v = 0; v < n; v++) {
+            DBFS_CHECK(degree[v] >= 0 && degree[v] < ((int64_t)1 << 32), DBFS_ECAPACITY, "degree exceeds 32 bits");
+            h[v] = (uint32_t)degree[v];
+        }
+        g.degree.alloc(std::max<int64_t>(n, 1));
+        DBFS_CUDA(cudaMemcpy(g.degree.p, h.data(), 4 * (size_t)std::max<int64_t>(n, 1), cudaMemcpyHostToDevice));
+        std::fill(h.begin(), h.end(), 0xffffffffu);
+        for (int64_t x = 0; x < d; x++) {
+            DBFS_CHECK(dgid[x] >= 0 && dgid[x] < n && (x == 0 || dgid[x] > dgid[x - 1]), DBFS_ESTRUCT,
+                       "delegate ids must be ascending global ids");
+            h[dgid[x]] = (uint32_t)x;
+        }
+        g.del_id.alloc(std::max<int64_t>(n, 1));
+        DBFS_CUDA(cudaMemcpy(g.del_id.p, h.data(), 4 * (size_t)std::max<int64_t>(n, 1), cudaMemcpyHostToDevice));
+        g.del_gid.alloc(std::max<int64_t>(d, 1));
+        if (d) DBFS_CUDA(cudaMemcpy(g.del_gid.p, dgid, 8 * d, cudaMemcpyHostToDevice));
+    }
+    // composite layout and absolute offsets
+    g.workers.resize(p);
+    std::vector<int64_t> wbase((size_t)p * 4);
+    int64_t nkeys = 0, m = 0;
+    for (int w = 0; w < p; w++) {
+        g.workers[w].w = w;
+        g.workers[w].n_local = n_local_of(n, p, w);
+        for (int k = 0; k < 4; k++) {
+            const int64_t rows = k < 2 ? g.workers[w].n_local : d;
+            const int64_t *o = off[(size_t)w * 4 + k];
+            DBFS_CHECK(o[0] == 0, DBFS_ESTRUCT, "row offsets must start at 0");
+            for (int64_t r = 0; r < rows; r++)
+                DBFS_CHECK(o[r + 1] >= o[r], DBFS_ESTRUCT, "row offsets must be non-decreasing");
+            wbase[(size_t)w * 4 + k] = nkeys;
+            nkeys += rows;
+            m += o[rows];
+        }
+    }
+    DBFS_CHECK(m == g.m, DBFS_ESTRUCT, "the workers' CSRs must hold the graph's m edges");
+    DBFS_CHECK(nkeys < ((int64_t)1 << 32), DBFS_ECAPACITY, "composite row space exceeds 32 bits");
+    std::vector<int64_t> hoff((size_t)nkeys + 1);
+    std::vector<uint32_t> hcol((size_t)std::max<int64_t>(m, 1));
+    int64_t acc = 0;
+    for (int k = 0; k < 4; k++) g.kind_totals[k] = 0;
+    for (int w = 0; w < p; w++) {
+        for (int o = 0; o < MAXW; o++) g.workers[w].remote_cap[o] = 0;
+        for (int k = 0; k < 4; k++) {
+            const int64_t rows = k < 2 ? g.workers[w].n_local : d;
+            const int64_t *o = off[(size_t)w * 4 + k];
+            const int64_t base = wbase[(size_t)w * 4 + k];
+            for (int64_t r = 0; r < rows; r++) hoff[base + r] = acc + o[r];
+            const int64_t nnz = o[rows];
+            const int64_t lim = k == KIND_NN ? n : (k == KIND_DN ? g.workers[w].n_local : d);
+            for (int64_t j = 0; j < nnz; j++) {
+                const int64_t c = k == KIND_NN ? static_cast<const int64_t *>(cols[(size_t)w * 4 + k])[j]
+                                               : (int64_t) static_cast<const uint32_t *>(cols[(size_t)w * 4 + k])[j];
+                DBFS_CHECK(c >= 0 && c < lim, DBFS_ESTRUCT, "column out of range for its kind");
+                hcol[acc + j] = (uint32_t)c;
+                if (k == KIND_NN && (int)(c % p) != w) g.workers[w].remote_cap[c % p]++;
+            }
+            acc += nnz;
+            g.kind_totals[k] += nnz;
+        }
+    }
+    hoff[nkeys] = acc;
+    g.off_all.alloc(nkeys + 1);
+    DBFS_CUDA(cudaMemcpy(g.off_all.p, hoff.data(), 8 * hoff.size(), cudaMemcpyHostToDevice));
+    g.col_all.alloc(std::max<int64_t>(m, 1));
+    if (m) DBFS_CUDA(cudaMemcpy(g.col_all.p, hcol.data(), 4 * (size_t)m, cudaMemcpyHostToDevice));
+    finish_workers(g, nkeys, wbase);
+}
+
 static void build_dist(Graph &g, const EdgeSrc &es, int64_t begin, int64_t end);
 
 void mem_note(const Ctx &ctx, const char *what) {

@@ -1,5 +1,6 @@
 // common.cuh -- shared helpers for libdbfs (sm_100a).
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,7 +33,7 @@ struct Error : std::runtime_error {
 
 // Every kernel launch in the library goes through this counter so callers can
 // report how many of *our* kernels ran (bench.py "gpu_launches").
-extern int64_t g_kernel_launches;
+extern std::atomic<int64_t> g_kernel_launches;  // several host threads may launch (group.py)
 inline void note_launch(int64_t k = 1) { g_kernel_launches += k; }
 #define DBFS_LAUNCHED()                          \
     do {                                         \

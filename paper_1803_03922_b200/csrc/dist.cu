@@ -40,6 +40,13 @@ void nccl_init(Ctx &ctx, const uint8_t *uid, int nranks, int rank) {
     ctx.rank = rank;
 }
 
+// Another rank failed: unblock this rank's pending collectives (NCCL kernels
+// see the abort flag and exit); the communicator is unusable afterwards.
+void nccl_abort(Ctx &ctx) {
+    if (ctx.comm) ncclCommAbort((ncclComm_t)ctx.comm);
+    ctx.comm = nullptr;
+}
+
 void nccl_destroy(Ctx &ctx) {
     if (ctx.comm) ncclCommDestroy((ncclComm_t)ctx.comm);
     ctx.comm = nullptr;

@@ -192,6 +192,8 @@ struct Ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int nranks = 1, rank = 0;
+    int local_group = 0;             // every rank is a thread of this process (one device each):
+                                     // peer arrays are mapped by pointer + peer access, not CUDA IPC
     void *comm = nullptr;            // ncclComm_t
     DArray<unsigned char> scratch;   // reusable device scratch
     DArray<unsigned char> flush;     // L2 flush buffer (bench hygiene)
@@ -308,6 +310,8 @@ void mem_note(const Ctx &ctx, const char *what);  // DBFS_VERBOSE=1: free device
 void build_graph_rmat(Graph &g, const dbfs_rmat_params &prm);
 void build_graph_edges(Graph &g, const int64_t *src, const int64_t *dst, int64_t m_local);
 void build_twins(Graph &g);
+void upload_partitioned(Graph &g, const int64_t *degree, const int64_t *dgid, const int64_t *const *off,
+                        const void *const *cols);
 void export_csr(const Graph &g, int worker, int kind, int64_t *off, void *cols);
 void export_sources(const Graph &g, int worker, int64_t *nd_src, uint8_t *dn, uint8_t *dd);
 void export_classification(const Graph &g, int64_t *deg, int64_t *del);
@@ -332,6 +336,7 @@ int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *paren
 void nccl_unique_id(uint8_t *out);
 void nccl_init(Ctx &ctx, const uint8_t *uid, int nranks, int rank);
 void nccl_destroy(Ctx &ctx);
+void nccl_abort(Ctx &ctx);
 void nccl_allreduce_u32_sum(Ctx &ctx, uint32_t *dbuf, int64_t count);
 void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op);  // 0 sum, 1 min, 2 max
 void nccl_allreduce_f64_max(Ctx &ctx, double *dbuf, int64_t count);

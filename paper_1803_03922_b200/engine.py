@@ -176,8 +176,16 @@ def _per_iteration(pg: PartitionedGraph, iterations: int):
     return recs, comm
 
 
+def _group(pg):
+    from .group import GroupPartitionedGraph
+    return isinstance(pg, GroupPartitionedGraph)
+
+
 def run_bfs(pg: PartitionedGraph, opts: BfsOptions) -> BfsRun:
     """One BFS/DOBFS on the GPU with the reference's result (engine.py:98-330)."""
+    if _group(pg):
+        from . import group
+        return group.run_bfs(pg, opts)
     t0 = time.perf_counter()
     n = pg.n
     if not (0 <= opts.source < n):
@@ -292,6 +300,14 @@ def bfs(pg: PartitionedGraph, root: int, parents: str = "any", mode: str = "dobf
     if parents not in ("any", "min"):
         raise ValueError("parents must be 'any' or 'min'")
     opts = BfsOptions(mode=mode, source=int(root), parents=parents)
+    if _group(pg):
+        from . import group
+        lv, pa, st = group.bfs(pg, root, opts)
+        if out is not None:
+            out[0][:pg.n] = lv
+            out[1][:pg.n] = pa
+            lv, pa = out
+        return (lv, pa, st) if stats else (lv, pa)
     if out is None:
         levels = np.empty(pg.n, dtype=np.int32)
         par = np.empty(pg.n, dtype=np.int64)
@@ -340,6 +356,13 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
         if not (0 <= r < pg.n):
             raise ValueError(f"source {r} out of range [0, {pg.n})")
     count = len(roots)
+    if _group(pg):
+        from . import group
+        if outs is None:
+            outs = [(np.empty(pg.n, dtype=np.int32), np.empty(pg.n, dtype=np.int64) if parents else None)
+                    for _ in range(count)]
+        return group.bfs_batch(pg, list(roots), outs, mode=mode, parents=parents, stats=stats, compact=compact,
+                               options=options, accounting=accounting)
     nout = batch_output_count(pg, local)
     if outs is None:
         outs = [(np.empty(nout, dtype=np.int32), np.empty(nout, dtype=np.int64) if parents else None)
@@ -370,6 +393,8 @@ def bfs_batch(pg: PartitionedGraph, roots, outs=None, mode: str = "dobfs", paren
 def batch_output_count(pg: PartitionedGraph, local: bool = False) -> int:
     """Entries per output array of ``bfs_batch``: n, or this rank's own vertex
     count when ``local`` in a distributed run."""
+    if _group(pg):
+        return pg.n
     c = ctypes.c_int64()
     _lib.check(_lib.load().dbfs_bfs_batch_output_count(pg.handle, int(bool(local)), ctypes.byref(c)))
     return int(c.value)
@@ -378,11 +403,17 @@ def batch_output_count(pg: PartitionedGraph, local: bool = False) -> int:
 def bfs_device(pg: PartitionedGraph, root: int, mode: str = "dobfs", parents: str | None = "any",
                exec_policy: str = "cost"):
     """One BFS leaving depth/parents in device memory (for timing); returns run stats."""
+    if _group(pg):
+        o = BfsOptions(mode=mode, source=int(root), parents=parents, exec_policy=exec_policy)
+        return pg.group.map(lambda r: _bfs_raw(pg.parts[r], o, None, None))[0]
     return _bfs_raw(pg, BfsOptions(mode=mode, source=int(root), parents=parents, exec_policy=exec_policy), None, None)
 
 
 def min_parents(pg: PartitionedGraph) -> np.ndarray:
     """Min-ID parents of the last BFS, computed on the GPU."""
+    if _group(pg):
+        from . import group
+        return group.min_parents(pg)
     out = np.empty(pg.n, dtype=np.int64)
     _lib.check(_lib.load().dbfs_min_parents(pg.handle, out.ctypes.data_as(_lib.vp)), "min_parents")
     return out
@@ -394,6 +425,9 @@ def validate_bfs_tree(pg: PartitionedGraph, root: int, levels=None, parents=None
     16 tree edge not in E, 32 parent of unreached / missing parent."""
     if not (0 <= root < pg.n):
         raise ValueError(f"root {root} out of range [0, {pg.n})")
+    if _group(pg):
+        from . import group
+        return group.validate(pg, root, levels, parents)
     rep = ctypes.c_int32()
     lva = pa_ = None
     if levels is not None:

@@ -215,7 +215,7 @@ class PartitionedGraph:
 
     def close(self):
         if getattr(self, "_h", None) and _lib._lib is not None:
-            _lib._lib.dbfs_graph_free(self._h)
+            _lib.release(_lib._lib.dbfs_graph_free, self._h)
             self._h = None
 
     def __del__(self):
@@ -226,14 +226,30 @@ class PartitionedGraph:
 
 
 def partition_graph(g: EdgeList, theta: int, shape: ClusterShape, verify: bool = False,
-                    ctx=None) -> PartitionedGraph:
+                    ctx=None, devices="auto") -> PartitionedGraph:
     """Classification + distribution + CSR build on the GPU (partition.py:343-351).
 
     ``verify`` keeps the reference signature; the structural checks of
     verify_buckets are asserted by the GPU build itself (kind totals == m).
+
+    A shape of p > 1 workers goes on p GPUs of this process when that many
+    are visible and the graph has >= 2^20 vertices (``devices="auto"``; a
+    list picks the GPUs for any size): worker w on GPU w, one host thread per
+    GPU, the peer engine over NVLink (``group.py``).
+    Otherwise -- one GPU, ``devices=None``, ``DBFS_DEVICE_GROUP=0``, or a
+    torchrun rank's context -- the p workers are simulated on one device, as
+    the reference simulates them in one process.
     """
     if theta < 0:
         raise ValueError("theta must be >= 0")
+    if ctx is None and shape.p > 1 and not (_lib._default_ctx is not None and _lib._default_ctx.nranks > 1):
+        from .group import group_for, partition_group
+        grp = group_for(shape.p, devices, int(g.n))
+        if grp is not None:
+            pg = partition_group(g, theta, shape, grp)
+            if verify and sum(pg.kind_totals.values()) != pg.m:
+                raise BucketViolation("edge conservation violated")
+            return pg
     ctx = ctx or _lib.default_context()
     L = _lib.load()
     h = _lib.vp()
@@ -257,6 +273,54 @@ def partition_graph(g: EdgeList, theta: int, shape: ClusterShape, verify: bool =
     if verify and sum(pg.kind_totals.values()) != pg.m:
         raise BucketViolation("edge conservation violated")
     return pg
+
+
+def upload_partitioned_graph(ref_pg, ctx=None, symmetric: bool = False, shape: ClusterShape | None = None,
+                             theta: int | None = None) -> PartitionedGraph:
+    """A partition built elsewhere -- the reference's own PartitionedGraph
+    (partition.py:263-292, from its partition_graph or load_partitioned_graph)
+    or any object with the same fields -- onto the device as is
+    (``dbfs_graph_upload_partitioned``): no edge list, no rebuild; every row
+    keeps its neighbour order.  ``symmetric`` declares that every edge's
+    reverse is present (build_rmat_graph with symmetrize): it enables the
+    executor's pull / counting-push substitutions, so only set it when true.
+    ``shape`` / ``theta`` default to the object's ``shape`` and
+    ``classification.theta``."""
+    shape = shape or ref_pg.shape
+    cls = ref_pg.classification
+    theta = int(cls.theta if theta is None else theta)
+    n, m, p = int(ref_pg.n), int(ref_pg.m), shape.p
+    if len(ref_pg.workers) != p:
+        raise ValueError(f"{len(ref_pg.workers)} workers for a {p}-worker shape")
+    dg = np.ascontiguousarray(cls.delegate_global_ids, dtype=np.int64)
+    deg = getattr(cls, "out_degree", None)
+    if deg is None:  # e.g. a partition loaded from DPG1 files: degrees from the rows
+        deg = np.zeros(n, dtype=np.int64)
+        for w in sorted(ref_pg.workers, key=lambda x: x.index):
+            for k in KINDS:
+                csr = w.subgraph(k)
+                lens = np.diff(np.asarray(csr.row_offsets, dtype=np.int64))
+                rows = (np.arange(len(lens), dtype=np.int64) * p + w.index) if k in ("nn", "nd") else dg[:len(lens)]
+                np.add.at(deg, rows, lens)
+    deg = np.ascontiguousarray(deg, dtype=np.int64)
+    keep, offs, cols = [], [], []
+    for w in sorted(ref_pg.workers, key=lambda x: x.index):
+        for k in KINDS:
+            csr = w.subgraph(k)
+            o = np.ascontiguousarray(csr.row_offsets, dtype=np.int64)
+            c = np.ascontiguousarray(csr.col_indices, dtype=np.int64 if k == "nn" else np.uint32)
+            keep += [o, c]
+            offs.append(o.ctypes.data)
+            cols.append(c.ctypes.data)
+    ctx = ctx or _lib.default_context()
+    h = _lib.vp()
+    off_arr = (_lib.vp * len(offs))(*offs)
+    col_arr = (_lib.vp * len(cols))(*cols)
+    _lib.check(_lib.load().dbfs_graph_upload_partitioned(
+        ctx.handle, n, m, theta, shape.p_rank, shape.p_gpu, len(dg), dg.ctypes.data_as(_lib.vp),
+        deg.ctypes.data_as(_lib.vp), off_arr, col_arr, int(bool(symmetric)), ctypes.byref(h)), "upload_partitioned")
+    del keep
+    return PartitionedGraph(h, ctx, shape)
 
 
 # ---------------------------------------------------------------------------
@@ -372,7 +436,10 @@ def load_partitioned_graph(directory, symmetric: bool | None = None, verify: boo
                            ctx=None) -> PartitionedGraph:
     """Read DPG1 worker files back into a device partition (partition.py:424-464).
 
-    Every worker's CSR entries are replayed as global (src, dst) edges --
+    In one process with ``symmetric`` given, the files' CSR arrays are
+    uploaded as they are (``upload_partitioned_graph``).  Otherwise (a
+    distributed context, or ``symmetric=None``, which checks the edge
+    multiset on the host) every worker's CSR entries are replayed as global (src, dst) edges --
     workers in index order, kinds nn, nd, dn, dd, rows ascending, columns in
     stored order -- and fed to the GPU build (``dbfs_graph_build_edges``) with
     the stored theta and shape.  That edge list is the partition's own edge
@@ -407,19 +474,28 @@ def load_partitioned_graph(directory, symmetric: bool | None = None, verify: boo
     if ctx.nranks == 1 and sorted(wf.index for wf in wfs) != list(range(shape.p)):
         raise ValueError(f"{directory}: expected workers 0..{shape.p - 1}")
     wfs.sort(key=lambda wf: wf.index)
-    parts = [_worker_edges(wf, shape.p) for wf in wfs]
-    src = np.concatenate([a for a, _ in parts]) if parts else np.zeros(0, np.int64)
-    dst = np.concatenate([b for _, b in parts]) if parts else np.zeros(0, np.int64)
-    if symmetric is None:
-        symmetric = _is_symmetric(src, dst, n, ctx)
-    L = _lib.load()
-    h = _lib.vp()
-    _lib.check(L.dbfs_graph_build_edges(ctx.handle, src.ctypes.data_as(_lib.vp), dst.ctypes.data_as(_lib.vp),
-                                        len(src), int(n), int(theta), p_rank, p_gpu, ctypes.byref(h)),
-               "graph_build_edges")
-    if symmetric:
-        _lib.check(L.dbfs_graph_set_symmetric(h, 1))
-    pg = PartitionedGraph(h, ctx, shape)
+    if ctx.nranks == 1 and symmetric is not None:
+        # single process: the files' arrays go to the device as they are
+        from types import SimpleNamespace
+        ref = SimpleNamespace(
+            shape=shape, n=n, m=m,
+            classification=SimpleNamespace(theta=theta, out_degree=None, delegate_global_ids=wfs[0].del_gid),
+            workers=[SimpleNamespace(index=wf.index, subgraph=(lambda k, wf=wf: wf.csr[k])) for wf in wfs])
+        pg = upload_partitioned_graph(ref, ctx=ctx, symmetric=bool(symmetric))
+    else:
+        parts = [_worker_edges(wf, shape.p) for wf in wfs]
+        src = np.concatenate([a for a, _ in parts]) if parts else np.zeros(0, np.int64)
+        dst = np.concatenate([b for _, b in parts]) if parts else np.zeros(0, np.int64)
+        if symmetric is None:
+            symmetric = _is_symmetric(src, dst, n, ctx)
+        L = _lib.load()
+        h = _lib.vp()
+        _lib.check(L.dbfs_graph_build_edges(ctx.handle, src.ctypes.data_as(_lib.vp), dst.ctypes.data_as(_lib.vp),
+                                            len(src), int(n), int(theta), p_rank, p_gpu, ctypes.byref(h)),
+                   "graph_build_edges")
+        if symmetric:
+            _lib.check(L.dbfs_graph_set_symmetric(h, 1))
+        pg = PartitionedGraph(h, ctx, shape)
     if pg.m != m or pg.classification.d != d:
         raise ValueError(f"{directory}: rebuilt partition disagrees with the files (m {pg.m} vs {m}, "
                          f"d {pg.classification.d} vs {d})")

@@ -164,3 +164,43 @@ def test_dpg_errors(tmp_path, api):
     (tmp_path / "worker_00000.dpg").write_bytes(b"XXXX" + bytes(64))
     with pytest.raises(ValueError, match="bad magic"):
         load_partitioned_graph(tmp_path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1, 1), (2, 1), (2, 2), (4, 2)])
+def test_upload_reference_shaped_partition(shape):
+    """dbfs_graph_upload_partitioned: a partition built elsewhere (here the
+    oracle's restatement of the reference's partition_graph, in the reference's
+    PartitionedGraph shape) goes to the device as is; BFS reports equal the
+    oracle's, the exported arrays equal the uploaded ones, with and without
+    out_degree (DPG1 files carry none)."""
+    from types import SimpleNamespace
+
+    import paper_1803_03922_b200 as api
+    from paper_1803_03922_b200 import _lib
+    if _lib.device_count() == 0:
+        pytest.fail("no CUDA device visible for a -m gpu test")
+    scale, seed, theta = 12, 3, 16
+    src, dst = O.rmat_edges(scale, seed=seed)
+    og = O.partition(src, dst, 1 << scale, theta, *shape)
+    for with_degree in (True, False):
+        ref = SimpleNamespace(
+            shape=api.ClusterShape(*shape), n=og.n, m=og.m,
+            classification=SimpleNamespace(theta=theta, out_degree=og.degrees if with_degree else None,
+                                           delegate_global_ids=og.delegate_global_ids),
+            workers=[SimpleNamespace(index=w.index, subgraph=(lambda k, w=w: getattr(w, k))) for w in og.workers])
+        pg = api.upload_partitioned_graph(ref, symmetric=True)
+        assert pg.classification.d == og.d and pg.kind_totals == og.kind_totals
+        assert np.array_equal(pg.classification.out_degree, og.degrees)
+        for w, ow in zip(pg.workers, og.workers):
+            for k in ("nn", "nd", "dn", "dd"):
+                assert np.array_equal(w.subgraph(k).row_offsets, getattr(ow, k).row_offsets)
+                assert np.array_equal(w.subgraph(k).col_indices, getattr(ow, k).col_indices)
+            assert np.array_equal(w.nd_source_list, ow.nd_source_list)
+        for root in (7, 100, 4000):
+            for mode in ("dobfs", "bfs"):
+                got = api.run_bfs(pg, api.BfsOptions(mode=mode, source=root)).to_dict()
+                want = O.run_bfs(og, root, mode=mode)
+                for key in ("levels_digest", "iterations", "per_iteration", "inspections", "comm"):
+                    assert got[key] == want[key], (shape, root, mode, key)
+        pg.close()
