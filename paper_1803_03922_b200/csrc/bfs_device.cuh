@@ -1192,17 +1192,20 @@ __device__ __forceinline__ void take_first(uint32_t *first, uint32_t x, uint64_t
     }
 }
 
-// Delegate state of new delegate x (lane-held): level, parent, global output,
-// push-list row lengths.
-__device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, uint64_t &ldn, uint64_t &ldd) {
+// Delegate state of new delegate x (lane-held): level, parent, global output.
+// gx = its global id (loaded when the global outputs are written here), par =
+// its parent when the caller already has it (one in-process worker), else
+// the minimum over the candidates of the workers that found it.
+constexpr int NB_DEL = 4;  // new delegates per lane whose loads are in flight together (F1)
+
+__device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, int64_t gx, int64_t par_known) {
     const uint32_t xw = x >> 5, xb = x & 31;
-    ldn = __ldg(&V.deg[KIND_DN][x]);
-    ldd = __ldg(&V.deg[KIND_DD][x]);
-    const int64_t gx = V.glevel ? __ldg(&V.del_gid[x]) : 0;
     V.dlevel[x] = L + 1;
     int64_t par = 0x7fffffffffffffffLL;
     if (V.parents) {
-        if (V.cand_all) {
+        if (V.cand_all && V.P_sources == 1) {
+            par = par_known;
+        } else if (V.cand_all) {
             for (int s = 0; s < V.P_sources; s++)
                 if ((__ldcg(&V.mask_src[L & 1][s][xw]) >> xb) & 1u) {
                     int64_t c = __ldcg(&V.cand_src[s][x]);
@@ -1282,20 +1285,38 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         }
         unsigned cnt = warp_compact(nw, wi, list);
         if (!cnt) continue;
-        // pass A: state + totals
+        // pass A: state + totals, NB delegates per lane at a time with every
+        // load of the batch issued before any store (stores through the state
+        // pointers would otherwise keep the compiler from overlapping them)
         unsigned long long cdn = 0, edn = 0, cdd = 0, edd = 0;
-#pragma unroll 4
-        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
-            unsigned i = g0 + lane;
-            if (i < cnt) {
-                uint64_t ldn, ldd;
-                new_delegate(V, L, list[i], ldn, ldd);
-                if (cnt_nd) take_first(cnt_nd, list[i], ldn, fc.skip[KIND_ND]);
-                if (cnt_dd) take_first(cnt_dd, list[i], ldd, fc.skip[KIND_DD]);
-                cdn += ldn > 0;
-                edn += ldn;
-                cdd += ldd > 0;
-                edd += ldd;
+        for (unsigned g0 = 0; g0 < cnt; g0 += 32 * NB_DEL) {
+            uint32_t x[NB_DEL], ldn[NB_DEL], ldd[NB_DEL];
+            int64_t gx[NB_DEL], par[NB_DEL];
+            bool ok[NB_DEL];
+#pragma unroll
+            for (int u = 0; u < NB_DEL; u++) {
+                const unsigned i = g0 + u * 32 + lane;
+                ok[u] = i < cnt;
+                x[u] = ok[u] ? list[i] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < NB_DEL; u++) {
+                ldn[u] = ok[u] ? __ldg(&V.deg[KIND_DN][x[u]]) : 0u;
+                ldd[u] = ok[u] ? __ldg(&V.deg[KIND_DD][x[u]]) : 0u;
+                gx[u] = (ok[u] && V.glevel) ? __ldg(&V.del_gid[x[u]]) : 0;
+                // a lone in-process worker's new delegates all come from its own mask
+                par[u] = (ok[u] && V.parents && V.cand_all && V.P_sources == 1) ? V.dcand[x[u]] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < NB_DEL; u++) {
+                if (!ok[u]) continue;
+                new_delegate(V, L, x[u], gx[u], par[u]);
+                if (cnt_nd) take_first(cnt_nd, x[u], ldn[u], fc.skip[KIND_ND]);
+                if (cnt_dd) take_first(cnt_dd, x[u], ldd[u], fc.skip[KIND_DD]);
+                cdn += ldn[u] > 0;
+                edn += ldn[u];
+                cdd += ldd[u] > 0;
+                edd += ldd[u];
                 fc.new_del++;
             }
         }
