@@ -442,6 +442,8 @@ static void ensure_resources(Graph &g) {
         Wk.dcand.alloc(std::max<int64_t>(g.d, 1));
         Wk.nvis.alloc(std::max<int64_t>(nw_n, 1));
         Wk.nseen.alloc(std::max<int64_t>(nw_n, 1));
+        Wk.ntouch.alloc(2 * std::max<int64_t>(nwords(ceil_div(nw_n, 32)), 1));
+        Wk.nchunk_list.alloc(2 * std::max<int64_t>(ceil_div(nw_n, 32), 1));
         Wk.dseen.alloc(std::max<int64_t>(nw_d, 1));
         Wk.nfront0.alloc(std::max<int64_t>(nw_n, 1));
         Wk.nfront1.alloc(std::max<int64_t>(nw_n, 1));
@@ -539,6 +541,11 @@ static void ensure_resources(Graph &g) {
         V.dcand = Wk.dcand.p;
         V.nvis = Wk.nvis.p;
         V.nseen = Wk.nseen.p;
+        V.ntw = Wk.ntouch.n / 2;
+        V.ntouch[0] = Wk.ntouch.p;
+        V.ntouch[1] = Wk.ntouch.p + V.ntw;
+        V.nchunk_list[0] = Wk.nchunk_list.p;
+        V.nchunk_list[1] = Wk.nchunk_list.p + Wk.nchunk_list.n / 2;
         V.dseen = Wk.dseen.p;
         V.nfront[0] = Wk.nfront0.p;
         V.nfront[1] = Wk.nfront1.p;

@@ -360,6 +360,7 @@ constexpr uint32_t REC_SKIP = 0xffffffffu;
 static_assert(32 * UNR <= SEND_CHUNK, "a warp step must fit one fresh chunk");
 
 struct VisitCounters {
+    bool light;                     // light level: normal claims mark the touch bitmap
     unsigned long long fv_nn;       // FV_nn of this level's frontier (activity slot)
     unsigned long long scur, send;  // peer engine: this warp's inbox chunk for destination lane_id()
     unsigned long long records;     // remote normal records (comm accounting)
@@ -368,6 +369,22 @@ struct VisitCounters {
     unsigned long long dirty;
     unsigned long long pull_rows;
 };
+
+// Light levels: every normal claim also marks its 1024-vertex chunk in the
+// next frontier's touch bitmap (1 bit per 32 bitmap words) and the first claim
+// of a chunk appends it to the chunk list of frontier L+1, so F and the next
+// T1 hand out the listed chunks to warps instead of sweeping all n/32 words.
+// Heavy levels do not mark; their F sweeps and builds the bitmap from the fold
+// (the next level then finds chunks by their touch bits).
+__device__ __noinline__ void touch_chunk(const View &V, int L, uint32_t c) {
+    const uint32_t chunk = c >> 10, bit = 1u << (chunk & 31);
+    uint32_t *touch = V.ntouch[(L + 1) & 1];
+    if (__ldcg(&touch[chunk >> 5]) & bit) return;
+    if (atomicOr(&touch[chunk >> 5], bit) & bit) return;
+    // first claim in this chunk: append it to the next frontier's chunk list
+    const unsigned long long i = atomicAdd(&V.ctl->s[(L + 1) % 3].nchunks, 1ull);
+    V.nchunk_list[(L + 1) & 1][i] = chunk;
+}
 
 // Claim normal c of worker `wv` (this worker, or an in-process peer) for
 // level L+1, fire-and-forget.  `seen` is visited(<= L) plus the pushes' claims
@@ -383,8 +400,11 @@ __device__ __forceinline__ void claim_on(uint32_t *__restrict__ seen, uint32_t *
     if (parents) nparent[c] = parent;     // the level is written by F3 (word order, coalesced)
 }
 
-__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent) {
+__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool light) {
+    const uint32_t wd = c >> 5, bit = 1u << (c & 31);
+    if (__ldcg(&V.nseen[wd]) & bit) return;
     claim_on(V.nseen, V.nfront[(L + 1) & 1], V.nparent, V.parents, c, parent);
+    if (light) touch_chunk(V, L, c);
 }
 
 // Remote nn records of one warp step (engine.py:207-222 -> comm.py:138-197):
@@ -538,6 +558,7 @@ template <int ACT, bool CNT, int U>
 __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t (&cc)[U], const uint32_t (&pp)[U],
                                            const uint32_t (&tw)[U], uint32_t *first, const bool (&valid)[U],
                                            VisitCounters &vc) {
+    const bool light = vc.light;
     // map the column to the (worker-local) vertex it names
     uint32_t tgt[U];
     bool local[U];
@@ -589,6 +610,12 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         } else if (V.parents) {
             V.nparent[x] = pp[u];
         }
+    }
+    if (ACT != ACT_DELEG && light) {
+        // light level: the claims' chunks into the touch bitmap / chunk list
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (!((s[u] >> (tgt[u] & 31)) & 1u)) touch_chunk(V, L, tgt[u]);
     }
     if (ACT == ACT_NN && V.p > 1) {
         bool remote[U];
@@ -965,6 +992,12 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     level_dirs(V, C, L, dirs, bv, cum);
     int ex[4];
     exec_dirs(V, S, cum, dirs, ex);
+    // light level: few normal claims expected (no dn pull, pushed normal-target
+    // edges <= n_local/32), so claims mark the touch bitmap for F and T1
+    const bool light = V.W == 1 && ex[KIND_DN] != BWD &&
+                       S.fv[KIND_NN] + (ex[KIND_DN] != BWD ? S.fv[KIND_DN] : 0ull) <= (unsigned long long)V.nw_n;
+    // frontier L's chunk list is complete when V(L-1) was light (level 0: the seed lists it)
+    const bool prev_light = V.W == 1 && (L == 0 || C.s[(L + 2) % 3].light != 0);
     if (wb == 0 && threadIdx.x == 0) {
         unsigned long long cumfv[4];
         for (int k = 0; k < 4; k++) cumfv[k] = (L == 0 ? 0ull : C.cumfv[(L + 1) & 1][k]) + S.fv[k];
@@ -973,6 +1006,10 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
             C.cumq[L & 1][k] = cum[k];
             C.cumfv[L & 1][k] = cumfv[k];
             C.s[L % 3].exec_dir[k] = ex[k];
+            if (k == 0) {
+                C.s[L % 3].light = light ? 1ull : 0ull;
+                C.s[L % 3].prev_light = prev_light ? 1ull : 0ull;
+            }
             C.s[L % 3].bv[k] = bv[k];
             if (k == 0) C.s[L % 3].prev_dirty = L > 0 ? C.s[(L + 2) % 3].dirty : 0ull;
             if (k > 0 && ex[k] != BWD) C.s[L % 3].work[k] = S.fv[k];
@@ -982,6 +1019,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         }
     }
     VisitCounters vc = {};
+    vc.light = light;
     block_acc_clear();
     __syncthreads();
     const unsigned lane = lane_id(), warp = warp_id();
@@ -1007,13 +1045,13 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         // scan, dominate (uniform frontier bits balance a static stride)
         const unsigned long long t1_edges = S.fv[KIND_NN] + (nd_fwd ? S.fv[KIND_ND] : 0ull);
         const bool t1_dyn = S.nfront > (unsigned long long)TW && t1_edges > (unsigned long long)V.t1_dyn_min * V.nw_n;
-        for (WarpChunks ch(t1_dyn ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
-            // groups of 1024 normals without frontier bits (coarse fold of F(L-1)) are skipped
-            if (DBFS_CWN == 32 && !__ldcg(&V.coarse_n[L & 1][ch.cur & (FW - 1)])) continue;
-            const int64_t wi = ch.word(V.nw_n);
+        const uint32_t *touch = V.ntouch[L & 1];
+        // one 32-word chunk of the frontier: compaction, then 32 rows per warp step
+        auto push_chunk = [&](int64_t chunk) {
+            const int64_t wi = chunk * 32 + lane;
             // only frontier vertices with an nn row (or an nd row when nd pushes)
-            uint32_t word = wi >= 0 ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
-            unsigned cnt = warp_compact(word, wi, list);
+            uint32_t word = wi < V.nw_n ? (nfront_cur[wi] & (has_nn[wi] | (nd_fwd ? has_nd[wi] : 0u))) : 0u;
+            unsigned cnt = warp_compact(word, wi < V.nw_n ? wi : 0, list);
             for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
                 unsigned i = g0 + lane;
                 bool ok = i < cnt;
@@ -1032,6 +1070,17 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                 }
             }
             __syncwarp();
+        };
+        if (prev_light) {
+            // frontier listed by the claims of a light V(L-1): a listed chunk per warp
+            const int64_t nl = (int64_t)S.nchunks;
+            for (int64_t i = gw; i < nl; i += TW) push_chunk(V.nchunk_list[L & 1][i]);
+        } else {
+            for (WarpChunks ch(t1_dyn ? &AT.sched[0] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
+                // chunks without frontier vertices are skipped
+                if (!((__ldcg(&touch[ch.cur >> 5]) >> (ch.cur & 31)) & 1u)) continue;
+                push_chunk(ch.cur);
+            }
         }
     }
 
@@ -1367,6 +1416,7 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
 
 // F2 (distributed only): ingest remote records (engine.py:147-157).
 __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
+    const bool light = V.ctl->s[L % 3].light != 0;
     if (V.peer) {  // senders stored into fixed segments of this inbox over NVLink
         __shared__ unsigned long long s_cnt[MAXW];
         if (threadIdx.x < V.p) s_cnt[threadIdx.x] = __ldcg(&V.ctl_all[threadIdx.x]->s[L % 3].sent[V.w]);
@@ -1384,7 +1434,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
                     uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
                     if (!(old & (1u << (rec.x & 31)))) uq++;
                 }
-                claim_normal(V, L, rec.x, (int64_t)rec.y);
+                claim_normal(V, L, rec.x, (int64_t)rec.y, light);
             }
         }
         uq = warp_sum(uq);
@@ -1403,57 +1453,89 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
             uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
             if (!(old & (1u << (rec.x & 31)))) uq++;
         }
-        claim_normal(V, L, rec.x, (int64_t)rec.y);
+        claim_normal(V, L, rec.x, (int64_t)rec.y, light);
     }
     uq = warp_sum(uq);
     if (lane_id() == 0 && uq) atomicAdd(&V.ctl->s[L % 3].uq_records, uq);
 }
 
-// F3: fold the new normal frontier into visited, clear the old one, and count
-// the new frontier's previsit statistics (FV_nd, q_nd, |frontier|).
-__device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uint32_t *list, FinishCounters &fc) {
-    const unsigned lane = lane_id();
+// Fold one 32-word chunk of the new normal frontier (chunk index ch, lane =
+// word): visited |= next, the new vertices' levels and previsit statistics;
+// clears the old frontier's words when clear_cur.  Returns true when the
+// chunk holds new vertices.
+__device__ __forceinline__ bool fold_chunk(const View &V, int L, int64_t ch, bool clear_cur, uint32_t *list,
+                                           FinishCounters &fc, uint32_t *cnt_dn) {
     uint32_t *cur = V.nfront[L & 1];
     const uint32_t *nxt = V.nfront[(L + 1) & 1];
-    const LevelSlot &A = V.ctl->s[L % 3];
-    const bool dyn = V.f3_dyn && A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
-    uint32_t *cnt_dn = A.exec_dir[KIND_DN] == PUSHC ? V.first[KIND_DN] : nullptr;
-    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[5] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
-        const int64_t base = ch.base();
-        const int64_t wi = ch.word(V.nw_n);
-        uint32_t nw = 0u;
-        if (wi >= 0) {
-            if (cur[wi]) cur[wi] = 0u;
-            nw = nxt[wi];
-            if (nw) {
-                const uint32_t vis = V.nvis[wi] | nw;
-                V.nvis[wi] = vis;
-                V.nseen[wi] = vis;  // + the pulls' finds (pulls do not mark seen: a push claiming the
-                                    // same vertex again only repeats an idempotent mark)
-            }
+    const int64_t wi = ch * 32 + lane_id();
+    uint32_t nw = 0u;
+    if (wi < V.nw_n) {
+        if (clear_cur && cur[wi]) cur[wi] = 0u;
+        nw = nxt[wi];
+        if (nw) {
+            const uint32_t vis = V.nvis[wi] | nw;
+            V.nvis[wi] = vis;
+            V.nseen[wi] = vis;  // + the pulls' finds (pulls do not mark seen: a push claiming the
+                                // same vertex again only repeats an idempotent mark)
         }
-        if (!__any_sync(FULL, nw != 0u)) continue;
-        {
-            uint32_t fold = nw;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) fold |= __shfl_xor_sync(FULL, fold, o);
-            if (lane == 0) atomicOr(&V.coarse_n[(L + 1) & 1][(base >> 5) & (FW - 1)], fold);
-        }
-        unsigned cnt = warp_compact(nw, wi, list);
-        for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
-            unsigned i = g0 + lane;
-            if (i < cnt) {
-                uint32_t c = list[i];
-                V.nlevel[c] = L + 1;  // every claim of level L+1 (push, pull, remote record) lands here
-                int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
-                if (cnt_dn) take_first(cnt_dn, c, (uint64_t)dnd, fc.skip[KIND_DN]);
-                fc.nfv_nd += (unsigned long long)dnd;
-                fc.nq_nd += dnd > 0;
-                fc.ncount++;
-            }
-        }
-        __syncwarp();
     }
+    if (!__any_sync(FULL, nw != 0u)) return false;
+    unsigned cnt = warp_compact(nw, wi < V.nw_n ? wi : 0, list);
+    for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
+        unsigned i = g0 + lane_id();
+        if (i < cnt) {
+            uint32_t c = list[i];
+            V.nlevel[c] = L + 1;  // every claim of level L+1 (push, pull, remote record) lands here
+            int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
+            if (cnt_dn) take_first(cnt_dn, c, (uint64_t)dnd, fc.skip[KIND_DN]);
+            fc.nfv_nd += (unsigned long long)dnd;
+            fc.nq_nd += dnd > 0;
+            fc.ncount++;
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// F3: fold the new normal frontier into visited, clear the old one, and count
+// the new frontier's previsit statistics (FV_nd, q_nd, |frontier|).  After a
+// light level V(L) the new frontier's chunks are those listed by its claims;
+// the old frontier's chunks come from its list (V(L-1) light) or its touch
+// bits.  After a heavy level every word is swept and the touch bitmap of
+// frontier L+1 is built from the fold.  Either way touch[(L+1)&1] marks
+// exactly the non-empty chunks of frontier L+1 and touch[L&1] ends zero.
+__device__ void finish_normals(const View &V, int L, int64_t gw, int64_t TW, uint32_t *list, FinishCounters &fc) {
+    const unsigned lane = lane_id();
+    const LevelSlot &A = V.ctl->s[L % 3];
+    uint32_t *cnt_dn = A.exec_dir[KIND_DN] == PUSHC ? V.first[KIND_DN] : nullptr;
+    uint32_t *t_old = V.ntouch[L & 1], *t_new = V.ntouch[(L + 1) & 1];
+    const int64_t nch = (V.nw_n + 31) >> 5;
+    if (A.light) {
+        uint32_t *cur = V.nfront[L & 1];
+        auto clear_old = [&](int64_t ch) {
+            const int64_t wi = ch * 32 + lane;
+            if (wi < V.nw_n && cur[wi]) cur[wi] = 0u;
+            if (lane == 0) atomicAnd(&t_old[ch >> 5], ~(1u << (ch & 31)));
+        };
+        if (A.prev_light) {  // old frontier listed by the claims of V(L-1)
+            const int64_t no = (int64_t)A.nchunks;
+            for (int64_t i = gw; i < no; i += TW) clear_old(V.nchunk_list[L & 1][i]);
+        } else {
+            for (int64_t ch = gw; ch < nch; ch += TW)
+                if ((__ldcg(&t_old[ch >> 5]) >> (ch & 31)) & 1u) clear_old(ch);
+        }
+        const int64_t nn = (int64_t)__ldcg(&V.ctl->s[(L + 1) % 3].nchunks);
+        for (int64_t i = gw; i < nn; i += TW) fold_chunk(V, L, V.nchunk_list[(L + 1) & 1][i], false, list, fc, cnt_dn);
+        return;
+    }
+    const int64_t tid = gw * 32 + lane, nth = TW * 32;
+    for (int64_t i = tid; i < V.ntw; i += nth) t_old[i] = 0u;
+    const bool dyn = V.f3_dyn && A.nfront + A.dfront > (unsigned long long)TW;  // heavy level: large next frontier likely
+    for (WarpChunks ch(dyn ? &V.ctl->s[L % 3].sched[5] : nullptr, V.nw_n, DBFS_CWN, gw, TW); ch.valid(); ch.next()) {
+        if (fold_chunk(V, L, ch.cur, true, list, fc, cnt_dn) && lane == 0)
+            atomicOr(&t_new[ch.cur >> 5], 1u << (ch.cur & 31));
+    }
+    (void)nch;
 }
 
 __device__ void flush_finish(const View &V, int L, FinishCounters &fc, int wb, bool zero_slot) {
@@ -1501,8 +1583,6 @@ __device__ void phase_finish(const View &V, int L, int wb, int nb, Smem &sm, int
         finish_delegates(V, L, gw, TW, list, fc);
         tt.stop(V.ctl->s[L % 3], 6);
     }
-    if (parts & F_NORMALS)
-        for (int64_t i = tid; i < FW; i += nth) V.coarse_n[L & 1][i] = 0u;
     if (parts & F_INGEST) finish_ingest(V, L, tid, nth);
     if ((parts & F_NORMALS) && V.uniquify)
         for (int64_t i = tid; i < (int64_t)V.p * V.nw_n; i += nth) V.uq[i] = 0u;
@@ -1537,6 +1617,7 @@ __device__ void phase_init(const View &V, int wb, int nb) {
     }
     if (V.sent)
         for (int64_t i = tid; i < V.nw_g; i += nth) V.sent[i] = 0u;
+    for (int64_t i = tid; i < 2 * V.ntw; i += nth) V.ntouch[0][i] = 0u;  // both parities (contiguous)
     for (int64_t i = tid; i < V.nw_d; i += nth) {
         V.dvis[i] = 0u;
         V.dseen[i] = 0u;
@@ -1586,7 +1667,9 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         V.nfront[0][c >> 5] |= 1u << (c & 31);
         V.nvis[c >> 5] |= 1u << (c & 31);
         V.nseen[c >> 5] |= 1u << (c & 31);
-        V.coarse_n[0][(c >> 10) & (FW - 1)] |= 1u << (c & 31);
+        V.ntouch[0][(c >> 10) >> 5] |= 1u << ((c >> 10) & 31);
+        V.nchunk_list[0][0] = c >> 10;
+        S.nchunks = 1;
         int64_t dnd = V.off[KIND_ND][c + 1] - V.off[KIND_ND][c];
         S.fv[KIND_ND] = dnd;
         S.q[KIND_ND] = dnd > 0;

@@ -34,6 +34,9 @@ struct LevelSlot {
     unsigned long long inbox;        // records delivered to this worker
     unsigned long long pull_rows;    // reverse rows scanned by pulls at this level
     unsigned long long uq_records;   // records left after per-group uniquify (comm.py:122-127)
+    unsigned long long light;        // light level: normal claims mark the touch bitmap (F folds touched chunks)
+    unsigned long long prev_light;   // level L-1 was light: frontier L's chunk list is complete
+    unsigned long long nchunks;      // chunks listed for this level's frontier (claims of a light level L-1)
     unsigned long long work[4];      // inspections actually executed (push: FV, pull: scanned)
     int exec_dir[4];                 // executed strategy per kind (may differ from the reported one)
     double bv[4];                    // BV per kind as the direction rule saw it (for the record)
@@ -119,6 +122,9 @@ struct alignas(16) View {
     int64_t *dcand;
     uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
     uint32_t *nseen, *dseen;         // visited(<= L) + claims of level L: the push's single test
+    uint32_t *ntouch[2];             // by level parity: 1 bit per 32-word chunk holding frontier normals
+    uint32_t *nchunk_list[2];        // by level parity: those chunks, listed by the claims of a light level
+    int64_t ntw;                     // words of one touch bitmap
     uint32_t *nseen_all[MAXW];       // in-process: peers' seen bits (direct remote claims)
     uint32_t *coarse_d[2], *coarse_n[2];  // coarse frontier filters by level parity
     uint32_t *dlist[2][2];           // delegate frontier per push kind (0 dn, 1 dd) and parity
@@ -225,6 +231,8 @@ struct WorkerHost {
     DArray<int64_t> nparent, dparent, dcand;
     DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
     DArray<uint32_t> nseen, dseen;   // visited + claims of the running level (push test)
+    DArray<uint32_t> ntouch;         // 2 x ntw words: touched chunks of the frontier by parity
+    DArray<uint32_t> nchunk_list;    // 2 x chunks: their lists
     DArray<uint32_t> coarse;         // 4 x 8192 words: coarse_d[0..1], coarse_n[0..1]
     DArray<uint32_t> dlist[4];       // [kind*2 + parity]
     DArray<int64_t> dpre[4];
