@@ -638,6 +638,7 @@ __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint3
     unsigned tot;
     unsigned excl = warp_excl_scan(len, &tot);
     const unsigned lane = lane_id();
+    const int64_t delta = rb - (int64_t)excl;
     for (unsigned base = 0; base < tot; base += 32 * U) {
         uint32_t cc[U];
         uint32_t pp[U];
@@ -646,11 +647,10 @@ __device__ __forceinline__ void warp_rows_push(const View &V, int L, const uint3
         for (int u = 0; u < U; u++) {
             unsigned x = base + u * 32 + lane;
             int o = owner_search<unsigned>(excl, x);
-            int64_t rbo = __shfl_sync(FULL, rb, o);
-            unsigned eo = __shfl_sync(FULL, excl, o);
+            const int64_t dl = __shfl_sync(FULL, delta, o);  // entry x at column dl + x
             pp[u] = __shfl_sync(FULL, par, o);
-            cc[u] = x < tot ? __ldg(&col[rbo + (x - eo)]) : 0u;
-            tw[u] = (CNT && x < tot) ? __ldg(&twin[rbo + (x - eo)]) : 0u;
+            cc[u] = x < tot ? __ldg(&col[dl + x]) : 0u;
+            tw[u] = (CNT && x < tot) ? __ldg(&twin[dl + x]) : 0u;
         }
         bool valid[U];
 #pragma unroll
@@ -697,19 +697,26 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
         if (lane == 0) wend = (i + 32 < cnt) ? pre[i + 32] : total;
         wend = __shfl_sync(FULL, wend, 0);
         int64_t lim = wend < x1 ? wend : x1;
+        // 32-bit keys relative to the window's first row (a window of 32 rows
+        // holds < 2^32 edges): half the shuffles of the owner search; entry x
+        // of the window lives at column delta(owner) + x
+        const int64_t wbase = __shfl_sync(FULL, pb, 0);
+        const int64_t rel = pb - wbase;
+        const uint32_t pb32 = rel < 0xffffffffll ? (uint32_t)rel : 0xffffffffu;
+        const int64_t delta = rb - pb;
         for (int64_t base = x0; base < lim; base += 32 * U) {
             uint32_t cc[U];
             uint32_t pp[U];
             uint32_t tw[U];
+            const uint32_t b32 = (uint32_t)(base - wbase);
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                int64_t x = base + u * 32 + lane;
-                int o = owner_search<int64_t>(pb, x);
-                int64_t rbo = __shfl_sync(FULL, rb, o);
-                int64_t pbo = __shfl_sync(FULL, pb, o);
+                const int64_t x = base + u * 32 + lane;
+                const int o = owner_search<uint32_t>(pb32, b32 + (uint32_t)(u * 32) + lane);
+                const int64_t dl = __shfl_sync(FULL, delta, o);
                 pp[u] = __shfl_sync(FULL, gx, o);
-                cc[u] = x < lim ? __ldg(&col[rbo + (x - pbo)]) : 0u;
-                tw[u] = (CNT && x < lim) ? __ldg(&twin[rbo + (x - pbo)]) : 0u;
+                cc[u] = x < lim ? __ldg(&col[dl + x]) : 0u;
+                tw[u] = (CNT && x < lim) ? __ldg(&twin[dl + x]) : 0u;
             }
             bool valid[U];
 #pragma unroll
