@@ -200,6 +200,9 @@ int32_t dbfs_graph_upload_partitioned(dbfs_ctx *ctx, int64_t n, int64_t m, int64
                                       int32_t p_gpu, int64_t d, const int64_t *delegate_global_ids,
                                       const int64_t *out_degree, const int64_t *const *row_offsets,
                                       const void *const *col_indices, int32_t symmetric, dbfs_graph **out);
+/* 1 when the peer engine ORs the delegate masks through an NVSwitch multicast
+ * object (DBFS_NVLS=1 in a device group, nvls.cu), else 0. */
+int32_t dbfs_graph_nvls_active(const dbfs_graph *g);
 int32_t dbfs_graph_free(dbfs_graph *g);
 /* Declare the edge multiset symmetric (every (u,v) has its (v,u)); RMAT builds with
  * symmetrize set are symmetric by construction. */

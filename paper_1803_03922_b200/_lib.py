@@ -108,6 +108,7 @@ SIGNATURES = {
     "dbfs_bfs_iteration_sends": (i32, [vp, i64, vp]),
     "dbfs_ctx_init_local_group": (i32, [vp, vp, i64, i32, i32]),
     "dbfs_ctx_abort": (i32, [vp]),
+    "dbfs_graph_nvls_active": (i32, [vp]),
     "dbfs_graph_upload_partitioned": (i32, [vp, i64, i64, i64, i32, i32, i64, vp, vp, vp, vp, i32, P(vp)]),
     "dbfs_validate": (i32, [vp, i64, vp, vp, P(i32)]),
     "dbfs_edges_text_capacity": (i32, [vp, i64, P(i64)]),

@@ -267,6 +267,8 @@ int32_t dbfs_graph_upload_partitioned(dbfs_ctx *ctx, int64_t n, int64_t m, int64
     return rc;
 }
 
+int32_t dbfs_graph_nvls_active(const dbfs_graph *g) { return g && g->g.nvls ? 1 : 0; }
+
 int32_t dbfs_graph_free(dbfs_graph *g) {
     return guard([&] {
         if (!g) return;

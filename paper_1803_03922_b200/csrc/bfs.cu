@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(BT) k_assemble(AsmArgs a) {
 
 
 Graph::~Graph() {
+    nvls_release(*this);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (batch_hrec) cudaFreeHost(batch_hrec);
     for (cudaEvent_t e : batch_evs) cudaEventDestroy(e);
@@ -683,7 +684,7 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     k_pack_status<<<1, 32, 0, ctx.stream>>>(Wk.ctl.p, L, p, st_dev);
     DBFS_LAUNCHED();
     nccl_allgather_bytes(ctx, st_dev, st_all, 8 * S);
-    uint32_t *own = (L & 1) ? Wk.dnext1.p : Wk.dnext0.p;
+    uint32_t *own = g.views_h[0].dnext[L & 1];  // (NVLS: the multicast-bound copy)
     nccl_allgather_bytes(ctx, own, g.mask_gather.p, nw_d * 4);
     DBFS_CUDA(cudaMemcpyAsync(g.h_status, st_all, 8 * S * p, cudaMemcpyDeviceToHost, ctx.stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -789,7 +790,19 @@ static void setup_peer(Graph &g) {
         std::vector<void *> ptr((size_t)NH * p, nullptr);
         for (int j = 0; j < p; j++)
             for (int i = 0; i < NH; i++) ptr[(size_t)j * NH + i] = all_rec[j].ptr[i];
+        // NVSwitch multicast for the delegate masks (opt-in): the masks move to
+        // multicast-bound memory; F reads the OR of all ranks with one load
+        uint32_t *masks[2] = {nullptr, nullptr};
+        const uint32_t *mc[2] = {nullptr, nullptr};
+        const char *nv = getenv("DBFS_NVLS");
+        const bool use_nvls = nv && nv[0] == '1' && nvls_setup(g, std::max<int64_t>(nwords(g.d), 1), masks, mc);
+        if (use_nvls) {
+            for (int b = 0; b < 2; b++) g.views_h[0].dnext[b] = masks[b];
+            DBFS_CUDA(cudaMemcpy(g.views.p, g.views_h.data(), sizeof(View) * g.views_h.size(), cudaMemcpyHostToDevice));
+        }
         finish_peer_setup(g, ptr);
+        if (use_nvls)
+            for (int b = 0; b < 2; b++) g.peer_view_h.mask_mc[b] = mc[b];
         return;
     }
     std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * p);

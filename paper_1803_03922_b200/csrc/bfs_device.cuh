@@ -1312,7 +1312,22 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         const int64_t base = ch.base();
         const int64_t wi = ch.word(V.nw_d);
         uint32_t nw = 0u;
-        if (wi >= 0) {
+        if (wi >= 0 && V.mask_mc[L & 1]) {
+            // NVLS: the NVSwitch returns the OR of every rank's copy of the word
+            uint32_t r;
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.or.b32 %0, [%1];"
+                         : "=r"(r)
+                         : "l"(V.mask_mc[L & 1] + wi)
+                         : "memory");
+            uint32_t dv = V.dvis[wi];
+            nw = r & ~dv;
+            next_mask[wi] = 0u;
+            V.dfront[wi] = nw;
+            if (nw) {
+                V.dvis[wi] = dv | nw;
+                V.dseen[wi] = dv | nw;
+            }
+        } else if (wi >= 0) {
             uint32_t r = 0;
             for (int s0 = 0; s0 < V.P_sources; s0 += 8) {
                 uint32_t t[8];

@@ -138,6 +138,7 @@ struct alignas(16) View {
     uint32_t *nfront_all[2][MAXW];
     int64_t *nparent_all[MAXW];
     const uint32_t *mask_src[2][MAXW];
+    const uint32_t *mask_mc[2];      // NVLS: multicast address of the masks (one ld_reduce.or = OR over ranks)
     const int64_t *cand_src[MAXW];
     IterRec *rec;
     unsigned long long *trace;       // DBFS_TRACE: per level x {V start, V done, F start, F done} x block globaltimer
@@ -304,6 +305,7 @@ struct Graph {
     unsigned *hesc = nullptr;        // pinned: escape counts of the 3 host sets
     DArray<unsigned> esc;            // device escape counters (2 staging buffers)
     DArray<unsigned long long> minpar;  // min-ID parent candidates (parent_mode 2)
+    void *nvls = nullptr;            // NVSwitch multicast state of the delegate masks (nvls.cu)
     DArray<IterRec> batch_drec;      // dbfs_bfs_batch scratch (grow-only): per-root records,
     IterRec *batch_hrec = nullptr;   //   their pinned host copy,
     DArray<int2> batch_info;         //   per-root (iterations, watchdog),
@@ -360,6 +362,10 @@ int64_t count_text_lines(const char *buf, int64_t len);
 void parse_edge_text(const char *buf, int64_t len, int64_t cap, int64_t *src, int64_t *dst, int64_t *m_out,
                      int64_t *header_n);
 void write_edge_text(const char *path, int64_t n, const int64_t *src, const int64_t *dst, int64_t m);
+
+// nvls.cu (NVSwitch multicast delegate masks, device groups)
+bool nvls_setup(Graph &g, int64_t mask_words, uint32_t **masks, const uint32_t **mc);
+void nvls_release(Graph &g);
 
 // scan.cu helpers (device-wide exclusive scans)
 void exclusive_scan_u32_to_i64(Ctx &ctx, const uint32_t *in, int64_t *out, int64_t n);  // out has n+1

@@ -127,3 +127,32 @@ def test_device_group_auto_placement_at_scale():
         api.run_bfs(pg, api.BfsOptions(source=1 << scale))
     assert api.run_bfs(pg, api.BfsOptions(source=3)).levels_digest == O.run_bfs(og, 3)["levels_digest"]
     pg.close()
+
+
+def test_nvls_multicast_delegate_masks(monkeypatch):
+    """DBFS_NVLS=1: the delegate masks of a device group live in NVSwitch
+    multicast memory and F ORs them with one multimem.ld_reduce per word
+    (comm.py:75-98); every report equals the oracle's (the peer reads are the
+    default path checked above)."""
+    have = _gpus()
+    if have < 2:
+        pytest.skip(f"needs >= 2 GPUs, {have} visible")
+    import oracle as O
+    import paper_1803_03922_b200 as api
+    from paper_1803_03922_b200 import _lib
+    monkeypatch.setenv("DBFS_NVLS", "1")
+    P = min(have, 4)
+    scale, theta = 18, 16
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=2)), theta,
+                             api.ClusterShape(1, P), devices=list(range(P)))
+    og = O.partition_rmat(scale, theta, 1, P, seed=2)
+    for root in (5, 777):
+        for mode in ("dobfs", "bfs"):
+            got = api.run_bfs(pg, api.BfsOptions(mode=mode, source=root)).to_dict()
+            ref = O.run_bfs(og, root, mode=mode)
+            for key in ("levels_digest", "iterations", "inspections", "per_iteration", "comm"):
+                assert got[key] == ref[key], (root, mode, key)
+    active = [_lib.load().dbfs_graph_nvls_active(pt.handle) for pt in pg.parts]
+    pg.close()
+    if not all(active):
+        pytest.skip("NVSwitch multicast unavailable on this box (peer reads were used)")
