@@ -1503,15 +1503,23 @@ __device__ __forceinline__ bool fold_chunk(const View &V, int L, int64_t ch, boo
     }
     if (!__any_sync(FULL, nw != 0u)) return false;
     unsigned cnt = warp_compact(nw, wi < V.nw_n ? wi : 0, list);
-    for (unsigned g0 = 0; g0 < cnt; g0 += 32) {
-        unsigned i = g0 + lane_id();
-        if (i < cnt) {
-            uint32_t c = list[i];
-            V.nlevel[c] = L + 1;  // every claim of level L+1 (push, pull, remote record) lands here
-            int64_t dnd = __ldg(&V.deg[KIND_ND][c]);
-            if (cnt_dn) take_first(cnt_dn, c, (uint64_t)dnd, fc.skip[KIND_DN]);
-            fc.nfv_nd += (unsigned long long)dnd;
-            fc.nq_nd += dnd > 0;
+    // NB_DEL new vertices per lane at a time: their row-length loads in flight together
+    for (unsigned g0 = 0; g0 < cnt; g0 += 32 * NB_DEL) {
+        uint32_t c[NB_DEL], dnd[NB_DEL];
+#pragma unroll
+        for (int u = 0; u < NB_DEL; u++) {
+            const unsigned i = g0 + u * 32 + lane_id();
+            c[u] = i < cnt ? list[i] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < NB_DEL; u++) dnd[u] = c[u] != 0xffffffffu ? __ldg(&V.deg[KIND_ND][c[u]]) : 0u;
+#pragma unroll
+        for (int u = 0; u < NB_DEL; u++) {
+            if (c[u] == 0xffffffffu) continue;
+            V.nlevel[c[u]] = L + 1;  // every claim of level L+1 (push, pull, remote record) lands here
+            if (cnt_dn) take_first(cnt_dn, c[u], (uint64_t)dnd[u], fc.skip[KIND_DN]);
+            fc.nfv_nd += (unsigned long long)dnd[u];
+            fc.nq_nd += dnd[u] > 0;
             fc.ncount++;
         }
     }
