@@ -136,23 +136,22 @@ struct AsmArgs {
     PDiv pd;
     const uint32_t *del_id;
     const int32_t *nlevel[MAXW];
-    const int64_t *nparent[MAXW];
+    const parent_t *nparent[MAXW];
     int64_t stride;  // dist: gathered arrays are [p][stride]
     const int32_t *dlevel;
-    const int64_t *dparent;
-    const int64_t *dpar_src[MAXW];  // peer-mapped: every rank's delegate candidates (min taken here)
+    const parent_t *dparent;
+    const parent_t *dpar_src[MAXW];  // peer-mapped: every rank's delegate candidates (min taken here)
     int n_dpar;
     int32_t *glevel;
-    int64_t *gparent;
+    parent_t *gparent;               // device-side global parents (int32)
+    int64_t *gparent64;              // or: the reference's int64 parents (staging for the host)
     int parents;
     int64_t first, step, count;  // output i is vertex first + i*step (global: 0, 1, n; rank r's own: r, p, n_local)
-    int8_t *glevel8;             // compact transfer form (dbfs_bfs_batch): depth as int8, parent as int32
-    int32_t *gparent32;
+    int8_t *glevel8;             // compact transfer form (dbfs_bfs_batch): depth as int8
     unsigned *esc;               // depths >= 127 (escaped: the root is re-run with full arrays)
 };
 
-// Compact wire form of one depth / parent entry (sign extension restores -1 on
-// the host; parents are global ids < 2^31).
+// Compact wire form of one depth entry (sign extension restores -1 on the host).
 __device__ __forceinline__ int8_t pack_level(int32_t l, unsigned *esc) {
     if (l < 127) return (int8_t)l;
     atomicAdd(esc, 1u);
@@ -165,58 +164,40 @@ __device__ __forceinline__ int8_t pack_level(int32_t l, unsigned *esc) {
 __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
     for (int64_t o = tid; o < a.count; o += nth) {
         const int64_t v = a.first + o * a.step;
-        uint32_t di = a.del_id[v];
-        if (a.glevel8) {  // compact form
-            int32_t l;
-            int64_t par = -1;
-            if (di != 0xffffffffu) {
-                l = a.dlevel[di];
-                if (a.parents && l >= 0) {
-                    if (a.n_dpar) {
-                        par = 0x7fffffffffffffffLL;
-                        for (int s = 0; s < a.n_dpar; s++) {
-                            const int64_t c = a.dpar_src[s][di];
-                            par = c < par ? c : par;
-                        }
-                    } else {
-                        par = a.dparent[di];
-                    }
-                }
-            } else {
-                uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
-                l = a.nlevel[w][i];
-                if (a.parents) par = a.nparent[w][i];
-            }
-            a.glevel8[o] = pack_level(l, a.esc);
-            if (a.parents) {
-                if (a.gparent32) a.gparent32[o] = (int32_t)par;
-                else a.gparent[o] = par;
-            }
-            continue;
-        }
+        const uint32_t di = a.del_id[v];
+        int32_t l;
+        parent_t par = -1;
         if (di != 0xffffffffu) {
-            a.glevel[o] = a.dlevel[di];
-            if (a.parents) {
-                int64_t par = -1;
-                if (a.dlevel[di] >= 0) {
-                    if (a.n_dpar) {
-                        par = 0x7fffffffffffffffLL;
-                        for (int s = 0; s < a.n_dpar; s++) {
-                            const int64_t c = a.dpar_src[s][di];
-                            par = c < par ? c : par;
-                        }
-                    } else {
-                        par = a.dparent[di];
+            l = a.dlevel[di];
+            if (a.parents && l >= 0) {
+                if (a.n_dpar) {
+                    par = PARENT_MAX;
+                    for (int s = 0; s < a.n_dpar; s++) {
+                        const parent_t c = a.dpar_src[s][di];
+                        par = c < par ? c : par;
                     }
+                } else {
+                    par = a.dparent[di];
                 }
-                a.gparent[o] = par;
             }
         } else {
-            uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
-            a.glevel[o] = a.nlevel[w][i];
-            if (a.parents) a.gparent[o] = a.nparent[w][i];
+            const uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
+            l = a.nlevel[w][i];
+            if (a.parents) par = a.nparent[w][i];
+        }
+        if (a.glevel8) a.glevel8[o] = pack_level(l, a.esc);
+        else a.glevel[o] = l;
+        if (a.parents) {
+            if (a.gparent64) a.gparent64[o] = par;
+            else a.gparent[o] = par;
         }
     }
+}
+
+// int32 device parents -> the reference's int64 (host copies, validation)
+__global__ void k_widen_parents(const parent_t *__restrict__ in, int64_t n, int64_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
 }
 
 // ----------------------------------------------------------------- kernels
@@ -333,8 +314,7 @@ __global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restric
 }
 
 // Compact wire form of the whole-graph outputs (single process): 4 entries per thread.
-__global__ void k_pack_result(const int32_t *__restrict__ lv, const int64_t *__restrict__ pa, int64_t n,
-                              int8_t *__restrict__ lv8, int32_t *__restrict__ p32, unsigned *esc) {
+__global__ void k_pack_result(const int32_t *__restrict__ lv, int64_t n, int8_t *__restrict__ lv8, unsigned *esc) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (n >> 2); q += nth) {
         const int4 l = reinterpret_cast<const int4 *>(lv)[q];
@@ -344,16 +324,8 @@ __global__ void k_pack_result(const int32_t *__restrict__ lv, const int64_t *__r
         c.z = pack_level(l.z, esc);
         c.w = pack_level(l.w, esc);
         reinterpret_cast<char4 *>(lv8)[q] = c;
-        if (pa) {
-            const longlong2 a0 = reinterpret_cast<const longlong2 *>(pa)[2 * q];
-            const longlong2 a1 = reinterpret_cast<const longlong2 *>(pa)[2 * q + 1];
-            reinterpret_cast<int4 *>(p32)[q] = make_int4((int)a0.x, (int)a0.y, (int)a1.x, (int)a1.y);
-        }
     }
-    for (int64_t i = ((n >> 2) << 2) + tid; i < n; i += nth) {
-        lv8[i] = pack_level(lv[i], esc);
-        if (pa) p32[i] = (int32_t)pa[i];
-    }
+    for (int64_t i = ((n >> 2) << 2) + tid; i < n; i += nth) lv8[i] = pack_level(lv[i], esc);
 }
 
 __global__ void __launch_bounds__(BT) k_init(const View *__restrict__ views, int W) {
@@ -398,7 +370,15 @@ Graph::~Graph() {
 }
 
 int32_t *Graph::levels_dev() { return (p == 1 && !dist) ? workers[0].nlevel.p : glevel.p; }
-int64_t *Graph::parents_dev() { return (p == 1 && !dist) ? workers[0].nparent.p : gparent.p; }
+parent_t *Graph::parents_dev() { return (p == 1 && !dist) ? workers[0].nparent.p : gparent.p; }
+
+const int64_t *Graph::parents_dev64() {
+    if (export_pv.n < std::max<int64_t>(n, 1)) export_pv.alloc(std::max<int64_t>(n, 1));
+    Ctx &c = *ctx;
+    k_widen_parents<<<c.num_sms * 4, 256, 0, c.stream>>>(parents_dev(), n, export_pv.p);
+    DBFS_LAUNCHED();
+    return export_pv.p;
+}
 
 void build_sorted_dd(Graph &g);
 
@@ -407,6 +387,7 @@ static void ensure_resources(Graph &g) {
     if (g.symmetric) build_sorted_dd(g);
     if (g.symmetric && !getenv("DBFS_NO_TWINS")) build_twins(g);
     Ctx &ctx = *g.ctx;
+    DBFS_CHECK(g.n <= PARENT_MAX, DBFS_ECAPACITY, "parent ids are int32 on the device: n must be < 2^31");
     const int W = (int)g.workers.size();
     g.W = W;
     g.rec_cap = (int)std::min<int64_t>(std::max<int64_t>(g.n + 2, 16), 1 << 16);
@@ -869,7 +850,7 @@ static void finish_peer_setup(Graph &g, const std::vector<void *> &ptr) {
         V.ctl_all[j] = (Ctl *)ptr[(size_t)j * NH + 0];
         V.mask_src[0][j] = (const uint32_t *)ptr[(size_t)j * NH + 1];
         V.mask_src[1][j] = (const uint32_t *)ptr[(size_t)j * NH + 2];
-        V.cand_src[j] = (const int64_t *)ptr[(size_t)j * NH + 3];
+        V.cand_src[j] = (const parent_t *)ptr[(size_t)j * NH + 3];
     }
     // receiver r's inbox: segments by sender, sized by the senders' capacities towards r
     auto seg = [&](int r, int s) {
@@ -886,8 +867,8 @@ static void finish_peer_setup(Graph &g, const std::vector<void *> &ptr) {
     g.peer_dparent.assign(p, nullptr);
     for (int j = 0; j < p; j++) {
         g.peer_nlevel[j] = (int32_t *)ptr[(size_t)j * NH + 5];
-        g.peer_nparent[j] = (int64_t *)ptr[(size_t)j * NH + 6];
-        g.peer_dparent[j] = (int64_t *)ptr[(size_t)j * NH + 7];
+        g.peer_nparent[j] = (parent_t *)ptr[(size_t)j * NH + 6];
+        g.peer_dparent[j] = (parent_t *)ptr[(size_t)j * NH + 7];
     }
     g.gbar = ptr[NH - 1];  // rank 0's (its own on rank 0)
     g.peer_view_h = V;
@@ -1242,10 +1223,10 @@ static void dist_assemble(Graph &g) {
     }
     // delegate parents: each rank holds the candidate its own edges found (or
     // INT64_MAX) -> the tree takes the minimum over ranks
-    if (parents && g.d) nccl_allreduce_i64(ctx, Wk.dparent.p, g.d, 1);
+    if (parents && g.d) nccl_allreduce_i32_min(ctx, Wk.dparent.p, g.d);
     int64_t stride = ceil_div(g.n, g.p);
     DArray<int32_t> &lv = g.asm_lv, &mylv = g.asm_mylv;
-    DArray<int64_t> &pv = g.asm_pv, &mypv = g.asm_mypv;
+    DArray<parent_t> &pv = g.asm_pv, &mypv = g.asm_mypv;
     if (lv.n != stride * g.p) {
         lv.alloc(stride * g.p);
         pv.alloc(stride * g.p);
@@ -1253,13 +1234,14 @@ static void dist_assemble(Graph &g) {
         mypv.alloc(stride);
     }
     DBFS_CUDA(cudaMemsetAsync(mylv.p, 0xff, 4 * stride, ctx.stream));
-    DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, 8 * stride, ctx.stream));
+    DBFS_CUDA(cudaMemsetAsync(mypv.p, 0xff, sizeof(parent_t) * stride, ctx.stream));
     if (Wk.n_local) {
         DBFS_CUDA(cudaMemcpyAsync(mylv.p, Wk.nlevel.p, 4 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
-        DBFS_CUDA(cudaMemcpyAsync(mypv.p, Wk.nparent.p, 8 * Wk.n_local, cudaMemcpyDeviceToDevice, ctx.stream));
+        DBFS_CUDA(cudaMemcpyAsync(mypv.p, Wk.nparent.p, sizeof(parent_t) * Wk.n_local, cudaMemcpyDeviceToDevice,
+                                  ctx.stream));
     }
     nccl_allgather_bytes(ctx, mylv.p, lv.p, 4 * stride);
-    if (parents) nccl_allgather_bytes(ctx, mypv.p, pv.p, 8 * stride);
+    if (parents) nccl_allgather_bytes(ctx, mypv.p, pv.p, sizeof(parent_t) * stride);
     for (int w = 0; w < g.p; w++) {
         aa.nlevel[w] = lv.p + (int64_t)w * stride;
         aa.nparent[w] = pv.p + (int64_t)w * stride;
@@ -1285,7 +1267,7 @@ void fetch_result(Graph &g, int32_t *levels, int64_t *parents) {
     if (levels) DBFS_CUDA(cudaMemcpyAsync(levels, g.levels_dev(), 4 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
     if (parents) {
         DBFS_CHECK(g.last_parent_mode != 0, DBFS_EINVAL, "last BFS ran without parents");
-        DBFS_CUDA(cudaMemcpyAsync(parents, g.parents_dev(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+        DBFS_CUDA(cudaMemcpyAsync(parents, g.parents_dev64(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
     }
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
 }
@@ -1406,7 +1388,8 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         if (asm_src) {
             AsmArgs aa = *asm_src;
             aa.glevel = g.stage_lv[b].p;
-            aa.gparent = pa ? g.stage_pv[b].p : nullptr;
+            aa.gparent = nullptr;
+            aa.gparent64 = pa ? g.stage_pv[b].p : nullptr;
             aa.parents = pa;
             k_assemble<<<blocks, BT, 0, ctx.stream>>>(aa);
             DBFS_LAUNCHED();
@@ -1417,8 +1400,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 DBFS_LAUNCHED();
             }
             if (pa) {
-                k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(),
-                                                             (uint8_t *)g.stage_pv[b].p, 8 * nout);
+                k_widen_parents<<<blocks, 256, 0, ctx.stream>>>(g.parents_dev(), nout, g.stage_pv[b].p);
                 DBFS_LAUNCHED();
             }
         }
@@ -1438,7 +1420,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             o.source = roots[k];
             run_bfs(g, o, st ? &st[k] : nullptr);
             if (g.dist) {
-                if (o0.parent_mode && g.d) nccl_allreduce_i64(ctx, g.workers[0].dparent.p, g.d, 1);
+                if (o0.parent_mode && g.d) nccl_allreduce_i32_min(ctx, g.workers[0].dparent.p, g.d);
                 AsmArgs aa = batch_asm(g, o0.parent_mode != 0, local != 0);
                 stage_and_copy(k, &aa);
                 g.assembled = false;
@@ -1565,19 +1547,18 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 if (g.dist) {
                     AsmArgs ca = out_asm;
                     ca.glevel8 = l8;
-                    ca.gparent32 = nullptr;  // parents travel as int64 (no host widening)
-                    ca.gparent = want_par ? g.stage_pv[b].p : nullptr;
+                    ca.gparent = nullptr;  // parents travel as int64 (no host widening)
+                    ca.gparent64 = want_par ? g.stage_pv[b].p : nullptr;
                     ca.parents = want_par;
                     ca.esc = g.esc.p + b;
                     k_assemble<<<blocks, BT, 0, ctx.stream>>>(ca);
                     DBFS_LAUNCHED();
                 } else {
-                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), nullptr, nout, l8, nullptr,
+                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), nout, l8,
                                                                   g.esc.p + b);
                     DBFS_LAUNCHED();
                     if (want_par) {
-                        k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.parents_dev(),
-                                                                     (uint8_t *)g.stage_pv[b].p, 8 * nout);
+                        k_widen_parents<<<blocks, 256, 0, ctx.stream>>>(g.parents_dev(), nout, g.stage_pv[b].p);
                         DBFS_LAUNCHED();
                     }
                 }
@@ -1635,7 +1616,8 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             if (g.dist) {
                 AsmArgs fa = batch_asm(g, want_par, local != 0);
                 fa.glevel = g.stage_lv[0].p;
-                fa.gparent = want_par ? g.stage_pv[0].p : nullptr;
+                fa.gparent = nullptr;
+                fa.gparent64 = want_par ? g.stage_pv[0].p : nullptr;
                 fa.parents = want_par;
                 k_assemble<<<ctx.num_sms * 4, BT, 0, ctx.stream>>>(fa);
                 DBFS_LAUNCHED();
@@ -1890,9 +1872,9 @@ __global__ void k_par_init(const int32_t *__restrict__ lv, int64_t n, unsigned l
 
 // min-ID tree into the parent output: root -> root, unreached -> -1
 __global__ void k_par_final(const unsigned long long *__restrict__ par, const int32_t *__restrict__ lv, int64_t n,
-                            int64_t root, int64_t *__restrict__ out) {
+                            int64_t root, parent_t *__restrict__ out) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-        out[v] = v == root ? root : (lv[v] < 0 ? -1 : (int64_t)par[v]);
+        out[v] = (parent_t)(v == root ? root : (lv[v] < 0 ? -1 : (int64_t)par[v]));
 }
 
 static EdgeWalk walk_of(Graph &g, WorkerHost &Wk, int k) {
@@ -1938,7 +1920,7 @@ void min_parents(Graph &g, int64_t *out) {
         min_parents_device(g, g.last_source);
         g.last_parent_mode = 2;
     }
-    DBFS_CUDA(cudaMemcpyAsync(out, g.parents_dev(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
+    DBFS_CUDA(cudaMemcpyAsync(out, g.parents_dev64(), 8 * g.n, cudaMemcpyDeviceToHost, ctx.stream));
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
@@ -2020,7 +2002,7 @@ int validate(Graph &g, int64_t root, const int32_t *levels, const int64_t *paren
     } else {
         DBFS_CHECK(g.last_valid && g.last_parent_mode != 0, DBFS_EINVAL, "no parents on device");
         dist_assemble(g);
-        pa = g.parents_dev();
+        pa = g.parents_dev64();
     }
     DArray<uint8_t> ok;
     ok.alloc(std::max<int64_t>(g.n, 1));

@@ -392,7 +392,7 @@ __device__ __noinline__ void touch_chunk(const View &V, int L, uint32_t c) {
 // push_stage): one L2 test decides; a claim sets it and the next-frontier bit.
 // F copies the folded visited bitmap back into it (pull finds included).
 __device__ __forceinline__ void claim_on(uint32_t *__restrict__ seen, uint32_t *__restrict__ nx,
-                                         int64_t *__restrict__ nparent, int parents, uint32_t c, int64_t parent) {
+                                         parent_t *__restrict__ nparent, int parents, uint32_t c, parent_t parent) {
     const uint32_t wd = c >> 5, bit = 1u << (c & 31);
     if (__ldcg(&seen[wd]) & bit) return;  // visited, or claimed this level (possibly stale: then harmless)
     atomicOr(&seen[wd], bit);             // results unused -> RED.OR
@@ -400,7 +400,7 @@ __device__ __forceinline__ void claim_on(uint32_t *__restrict__ seen, uint32_t *
     if (parents) nparent[c] = parent;     // the level is written by F3 (word order, coalesced)
 }
 
-__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, int64_t parent, bool light) {
+__device__ __forceinline__ void claim_normal(const View &V, int L, uint32_t c, parent_t parent, bool light) {
     const uint32_t wd = c >> 5, bit = 1u << (c & 31);
     if (__ldcg(&V.nseen[wd]) & bit) return;
     claim_on(V.nseen, V.nfront[(L + 1) & 1], V.nparent, V.parents, c, parent);
@@ -1145,7 +1145,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](bool hit, uint32_t c, uint32_t x) {
                       warp_mark(V.nfront[(L + 1) & 1], hit, c);
-                      if (hit && V.parents) V.nparent[c] = __ldg(&V.del_gid[x]);
+                      if (hit && V.parents) V.nparent[c] = (parent_t)__ldg(&V.del_gid[x]);
                   });
     }
     tt.stop(AT, 3);
@@ -1164,7 +1164,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                       warp_mark(V.dnext[L & 1], hit, x);
                       if (hit) {
                           vc.dirty = 1;
-                          if (V.parents) V.dcand[x] = __ldg(&V.del_gid[y]);
+                          if (V.parents) V.dcand[x] = (parent_t)__ldg(&V.del_gid[y]);
                       }
                   });
     }
@@ -1188,7 +1188,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                       warp_mark(V.dnext[L & 1], hit, x);
                       if (hit) {
                           vc.dirty = 1;
-                          if (V.parents) V.dcand[x] = (int64_t)c * p + w;
+                          if (V.parents) V.dcand[x] = (parent_t)(c * (uint32_t)p + (uint32_t)w);
                       }
                   });
     }
@@ -1254,17 +1254,17 @@ __device__ __forceinline__ void take_first(uint32_t *first, uint32_t x, uint64_t
 // the minimum over the candidates of the workers that found it.
 constexpr int NB_DEL = 4;  // new delegates per lane whose loads are in flight together (F1)
 
-__device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, int64_t gx, int64_t par_known) {
+__device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, int64_t gx, parent_t par_known) {
     const uint32_t xw = x >> 5, xb = x & 31;
     V.dlevel[x] = L + 1;
-    int64_t par = 0x7fffffffffffffffLL;
+    parent_t par = PARENT_MAX;
     if (V.parents) {
         if (V.cand_all && V.P_sources == 1) {
             par = par_known;
         } else if (V.cand_all) {
             for (int s = 0; s < V.P_sources; s++)
                 if ((__ldcg(&V.mask_src[L & 1][s][xw]) >> xb) & 1u) {
-                    int64_t c = __ldcg(&V.cand_src[s][x]);
+                    const parent_t c = __ldcg(&V.cand_src[s][x]);
                     par = c < par ? c : par;
                 }
         } else if ((V.dnext[L & 1][xw] >> xb) & 1u) {
@@ -1362,7 +1362,8 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
         unsigned long long cdn = 0, edn = 0, cdd = 0, edd = 0;
         for (unsigned g0 = 0; g0 < cnt; g0 += 32 * NB_DEL) {
             uint32_t x[NB_DEL], ldn[NB_DEL], ldd[NB_DEL];
-            int64_t gx[NB_DEL], par[NB_DEL];
+            int64_t gx[NB_DEL];
+            parent_t par[NB_DEL];
             bool ok[NB_DEL];
 #pragma unroll
             for (int u = 0; u < NB_DEL; u++) {
@@ -1456,7 +1457,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
                     uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
                     if (!(old & (1u << (rec.x & 31)))) uq++;
                 }
-                claim_normal(V, L, rec.x, (int64_t)rec.y, light);
+                claim_normal(V, L, rec.x, (parent_t)rec.y, light);
             }
         }
         uq = warp_sum(uq);
@@ -1475,7 +1476,7 @@ __device__ void finish_ingest(const View &V, int L, int64_t tid, int64_t nth) {
             uint32_t old = atomicOr(&V.uq[(int64_t)grp * V.nw_n + (rec.x >> 5)], 1u << (rec.x & 31));
             if (!(old & (1u << (rec.x & 31)))) uq++;
         }
-        claim_normal(V, L, rec.x, (int64_t)rec.y, light);
+        claim_normal(V, L, rec.x, (parent_t)rec.y, light);
     }
     uq = warp_sum(uq);
     if (lane_id() == 0 && uq) atomicAdd(&V.ctl->s[L % 3].uq_records, uq);
@@ -1668,10 +1669,10 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
         V.dseen[x >> 5] |= 1u << (x & 31);
         V.dfront[x >> 5] |= 1u << (x & 31);
         V.coarse_d[0][(x >> 10) & (FW - 1)] |= 1u << (x & 31);
-        if (V.parents) V.dparent[x] = source;
+        if (V.parents) V.dparent[x] = (parent_t)source;
         if (V.glevel) {
             V.glevel[source] = 0;
-            if (V.parents) V.gparent[source] = source;
+            if (V.parents) V.gparent[source] = (parent_t)source;
         }
         int64_t ddn = V.off[KIND_DN][x + 1] - V.off[KIND_DN][x];
         int64_t ddd = V.off[KIND_DD][x + 1] - V.off[KIND_DD][x];
@@ -1693,7 +1694,7 @@ __device__ void seed_worker(const View &V, int64_t source, uint32_t del_id) {
     } else if ((int)(source % V.p) == V.w) {
         uint32_t c = (uint32_t)(source / V.p);
         V.nlevel[c] = 0;
-        if (V.parents) V.nparent[c] = source;
+        if (V.parents) V.nparent[c] = (parent_t)source;
         V.nfront[0][c >> 5] |= 1u << (c & 31);
         V.nvis[c >> 5] |= 1u << (c & 31);
         V.nseen[c >> 5] |= 1u << (c & 31);

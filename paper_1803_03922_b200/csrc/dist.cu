@@ -57,6 +57,11 @@ void nccl_allreduce_u32_sum(Ctx &ctx, uint32_t *dbuf, int64_t count) {
     DBFS_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclUint32, ncclSum, comm_of(ctx), ctx.stream));
 }
 
+void nccl_allreduce_i32_min(Ctx &ctx, int32_t *dbuf, int64_t count) {
+    if (count <= 0) return;
+    DBFS_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclInt32, ncclMin, comm_of(ctx), ctx.stream));
+}
+
 void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op) {  // 0 sum, 1 min, 2 max
     if (count <= 0) return;
     DBFS_NCCL(ncclAllReduce(dbuf, dbuf, (size_t)count, ncclInt64, op == 2 ? ncclMax : (op ? ncclMin : ncclSum),

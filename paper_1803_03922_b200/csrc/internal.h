@@ -18,6 +18,14 @@
 
 namespace dbfs {
 
+// Parent ids on the device: global vertex ids as int32 (n < 2^31, checked
+// when the BFS resources are set up), widened to the reference's int64 only
+// where results leave the device (fetch, batch staging, validation of
+// caller arrays).  Half the footprint of int64 parents keeps the scattered
+// claim-time parent stores inside L2.
+using parent_t = int32_t;
+constexpr parent_t PARENT_MAX = 0x7fffffff;
+
 // Per-level counters of one worker.  Slot L%3 holds the stats of the frontier
 // at level L (accumulated while level L-1 ran) and the activity of level L.
 struct LevelSlot {
@@ -116,10 +124,10 @@ struct alignas(16) View {
     uint32_t *first[4];              // counting pushes: ND/DD per delegate, DN per local normal
     const int64_t *del_gid;
     int32_t *nlevel;
-    int64_t *nparent;
+    parent_t *nparent;
     int32_t *dlevel;
-    int64_t *dparent;
-    int64_t *dcand;
+    parent_t *dparent;
+    parent_t *dcand;
     uint32_t *nvis, *nfront[2], *dvis, *dfront, *dnext[2];
     uint32_t *nseen, *dseen;         // visited(<= L) + claims of level L: the push's single test
     uint32_t *ntouch[2];             // by level parity: 1 bit per 32-word chunk holding frontier normals
@@ -136,14 +144,14 @@ struct alignas(16) View {
     Ctl *ctl;
     Ctl *ctl_all[MAXW];              // in-process: every worker's control block
     uint32_t *nfront_all[2][MAXW];
-    int64_t *nparent_all[MAXW];
+    parent_t *nparent_all[MAXW];
     const uint32_t *mask_src[2][MAXW];
     const uint32_t *mask_mc[2];      // NVLS: multicast address of the masks (one ld_reduce.or = OR over ranks)
-    const int64_t *cand_src[MAXW];
+    const parent_t *cand_src[MAXW];
     IterRec *rec;
     unsigned long long *trace;       // DBFS_TRACE: per level x {V start, V done, F start, F done} x block globaltimer
     int32_t *glevel;                 // global outputs when p == 1 (alias nlevel)
-    int64_t *gparent;
+    parent_t *gparent;
 };
 
 template <typename T>
@@ -229,7 +237,7 @@ struct WorkerHost {
     int64_t dd_base = 0;             // absolute offset of this worker's first dd entry
     // BFS state
     DArray<int32_t> nlevel, dlevel;
-    DArray<int64_t> nparent, dparent, dcand;
+    DArray<parent_t> nparent, dparent, dcand;
     DArray<uint32_t> nvis, nfront0, nfront1, dvis, dfront, dnext0, dnext1;
     DArray<uint32_t> nseen, dseen;   // visited + claims of the running level (push test)
     DArray<uint32_t> ntouch;         // 2 x ntw words: touched chunks of the frontier by parity
@@ -264,7 +272,8 @@ struct Graph {
     DArray<View> views;
     std::vector<View> views_h;
     DArray<int32_t> glevel;          // assembled outputs (p > 1)
-    DArray<int64_t> gparent;
+    DArray<parent_t> gparent;
+    DArray<int64_t> export_pv;       // int64 copy of the parents for the host (fetch, validation)
     DArray<uint32_t> mask_gather;    // dist: allgather of dnext slices
     DArray<int64_t> recv_off;        // dist: per-source inbox offsets of the current level
     DArray<unsigned long long> dist_scratch;
@@ -293,9 +302,9 @@ struct Graph {
     DArray<View> peer_view;
     std::vector<int64_t> cap_all;    // dist: [src][dst] remote record capacities
     std::vector<int32_t *> peer_nlevel;  // peer-mapped outputs of every rank (assembly over NVLink)
-    std::vector<int64_t *> peer_nparent, peer_dparent;
+    std::vector<parent_t *> peer_nparent, peer_dparent;
     DArray<int32_t> asm_lv, asm_mylv;    // NCCL assembly buffers (kept between runs)
-    DArray<int64_t> asm_pv, asm_mypv;
+    DArray<parent_t> asm_pv, asm_mypv;
     DArray<unsigned long long> trace;  // DBFS_TRACE=<file>: block phase timestamps (diagnostics)
     DArray<int32_t> stage_lv[2];     // dbfs_bfs_batch: result staging, double-buffered
     DArray<int64_t> stage_pv[2];
@@ -312,7 +321,8 @@ struct Graph {
     std::vector<cudaEvent_t> batch_evs;  // and per-root timing events
     ~Graph();
     int32_t *levels_dev();
-    int64_t *parents_dev();
+    parent_t *parents_dev();
+    const int64_t *parents_dev64();  // widened into export_pv (ctx stream)
 };
 
 // build.cu
@@ -349,6 +359,7 @@ void nccl_destroy(Ctx &ctx);
 void nccl_abort(Ctx &ctx);
 void nccl_allreduce_u32_sum(Ctx &ctx, uint32_t *dbuf, int64_t count);
 void nccl_allreduce_i64(Ctx &ctx, int64_t *dbuf, int64_t count, int op);  // 0 sum, 1 min, 2 max
+void nccl_allreduce_i32_min(Ctx &ctx, int32_t *dbuf, int64_t count);
 void nccl_allreduce_f64_max(Ctx &ctx, double *dbuf, int64_t count);
 void nccl_allgather_bytes(Ctx &ctx, const void *send, void *recv, int64_t bytes);
 void nccl_alltoallv_bytes(Ctx &ctx, const void *send, const int64_t *send_off, const int64_t *send_bytes,
