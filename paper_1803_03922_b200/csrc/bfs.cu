@@ -194,6 +194,11 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
     }
 }
 
+__global__ void k_narrow_ids(const int64_t *__restrict__ in, int64_t n, uint32_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)in[i];
+}
+
 // int32 device parents -> the reference's int64 (host copies, validation)
 __global__ void k_widen_parents(const parent_t *__restrict__ in, int64_t n, int64_t *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -388,6 +393,11 @@ static void ensure_resources(Graph &g) {
     if (g.symmetric && !getenv("DBFS_NO_TWINS")) build_twins(g);
     Ctx &ctx = *g.ctx;
     DBFS_CHECK(g.n <= PARENT_MAX, DBFS_ECAPACITY, "parent ids are int32 on the device: n must be < 2^31");
+    g.del_gid32.alloc(std::max<int64_t>(g.d, 1));
+    if (g.d) {
+        k_narrow_ids<<<g.ctx->num_sms * 4, 256, 0, g.ctx->stream>>>(g.del_gid.p, g.d, g.del_gid32.p);
+        DBFS_LAUNCHED();
+    }
     const int W = (int)g.workers.size();
     g.W = W;
     g.rec_cap = (int)std::min<int64_t>(std::max<int64_t>(g.n + 2, 16), 1 << 16);
@@ -510,6 +520,7 @@ static void ensure_resources(Graph &g) {
             V.nnz[k] = (unsigned long long)Wk.nnz[k];
         }
         V.del_gid = g.del_gid.p;
+        V.del_gid32 = g.del_gid32.p;
         // indexed with absolute dd offsets (the worker's copy starts at dd_base)
         V.col_sorted_dd = Wk.col_sorted.n ? Wk.col_sorted.p - Wk.dd_base : nullptr;
         for (int k = 1; k < 4; k++) {

@@ -692,7 +692,7 @@ __device__ __forceinline__ void list_push(const View &V, int L, const int64_t *_
         int64_t pb = e < cnt ? pre[e] : total;
         uint32_t v = e < cnt ? list[e] : 0u;
         int64_t rb = e < cnt ? __ldg(&off[v]) : 0;
-        uint32_t gx = e < cnt ? (uint32_t)__ldg(&V.del_gid[v]) : 0u;
+        uint32_t gx = e < cnt ? __ldg(&V.del_gid32[v]) : 0u;
         int64_t wend = 0;
         if (lane == 0) wend = (i + 32 < cnt) ? pre[i + 32] : total;
         wend = __shfl_sync(FULL, wend, 0);
@@ -1145,7 +1145,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](bool hit, uint32_t c, uint32_t x) {
                       warp_mark(V.nfront[(L + 1) & 1], hit, c);
-                      if (hit && V.parents) V.nparent[c] = (parent_t)__ldg(&V.del_gid[x]);
+                      if (hit && V.parents) V.nparent[c] = (parent_t)__ldg(&V.del_gid32[x]);
                   });
     }
     tt.stop(AT, 3);
@@ -1164,7 +1164,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
                       warp_mark(V.dnext[L & 1], hit, x);
                       if (hit) {
                           vc.dirty = 1;
-                          if (V.parents) V.dcand[x] = (parent_t)__ldg(&V.del_gid[y]);
+                          if (V.parents) V.dcand[x] = (parent_t)__ldg(&V.del_gid32[y]);
                       }
                   });
     }
@@ -1375,7 +1375,7 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
             for (int u = 0; u < NB_DEL; u++) {
                 ldn[u] = ok[u] ? __ldg(&V.deg[KIND_DN][x[u]]) : 0u;
                 ldd[u] = ok[u] ? __ldg(&V.deg[KIND_DD][x[u]]) : 0u;
-                gx[u] = (ok[u] && V.glevel) ? __ldg(&V.del_gid[x[u]]) : 0;
+                gx[u] = (ok[u] && V.glevel) ? (int64_t)__ldg(&V.del_gid32[x[u]]) : 0;
                 // a lone in-process worker's new delegates all come from its own mask
                 par[u] = (ok[u] && V.parents && V.cand_all && V.P_sources == 1) ? V.dcand[x[u]] : 0;
             }

@@ -123,6 +123,7 @@ struct alignas(16) View {
     const uint32_t *twin[4];         // indexed by absolute entry position (nullptr: kind has no twins)
     uint32_t *first[4];              // counting pushes: ND/DD per delegate, DN per local normal
     const int64_t *del_gid;
+    const uint32_t *del_gid32;       // the same ids as uint32 (n < 2^31): half the footprint for device lookups
     int32_t *nlevel;
     parent_t *nparent;
     int32_t *dlevel;
@@ -264,6 +265,7 @@ struct Graph {
     DArray<uint32_t> degree;         // out-degree per global vertex
     DArray<uint32_t> del_id;         // delegate id per global vertex, 0xffffffff for normals
     DArray<int64_t> del_gid;         // delegate global ids (ascending)
+    DArray<uint32_t> del_gid32;      // their uint32 copy (BFS lookups)
     DArray<int64_t> off_all;         // concatenated CSR offsets (absolute)
     DArray<uint32_t> col_all;        // concatenated CSR columns
     std::vector<WorkerHost> workers; // local workers
