@@ -287,7 +287,10 @@ constexpr int ROWS_UNR = DBFS_ROWS_UNR;  // normal-row pushes (nn, nd)
 constexpr int LIST_UNR = DBFS_LIST_UNR;  // delegate-list pushes (dn, dd)
 static_assert(ROWS_UNR <= UNR && LIST_UNR <= UNR, "send chunks are sized for UNR");
 constexpr int PULL_U = 4;        // 32 * PULL_U columns per warp-wide pull step
-constexpr int PROBE = 4;         // candidate groups whose first entry is probed together
+#ifndef DBFS_PROBE
+#define DBFS_PROBE 2
+#endif
+constexpr int PROBE = DBFS_PROBE;  // candidate groups whose first entry is probed together
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ bool tbit(const uint32_t *b, uint32_t i) { return (b[i >> 5] >> (i & 31)) & 1u; }
