@@ -1255,7 +1255,10 @@ __device__ __forceinline__ void take_first(uint32_t *first, uint32_t x, uint64_t
 // gx = its global id (loaded when the global outputs are written here), par =
 // its parent when the caller already has it (one in-process worker), else
 // the minimum over the candidates of the workers that found it.
-constexpr int NB_DEL = 4;  // new delegates per lane whose loads are in flight together (F1)
+#ifndef DBFS_NB
+#define DBFS_NB 4
+#endif
+constexpr int NB_DEL = DBFS_NB;  // new vertices per lane whose loads are in flight together (F1, F3)
 
 __device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, int64_t gx, parent_t par_known) {
     const uint32_t xw = x >> 5, xb = x & 31;
