@@ -1045,7 +1045,10 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
         if (trace_path) {
             std::vector<unsigned long long> tr(g.trace.n);
             DBFS_CUDA(cudaMemcpy(tr.data(), g.trace.p, g.trace.bytes(), cudaMemcpyDeviceToHost));
-            if (FILE *f = fopen(trace_path, "a")) {
+            // one file per rank when several ranks share a process (device groups)
+            const std::string tpath = ctx.local_group ? std::string(trace_path) + "." + std::to_string(ctx.rank)
+                                                      : std::string(trace_path);
+            if (FILE *f = fopen(tpath.c_str(), "a")) {
                 const int nbk = g.pgrid;
                 for (int lv = 0; lv < std::min(iterations, 64); lv++)
                     for (int ph = 0; ph < 8; ph++)
