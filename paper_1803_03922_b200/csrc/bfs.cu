@@ -194,6 +194,15 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
     }
 }
 
+// first column of every row [off[r], off[r+1]) of a kind (pull first probes)
+__global__ void k_row_heads(const int64_t *__restrict__ off, int64_t rows, const uint32_t *__restrict__ col,
+                            int64_t col_base, uint32_t *__restrict__ head) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = off[r];
+        head[r] = b < off[r + 1] ? col[b - col_base] : 0u;
+    }
+}
+
 __global__ void k_narrow_ids(const int64_t *__restrict__ in, int64_t n, uint32_t *__restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = (uint32_t)in[i];
@@ -463,6 +472,21 @@ static void ensure_resources(Graph &g) {
         }
         Wk.ctl.alloc(1);
         Wk.rec.alloc(g.rec_cap);
+        if (!getenv("DBFS_NO_HEADS"))  // row heads of the pulled kinds
+            for (int k = 1; k < 4; k++) {
+                if (Wk.rows[k] <= 0 || Wk.head[k].n) continue;
+                Wk.head[k].alloc(Wk.rows[k]);
+                k_row_heads<<<ctx.num_sms * 4, 256, 0, ctx.stream>>>(g.off_all.p + Wk.base[k], Wk.rows[k],
+                                                                     g.col_all.p, 0, Wk.head[k].p);
+                DBFS_LAUNCHED();
+                if (k == KIND_DD && Wk.col_sorted.n) {
+                    Wk.head_sorted.alloc(Wk.rows[k]);
+                    k_row_heads<<<ctx.num_sms * 4, 256, 0, ctx.stream>>>(g.off_all.p + Wk.base[k], Wk.rows[k],
+                                                                         Wk.col_sorted.p, Wk.dd_base,
+                                                                         Wk.head_sorted.p);
+                    DBFS_LAUNCHED();
+                }
+            }
         for (int k = 1; k < 4; k++)
             if (Wk.twin[k].n && !Wk.first[k].n) {
                 Wk.first[k].alloc(std::max<int64_t>(k == KIND_DN ? nl : g.d, 1));
@@ -523,6 +547,9 @@ static void ensure_resources(Graph &g) {
         V.del_gid32 = g.del_gid32.p;
         // indexed with absolute dd offsets (the worker's copy starts at dd_base)
         V.col_sorted_dd = Wk.col_sorted.n ? Wk.col_sorted.p - Wk.dd_base : nullptr;
+        for (int k = 0; k < 4; k++) V.head[k] = Wk.head[k].n ? Wk.head[k].p : nullptr;
+        V.head_sorted_dd = Wk.head_sorted.n ? Wk.head_sorted.p : nullptr;
+        if (V.col_sorted_dd && !V.head_sorted_dd) V.head[KIND_DD] = nullptr;  // both orders or neither
         for (int k = 1; k < 4; k++) {
             V.twin[k] = Wk.twin[k].n ? Wk.twin[k].p - Wk.twin_base[k] : nullptr;
             V.first[k] = Wk.twin[k].n ? Wk.first[k].p : nullptr;

@@ -857,9 +857,9 @@ struct WarpChunks {
 template <class CandF, class HitF>
 __device__ __forceinline__ void pull_kind(int64_t nw, int cw, int64_t gw, int64_t TW, unsigned *sched, uint32_t *list,
                                           const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
-                                          const uint32_t *__restrict__ front, const uint32_t *filt,
-                                          unsigned long long &insp, unsigned long long &rows, CandF cand,
-                                          HitF on_hit) {
+                                          const uint32_t *__restrict__ head, const uint32_t *__restrict__ front,
+                                          const uint32_t *filt, unsigned long long &insp, unsigned long long &rows,
+                                          CandF cand, HitF on_hit) {
     const unsigned lane = lane_id();
     for (WarpChunks ch(sched, nw, cw, gw, TW); ch.valid(); ch.next()) {
         const int64_t wi = ch.word(nw);
@@ -879,16 +879,34 @@ __device__ __forceinline__ void pull_kind(int64_t nw, int cw, int64_t gw, int64_
                 ok[q] = i < cnt;
                 v[q] = ok[q] ? list[i] : 0u;
             }
+            if (head) {
+                // row heads: a candidate's first column from a dense per-row array
+                // (coalesced, no offsets, no random column sector); only the misses
+                // load their offsets and scan on from the second entry.  Candidates
+                // come from the rows-present bitmap, so every row has a head.
 #pragma unroll
-            for (int q = 0; q < PROBE; q++) {
-                b[q] = ok[q] ? __ldg(&off[v[q]]) : 0;
-                e[q] = ok[q] ? __ldg(&off[v[q] + 1]) : 0;
+                for (int q = 0; q < PROBE; q++) c0[q] = ok[q] ? __ldg(&head[v[q]]) : 0u;
+#pragma unroll
+                for (int q = 0; q < PROBE; q++)
+                    h0[q] = ok[q] && (!filt || coarse_hit(filt, c0[q])) && tbit(front, c0[q]);
+#pragma unroll
+                for (int q = 0; q < PROBE; q++) {
+                    const bool need = ok[q] && !h0[q];
+                    b[q] = need ? __ldg(&off[v[q]]) : 0;
+                    e[q] = need ? __ldg(&off[v[q] + 1]) : (h0[q] ? 1 : 0);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PROBE; q++) {
+                    b[q] = ok[q] ? __ldg(&off[v[q]]) : 0;
+                    e[q] = ok[q] ? __ldg(&off[v[q] + 1]) : 0;
+                }
+#pragma unroll
+                for (int q = 0; q < PROBE; q++) c0[q] = (ok[q] && b[q] < e[q]) ? __ldg(&col[b[q]]) : 0u;
+#pragma unroll
+                for (int q = 0; q < PROBE; q++)
+                    h0[q] = ok[q] && b[q] < e[q] && (!filt || coarse_hit(filt, c0[q])) && tbit(front, c0[q]);
             }
-#pragma unroll
-            for (int q = 0; q < PROBE; q++) c0[q] = (ok[q] && b[q] < e[q]) ? __ldg(&col[b[q]]) : 0u;
-#pragma unroll
-            for (int q = 0; q < PROBE; q++)
-                h0[q] = ok[q] && b[q] < e[q] && (!filt || coarse_hit(filt, c0[q])) && tbit(front, c0[q]);
 #pragma unroll
             for (int q = 0; q < PROBE; q++) {
                 PullRes r;
@@ -1144,7 +1162,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (ex[KIND_DN] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_ND];
         const uint32_t *nvis = V.nvis;
-        pull_kind(V.nw_n, DBFS_CWN, gw, TW, dyn_pull(V, cum, KIND_DN, TW) ? &AT.sched[1] : nullptr, list, V.off[KIND_ND], V.col[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
+        pull_kind(V.nw_n, DBFS_CWN, gw, TW, dyn_pull(V, cum, KIND_DN, TW) ? &AT.sched[1] : nullptr, list, V.off[KIND_ND], V.col[KIND_ND], V.head[KIND_ND], V.dfront, filt, vc.insp_bwd[KIND_DN], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~nvis[wi]; },
                   [&](bool hit, uint32_t c, uint32_t x) {
                       warp_mark(V.nfront[(L + 1) & 1], hit, c);
@@ -1160,8 +1178,10 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
         // reported FORWARD: any scan order finds the same set, so use the rows
         // sorted by neighbour degree (hubs first); reported BACKWARD: the
         // reference order, whose early-exit position is the counter.
-        const uint32_t *cdd = (dirs[KIND_DD] == FWD && V.col_sorted_dd) ? V.col_sorted_dd : V.col[KIND_DD];
-        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_DD, TW) ? &AT.sched[2] : nullptr, list, V.off[KIND_DD], cdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
+        const bool sorted = dirs[KIND_DD] == FWD && V.col_sorted_dd;
+        const uint32_t *cdd = sorted ? V.col_sorted_dd : V.col[KIND_DD];
+        const uint32_t *hdd = sorted ? V.head_sorted_dd : V.head[KIND_DD];
+        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_DD, TW) ? &AT.sched[2] : nullptr, list, V.off[KIND_DD], cdd, hdd, V.dfront, filt, vc.insp_bwd[KIND_DD], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
                   [&](bool hit, uint32_t x, uint32_t y) {
                       warp_mark(V.dnext[L & 1], hit, x);
@@ -1184,7 +1204,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     if (ex[KIND_ND] == BWD) {
         const uint32_t *srcb = V.src_bits[KIND_DN];
         const uint32_t *dvis = V.dvis;
-        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_ND, TW) ? &AT.sched[3] : nullptr, list, V.off[KIND_DN], V.col[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
+        pull_kind(V.nw_d, DBFS_CWD, gw, TW, dyn_pull(V, cum, KIND_ND, TW) ? &AT.sched[3] : nullptr, list, V.off[KIND_DN], V.col[KIND_DN], V.head[KIND_DN], nfront_cur, nfilt ? sm.filt : nullptr,
                   vc.insp_bwd[KIND_ND], vc.pull_rows,
                   [&](int64_t wi) { return srcb[wi] & ~dvis[wi]; },
                   [&](bool hit, uint32_t x, uint32_t c) {

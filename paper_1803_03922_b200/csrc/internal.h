@@ -120,6 +120,8 @@ struct alignas(16) View {
     const uint32_t *src_bits[4];     // rows present: [NN]/[ND] per local normal, [DN]/[DD] per delegate
     const uint32_t *deg[4];          // row lengths ([ND], [DN], [DD])
     const uint32_t *col_sorted_dd;   // dd rows reordered by neighbour degree (executor pulls only)
+    const uint32_t *head[4];         // first column of every row of the kind (pull first probes; nullptr: none)
+    const uint32_t *head_sorted_dd;  // first column of every sorted dd row
     const uint32_t *twin[4];         // indexed by absolute entry position (nullptr: kind has no twins)
     uint32_t *first[4];              // counting pushes: ND/DD per delegate, DN per local normal
     const int64_t *del_gid;
@@ -231,6 +233,8 @@ struct WorkerHost {
     DArray<uint32_t> src_bits[4];
     DArray<uint32_t> deg[4];         // row lengths: [ND] per local normal, [DN]/[DD] per delegate
     DArray<uint32_t> col_sorted;     // dd rows with neighbours by descending degree (executor pulls)
+    DArray<uint32_t> head[4];        // [ND]/[DN]/[DD]: first column per row (0 for empty rows)
+    DArray<uint32_t> head_sorted;    // first column per sorted dd row
     DArray<uint32_t> twin[4];        // [ND]/[DN]/[DD]: per entry, the source's position in the target's reverse row
     int64_t twin_base[4] = {0, 0, 0, 0};  // absolute col_all position of the kind's first entry
     DArray<uint32_t> first[4];       // per target: min twin position found by a counting push (0xffffffff = none)
