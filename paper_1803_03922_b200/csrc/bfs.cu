@@ -1580,6 +1580,24 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         // the host's cores shared by the ranks on it (launchers such as torchrun
         // pin OMP_NUM_THREADS to 1, so the count is set here explicitly)
         const int host_threads = std::max(1, std::min(16, usable_cpus() / std::max(1, g.dist ? ctx.nranks : 1)));
+        // depths sent as int32 per root (rest int8): only into page-locked caller
+        // arrays (a pageable destination would make the copy synchronous)
+        const char *fs = getenv("DBFS_COMPACT_SPLIT");
+        const double split_frac = fs ? atof(fs) : 0.4;
+        std::vector<int64_t> split((size_t)count, 0);
+        for (int64_t k = 0; k < count && !g.dist; k++) {
+            if (!levels[k]) continue;
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, levels[k]) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            if (pa.type != cudaMemoryTypeHost) continue;
+            int64_t sp = (int64_t)(split_frac * (double)nout);
+            sp -= sp % 64;  // keeps the int8 part 16-byte aligned for k_pack_result
+            split[(size_t)k] = std::max<int64_t>(0, std::min(sp, nout));
+        }
+        auto split_of = [&](int64_t k) { return split[(size_t)k]; };
         for (int64_t k = 0; k < count + 2; k++) {
             if (k < count) {
                 const int b = (int)(k & 1);
@@ -1595,7 +1613,16 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                     k_assemble<<<blocks, BT, 0, ctx.stream>>>(ca);
                     DBFS_LAUNCHED();
                 } else {
-                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev(), nout, l8,
+                    // the first split_of(k) depths travel as int32 straight into the
+                    // caller's (page-locked) array, the rest as int8 for the host to
+                    // widen: PCIe and the host's memory bandwidth share the work
+                    const int64_t sp = split_of(k);
+                    if (sp) {
+                        k_copy_bytes<<<blocks, 256, 0, ctx.stream>>>((const uint8_t *)g.levels_dev(),
+                                                                     (uint8_t *)g.stage_lv[b].p, 4 * sp);
+                        DBFS_LAUNCHED();
+                    }
+                    k_pack_result<<<blocks, 256, 0, ctx.stream>>>(g.levels_dev() + sp, nout - sp, l8 + 4 * sp,
                                                                   g.esc.p + b);
                     DBFS_LAUNCHED();
                     if (want_par) {
@@ -1608,8 +1635,12 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 // while the host widens root k-2 (host set k%3 last held root k-3)
                 const int hb = (int)(k % 3);
                 DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
-                DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb], g.stage_lv[b].p, nout, cudaMemcpyDeviceToHost,
-                                          ctx.copy_stream));
+                const int64_t sp = g.dist ? 0 : split_of(k);
+                if (sp)
+                    DBFS_CUDA(cudaMemcpyAsync(levels[k], g.stage_lv[b].p, 4 * sp, cudaMemcpyDeviceToHost,
+                                              ctx.copy_stream));
+                DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb], reinterpret_cast<const int8_t *>(g.stage_lv[b].p) + 4 * sp,
+                                          nout - sp, cudaMemcpyDeviceToHost, ctx.copy_stream));
                 if (want_par && parents[k])  // straight into the caller's array
                     DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * nout, cudaMemcpyDeviceToHost,
                                               ctx.copy_stream));
@@ -1617,7 +1648,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 copy_recs(k);
                 DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
                 DBFS_CUDA(cudaEventRecord(ctx.ev_hdone[hb], ctx.copy_stream));
-                if (st) st[k].d2h_bytes += nout + (want_par && parents[k] ? 8 * nout : 0) + 4;
+                if (st) st[k].d2h_bytes += nout + 3 * sp + (want_par && parents[k] ? 8 * nout : 0) + 4;
             }
             if (k >= 2) {
                 const int64_t j = k - 2;
@@ -1626,7 +1657,10 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 DBFS_CUDA(cudaEventSynchronize(ctx.ev_hdone[hb]));
                 const double tw1 = btrace ? now_ms() : 0;
                 if (g.hesc[hb]) rerun.push_back(j);
-                else if (levels[j]) widen_result(g.hstage8[hb], nullptr, nout, levels[j], nullptr, host_threads);
+                else if (levels[j]) {
+                    const int64_t sp = g.dist ? 0 : split_of(j);
+                    widen_result(g.hstage8[hb], nullptr, nout - sp, levels[j] + sp, nullptr, host_threads);
+                }
                 if (btrace) {
                     t_wait += tw1 - tw0;
                     t_widen += now_ms() - tw1;
