@@ -298,6 +298,7 @@ def measure_series(api, ctx, name, scale, theta, mode, world, dist, scrambled, g
            "mode": mode, "graph": graph, "n_gpus": world, "scaling": scaling, "steps": steps, "roots": len(roots),
            "ms_per_bfs": round(float(np.mean(dev_ms)), 4), "build_s": round(build_s, 2),
            "labeling": "scrambled" if scrambled else "reference", "gpu_launches": int(launches),
+           "device_bytes_per_gpu": int(pg.device_bytes), "m": int(pg.m), "d": int(pg.classification.d),
            "worker_edges_max_over_mean": _load_imbalance(ctx, pg, dist),
            "roofline": roofline_of(ctx, pg, stats, dev_ms, world, dist, peaks), "note": note}
     pg.close()
