@@ -147,7 +147,8 @@ struct AsmArgs {
     int64_t *gparent64;              // or: the reference's int64 parents (staging for the host)
     int parents;
     int64_t first, step, count;  // output i is vertex first + i*step (global: 0, 1, n; rank r's own: r, p, n_local)
-    int8_t *glevel8;             // compact transfer form (dbfs_bfs_batch): depth as int8
+    int8_t *glevel8;             // compact transfer form (dbfs_bfs_batch): depth as int8 from output `split` on
+    int64_t split;               //   (outputs before it as int32 into glevel)
     unsigned *esc;               // depths >= 127 (escaped: the root is re-run with full arrays)
 };
 
@@ -185,7 +186,7 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
             l = a.nlevel[w][i];
             if (a.parents) par = a.nparent[w][i];
         }
-        if (a.glevel8) a.glevel8[o] = pack_level(l, a.esc);
+        if (a.glevel8 && o >= a.split) a.glevel8[o - a.split] = pack_level(l, a.esc);
         else a.glevel[o] = l;
         if (a.parents) {
             if (a.gparent64) a.gparent64[o] = par;
@@ -1585,7 +1586,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         const char *fs = getenv("DBFS_COMPACT_SPLIT");
         const double split_frac = fs ? atof(fs) : 0.4;
         std::vector<int64_t> split((size_t)count, 0);
-        for (int64_t k = 0; k < count && !g.dist; k++) {
+        for (int64_t k = 0; k < count; k++) {
             if (!levels[k]) continue;
             cudaPointerAttributes pa{};
             if (cudaPointerGetAttributes(&pa, levels[k]) != cudaSuccess) {
@@ -1603,9 +1604,13 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 const int b = (int)(k & 1);
                 enqueue_root(k, g.esc.p + b);
                 int8_t *l8 = reinterpret_cast<int8_t *>(g.stage_lv[b].p);
-                if (g.dist) {
+                if (g.dist && !levels[k] && !(want_par && parents[k])) {
+                    // this rank receives nothing for root k (e.g. benchmark() on ranks > 0)
+                } else if (g.dist) {
                     AsmArgs ca = out_asm;
-                    ca.glevel8 = l8;
+                    ca.split = split_of(k);
+                    ca.glevel = g.stage_lv[b].p;
+                    ca.glevel8 = l8 + 4 * ca.split;
                     ca.gparent = nullptr;  // parents travel as int64 (no host widening)
                     ca.gparent64 = want_par ? g.stage_pv[b].p : nullptr;
                     ca.parents = want_par;
@@ -1635,12 +1640,14 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 // while the host widens root k-2 (host set k%3 last held root k-3)
                 const int hb = (int)(k % 3);
                 DBFS_CUDA(cudaStreamWaitEvent(ctx.copy_stream, ctx.ev_ready[b], 0));
-                const int64_t sp = g.dist ? 0 : split_of(k);
+                const int64_t sp = split_of(k);
                 if (sp)
                     DBFS_CUDA(cudaMemcpyAsync(levels[k], g.stage_lv[b].p, 4 * sp, cudaMemcpyDeviceToHost,
                                               ctx.copy_stream));
-                DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb], reinterpret_cast<const int8_t *>(g.stage_lv[b].p) + 4 * sp,
-                                          nout - sp, cudaMemcpyDeviceToHost, ctx.copy_stream));
+                if (levels[k])
+                    DBFS_CUDA(cudaMemcpyAsync(g.hstage8[hb],
+                                              reinterpret_cast<const int8_t *>(g.stage_lv[b].p) + 4 * sp, nout - sp,
+                                              cudaMemcpyDeviceToHost, ctx.copy_stream));
                 if (want_par && parents[k])  // straight into the caller's array
                     DBFS_CUDA(cudaMemcpyAsync(parents[k], g.stage_pv[b].p, 8 * nout, cudaMemcpyDeviceToHost,
                                               ctx.copy_stream));
@@ -1648,7 +1655,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 copy_recs(k);
                 DBFS_CUDA(cudaEventRecord(ctx.ev_done[b], ctx.copy_stream));
                 DBFS_CUDA(cudaEventRecord(ctx.ev_hdone[hb], ctx.copy_stream));
-                if (st) st[k].d2h_bytes += nout + 3 * sp + (want_par && parents[k] ? 8 * nout : 0) + 4;
+                if (st) st[k].d2h_bytes += (levels[k] ? nout + 3 * sp : 0) + (want_par && parents[k] ? 8 * nout : 0) + 4;
             }
             if (k >= 2) {
                 const int64_t j = k - 2;
@@ -1658,7 +1665,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                 const double tw1 = btrace ? now_ms() : 0;
                 if (g.hesc[hb]) rerun.push_back(j);
                 else if (levels[j]) {
-                    const int64_t sp = g.dist ? 0 : split_of(j);
+                    const int64_t sp = split_of(j);
                     widen_result(g.hstage8[hb], nullptr, nout - sp, levels[j] + sp, nullptr, host_threads);
                 }
                 if (btrace) {

@@ -209,6 +209,13 @@ def _run_entry(s, iterations, teps, total_insp, mask_bytes, normal_bytes, s_prim
             "mask_bytes": mask_bytes, "normal_bytes": normal_bytes, "s_prime": s_prime, "levels_digest": digest}
 
 
+def _share_digests(pg, digests):
+    """Rank 0's 8-byte digests to every rank (an NCCL sum with zeros elsewhere)."""
+    vals = np.array([int(d, 16) if d is not None else 0 for d in digests], dtype=np.uint64).view(np.int64)
+    _lib.check(_lib.load().dbfs_ctx_allreduce_sum_i64(pg._ctx.handle, vals.ctypes.data_as(_lib.vp), len(vals)))
+    return [f"{int(v):016x}" for v in vals.view(np.uint64)]
+
+
 def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     """Per-source runs, discard S <= 1, geometric-mean TEPS (engine.py:333-364);
     the Graph500 harmonic mean is reported beside it.
@@ -241,25 +248,34 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
                                                        run.comm_stats.s_prime, run.levels_digest)))
     else:
         n = pg.n
+        # one worker per GPU (torchrun): rank 0 receives every root's levels (the
+        # other ranks take part in the traversals only, so a host widens one copy)
+        # and shares its digests with the ranks over NCCL
+        receiver = pg.nranks == 1 or pg.rank == 0
         chunk = max(1, min(len(sources), (8 << 30) // max(4 * n, 1)))  # <= 8 GiB of host levels per call
         # host level arrays: page-locked, kept with the graph and reused by later
         # calls (pageable pages are faulted in -- or NUMA-migrated -- while the
         # host widens the depths inside the call)
         held = getattr(pg, "_benchmark_levels", None)
-        if held is None or len(held) < chunk or held[0].array.size != n:
+        if receiver and (held is None or len(held) < chunk or held[0].array.size != n):
             pg._benchmark_levels = None
             held = [_lib.pinned_empty(n, np.int32) for _ in range(chunk)]
             pg._benchmark_levels = held
-        bufs = [h.array for h in held]
+        bufs = [h.array for h in held] if receiver else [None] * chunk
         for c0 in range(0, len(sources), chunk):
             roots = sources[c0:c0 + chunk]
             t0 = time.perf_counter()
             outs, sts = bfs_batch(pg, roots, outs=[(bufs[i], None) for i in range(len(roots))], mode=opts.mode,
-                                  parents=opts.parents, stats=True, options=opts, accounting=True)
+                                  parents=opts.parents, stats=True, options=opts, accounting=True,
+                                  compact=True if pg.nranks > 1 else None)
             t_total += time.perf_counter() - t0
-            from concurrent.futures import ThreadPoolExecutor  # digests after the timed call (hashlib drops the GIL)
-            with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
-                digests = list(ex.map(levels_digest, bufs[:len(roots)]))
+            digests = [None] * len(roots)
+            if receiver:
+                from concurrent.futures import ThreadPoolExecutor  # digests after the timed call (hashlib drops the GIL)
+                with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+                    digests = list(ex.map(levels_digest, bufs[:len(roots)]))
+            if pg.nranks > 1:
+                digests = _share_digests(pg, digests)
             for i, (s, st) in enumerate(zip(roots, sts)):
                 if not st.accounting_valid:  # records truncated (deep BFS): exact stats from a single run
                     run = run_bfs(pg, dataclasses.replace(opts, source=s))
