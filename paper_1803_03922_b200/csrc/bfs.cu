@@ -53,9 +53,11 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
 
 // Sense-counting grid barrier with a watchdog: a block that waits > 4 s sets
 // `abort`, every block then leaves the kernel (reported as DBFS_ETIMEOUT).
-// With `gbar` (peer engine) the last local arriver also meets the other GPUs
-// on a system-scope barrier in rank 0's memory before releasing its GPU, so
-// exactly one thread per GPU polls over NVLink.
+// With `pv` (the peer engine's view) the last local arriver also meets the
+// other GPUs before releasing its GPU: it posts the barrier's generation into
+// every rank's mailbox over NVLink (one release store each, no round trip)
+// and then waits on its OWN mailbox until every rank's generation arrived --
+// local polling, so a cross-GPU barrier costs about one NVLink latency.
 // `cv`: the last arriver also evaluates the termination rule of level
 // `cont_level` (over every worker's / rank's control block) once for the grid
 // and publishes it in cv->ctl->cont before releasing; `ts` gets its
@@ -63,38 +65,48 @@ __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned *p) {
 #ifndef DBFS_BAR_SLEEP
 #define DBFS_BAR_SLEEP 64  // ns between a waiting block's polls of the barrier generation
 #endif
-__device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBar *gbar = nullptr,
-                                          unsigned nranks = 1, const View *cv = nullptr, int cont_level = 0,
+constexpr int MAIL_ABORT = MAXW, MAIL_GEN = MAXW + 1, MAIL_WORDS = MAXW + 2;
+
+// (the arriving thread fenced at system scope before it arrived, so the
+// mailbox stores themselves can be relaxed)
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, const View *pv = nullptr,
+                                          const View *cv = nullptr, int cont_level = 0,
                                           unsigned long long *ts = nullptr) {
     __shared__ int s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned gen = ld_acquire_u32(&bar->gen);
-        if (gbar) __threadfence_system();
+        if (pv) __threadfence_system();
         else __threadfence();
         unsigned arrived = atomicAdd(&bar->count, 1u);
         if (arrived == nblocks - 1) {
             if (ts) ts[0] = globaltimer_ns();
-            if (gbar) {
-                // one 64-bit arrival counter in rank 0's memory, never reset: the
-                // k-th barrier completes when it reaches k * nranks, so a GPU
-                // needs one NVLink atomic and then polls (abort every 64 polls)
-                unsigned long long *gc = reinterpret_cast<unsigned long long *>(&gbar->count);
-                const unsigned long long old = atomicAdd_system(gc, 1ull);
-                const unsigned long long target = old - old % nranks + nranks;
+            if (pv) {
+                unsigned long long *mail = pv->pmail;
+                const unsigned long long k = mail[MAIL_GEN] + 1;  // identical barrier sequence on every rank
+                mail[MAIL_GEN] = k;
+                for (int r = 0; r < pv->p; r++) st_relaxed_sys_u64(&pv->pmail_peer[r][pv->w], k);
                 unsigned long long t0 = 0;
                 unsigned polls = 0;
                 bool aborted = false;
-                while (ld_acquire_sys_u64(gc) < target) {
+                for (int j = 0; j < pv->p;) {
+                    if (ld_acquire_sys_u64(&mail[j]) >= k) {
+                        j++;
+                        continue;
+                    }
                     if ((++polls & 63u) == 0) {
-                        if (ld_acquire_sys_u32(&gbar->abort)) {
+                        if (ld_acquire_sys_u64(&mail[MAIL_ABORT])) {
                             aborted = true;
                             break;
                         }
                         const unsigned long long t = globaltimer_ns();
                         if (t0 == 0) t0 = t;
                         else if (t - t0 > 4000000000ull) {
-                            atomicExch_system(&gbar->abort, 1u);
+                            for (int r = 0; r < pv->p; r++) st_relaxed_sys_u64(&pv->pmail_peer[r][MAIL_ABORT], 1ull);
                             aborted = true;
                             break;
                         }
@@ -120,7 +132,7 @@ __device__ __forceinline__ bool grid_sync(GridBar *bar, unsigned nblocks, GridBa
 #endif
             }
         }
-        if (gbar) __threadfence_system();
+        if (pv) __threadfence_system();
         else __threadfence();
         s_ok = ld_acquire_u32(&bar->abort) == 0;
     }
@@ -242,10 +254,11 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
         if (threadIdx.x == 0) V.trace[((size_t)lv * 8 + ph) * gridDim.x + blockIdx.x] = globaltimer_ns();
     };
     phase_init(V, wb, nb);
-    if (!grid_sync(bar, nblocks, gbar, nranks)) return;
+    const View *pv = gbar ? &views[0] : nullptr;  // peer engine: cross-GPU barriers
+    if (!grid_sync(bar, nblocks, pv)) return;
     if (wb == 0 && threadIdx.x == 0)  // SRC_DEL_LOOKUP: the host did not read del_id[source] (dbfs_bfs_batch)
         seed_worker(V, source, src_del == SRC_DEL_LOOKUP ? __ldg(&del_id[source]) : src_del);
-    if (!grid_sync(bar, nblocks, gbar, nranks)) return;
+    if (!grid_sync(bar, nblocks, pv)) return;
     if (timer) V.ctl->t_seeded = globaltimer_ns();
     int L = 0;
     for (;; L++) {
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
             if (__shfl_sync(0xffffffffu, mine, 0)) make_record_warp(V, *V.ctl, L - 1, V.rec[L - 1]);
         }
         stamp(L, 5);
-        if (!grid_sync(bar, nblocks, gbar, nranks, nullptr, 0, tb)) return;
+        if (!grid_sync(bar, nblocks, pv, nullptr, 0, tb)) return;
         if (timer && L < rec_cap) V.rec[L].t[1] = globaltimer_ns();
         stamp(L, 6);
         if (V.peer) {  // peers' records are claimed before the frontier is folded
@@ -280,13 +293,13 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
             phase_finish(V, L, wb, nb, sm, F_DELEGATES | F_NORMALS);
         }
         stamp(L, 7);
-        if (!grid_sync(bar, nblocks, gbar, nranks, &views[0], L, tb ? tb + 2 : nullptr)) return;
+        if (!grid_sync(bar, nblocks, pv, &views[0], L, tb ? tb + 2 : nullptr)) return;
         if (timer && L < rec_cap) V.rec[L].t[2] = globaltimer_ns();
     }
     if (wb == 0 && threadIdx.x == 0) V.ctl->last_level = L;
     // peers read this GPU's control block until they leave the loop: nobody may
     // start the next BFS (host resets the block) before every GPU is past it
-    if (gbar && !grid_sync(bar, nblocks, gbar, nranks)) return;
+    if (gbar && !grid_sync(bar, nblocks, pv)) return;
     if (do_assemble) phase_assemble(asm_args, (int64_t)blockIdx.x * BT + threadIdx.x, (int64_t)gridDim.x * BT);
 }
 
@@ -765,8 +778,8 @@ static void setup_peer(Graph &g) {
     const char *env = getenv("DBFS_PEER");
     int ok = (!env || env[0] != '0') && p <= MAXW && g.workers.size() == 1 && (int)g.cap_all.size() == p * p;
     WorkerHost &Wk = g.workers[0];
-    g.gbar_mem.alloc(4);
-    DBFS_CUDA(cudaMemset(g.gbar_mem.p, 0, 16));
+    g.gbar_mem.alloc(2 * MAIL_WORDS);  // this rank's barrier mailbox (u64 words)
+    DBFS_CUDA(cudaMemset(g.gbar_mem.p, 0, g.gbar_mem.bytes()));
     constexpr int NH = 9;
     void *bases[NH] = {Wk.ctl.p,    Wk.dnext0.p,  Wk.dnext1.p,  Wk.dcand.p,    Wk.inbox0.p,
                        Wk.nlevel.p, Wk.nparent.p, Wk.dparent.p, g.gbar_mem.p};
@@ -855,7 +868,6 @@ static void setup_peer(Graph &g) {
                 ptr[(size_t)j * NH + i] = bases[i];
                 continue;
             }
-            if (i == NH - 1 && j != 0) continue;  // only rank 0's barrier is used
             void *q = nullptr;
             if (ok && cudaIpcOpenMemHandle(&q, all[(size_t)j * NH + i], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
                 g.peer_opened.push_back(q);
@@ -909,7 +921,9 @@ static void finish_peer_setup(Graph &g, const std::vector<void *> &ptr) {
         g.peer_nparent[j] = (parent_t *)ptr[(size_t)j * NH + 6];
         g.peer_dparent[j] = (parent_t *)ptr[(size_t)j * NH + 7];
     }
-    g.gbar = ptr[NH - 1];  // rank 0's (its own on rank 0)
+    g.gbar = ptr[NH - 1];  // non-null: the kernel runs the cross-GPU barriers (mailboxes below)
+    V.pmail = reinterpret_cast<unsigned long long *>(g.gbar_mem.p);
+    for (int j = 0; j < p; j++) V.pmail_peer[j] = reinterpret_cast<unsigned long long *>(ptr[(size_t)j * NH + NH - 1]);
     g.peer_view_h = V;
     g.peer_view.alloc(1);
     g.peer_state = 1;

@@ -151,6 +151,8 @@ struct alignas(16) View {
     const uint32_t *mask_src[2][MAXW];
     const uint32_t *mask_mc[2];      // NVLS: multicast address of the masks (one ld_reduce.or = OR over ranks)
     const parent_t *cand_src[MAXW];
+    unsigned long long *pmail;       // peer engine: this rank's barrier mailbox (arrivals by rank, abort, gen)
+    unsigned long long *pmail_peer[MAXW];  // every rank's mailbox (own included)
     IterRec *rec;
     unsigned long long *trace;       // DBFS_TRACE: per level x {V start, V done, F start, F done} x block globaltimer
     int32_t *glevel;                 // global outputs when p == 1 (alias nlevel)
