@@ -1147,7 +1147,7 @@ __device__ void phase_visit(const View &V, int L, int wb, int nb, Smem &sm) {
     // are tested in shared memory first (block-uniform decisions).
     const bool dpull = ex[KIND_DN] == BWD || ex[KIND_DD] == BWD;
     const bool dfilt = DBFS_FILTER && dpull && (double)S.dfront < 0.7 * FW * 32;
-    const bool nfilt = DBFS_FILTER && ex[KIND_ND] == BWD && (double)S.nfront < 0.7 * FW * 32;
+    const bool nfilt = false;  // (the normal frontier has no coarse filter: light levels list their chunks)
     if (dfilt) {
         __syncthreads();
         const uint32_t *src = V.coarse_d[L & 1];
