@@ -431,6 +431,9 @@ __device__ __forceinline__ unsigned long long *block_sendmask() {
 // bit per global id (test, then set) keeps each remote target to a single
 // record per sender.  The reference counters see every record
 // (vc.records, the destination mask).
+#ifndef DBFS_SENT_WAIT
+#define DBFS_SENT_WAIT 0  // 1: ship only if the returning atomic saw the bit clear (no duplicate records)
+#endif
 template <int U>
 __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool (&need)[U], const uint32_t (&o)[U],
                                                 const uint32_t (&c)[U], const uint32_t (&parent)[U],
@@ -476,15 +479,20 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
             const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
             w[u] = need[u] ? __ldcg(&V.sent[gv >> 5]) : 0xffffffffu;
         }
+        // mark and ship without waiting for the atomic's old value: two senders
+        // racing on one target may both ship it (the owner's claim is
+        // idempotent; a segment holds one record per remote edge at most)
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t gv = c[u] * (uint32_t)V.p + o[u];
             const uint32_t bit = 1u << (gv & 31);
             ship[u] = need[u] && !(w[u] & bit);
-            if (ship[u]) w[u] = atomicOr(&V.sent[gv >> 5], bit);
+#if DBFS_SENT_WAIT
+            if (ship[u]) ship[u] = !(atomicOr(&V.sent[gv >> 5], bit) & bit);
+#else
+            if (ship[u]) atomicOr(&V.sent[gv >> 5], bit);
+#endif
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) ship[u] = ship[u] && !(w[u] & (1u << ((c[u] * (uint32_t)V.p + o[u]) & 31)));
     } else {
 #pragma unroll
         for (int u = 0; u < U; u++) ship[u] = need[u];
