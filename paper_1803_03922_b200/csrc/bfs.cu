@@ -19,6 +19,9 @@
 
 #include "bfs_device.cuh"
 
+#ifndef DBFS_VIEW_SMEM
+#define DBFS_VIEW_SMEM 1  // the block's View read from shared memory (0: from global, read-only path)
+#endif
 #ifndef DBFS_MINB
 #define DBFS_MINB 1
 #endif
@@ -243,7 +246,11 @@ __global__ void __launch_bounds__(BT, DBFS_MINB) k_bfs_persistent(const View *__
         for (int i = threadIdx.x; i < (int)(sizeof(View) / 16); i += blockDim.x) dst[i] = src[i];
         __syncthreads();
     }
+#if DBFS_VIEW_SMEM
     const View &V = sm.view;
+#else
+    const View &V = views[wsel];
+#endif
     const unsigned nblocks = gridDim.x;
     const bool timer = wb == 0 && threadIdx.x == 0;
     if (timer) V.ctl->t_start = globaltimer_ns();

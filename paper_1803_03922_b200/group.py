@@ -248,6 +248,8 @@ def bfs_batch(pg: GroupPartitionedGraph, roots, outs, **kw):
     """Rank 0 receives every root's outputs; the other ranks take part in the
     collective traversals and assemblies only."""
     from .engine import bfs_batch as one
+    if kw.get("parents") == "min":  # checked here: a rank failing in C would abort the whole group
+        raise ValueError("min-ID parents are not available in multi-GPU batches; use bfs(pg, root, parents='min')")
     kw = dict(kw)
     compact = kw.pop("compact", None)
     stats = kw.pop("stats", False)
