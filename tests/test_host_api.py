@@ -85,3 +85,36 @@ def test_traversal_helpers_equal_reference(reference):
     for args in ((100, 10, 30), (7, 3, 2), (0, 1, 0)):
         assert traversal.estimate_backward_workload(*args) == rt.estimate_backward_workload(*args)
     assert traversal.DEFAULT_FACTOR0 == rt.DEFAULT_FACTOR0
+
+
+def test_device_group_placement_rule(monkeypatch):
+    """group_for: ClusterShape(.., P) in one process goes on P GPUs only when P
+    are visible, n >= 2^20 and DBFS_DEVICE_GROUP is not 0 (CPU-only check of
+    the decision; the groups themselves are tested on GPUs)."""
+    from paper_1803_03922_b200 import _lib, group
+    made = []
+    monkeypatch.setattr(group, "DeviceGroup", lambda devs: made.append(devs) or ("group", tuple(devs)))
+    monkeypatch.setattr(group, "_groups", {})
+    monkeypatch.setattr(_lib, "device_count", lambda: 4)
+    assert group.group_for(1, "auto", 1 << 24) is None
+    assert group.group_for(2, None, 1 << 24) is None
+    assert group.group_for(8, "auto", 1 << 24) is None          # more workers than GPUs: simulated
+    assert group.group_for(4, "auto", 1 << 16) is None          # small graph: one device
+    assert group.group_for(4, "auto", 1 << 24) == ("group", (0, 1, 2, 3))
+    assert group.group_for(2, [2, 3], 1 << 10) == ("group", (2, 3))  # explicit devices: any size
+    with pytest.raises(ValueError):
+        group.group_for(2, [0, 1, 2], 1 << 24)
+    monkeypatch.setenv("DBFS_DEVICE_GROUP", "0")
+    assert group.group_for(4, "auto", 1 << 24) is None
+    assert made == [[0, 1, 2, 3], [2, 3]]
+
+
+def test_digest_sharing_roundtrip(monkeypatch):
+    """benchmark() across ranks: rank 0's hex digests survive the int64 round
+    trip used to share them over NCCL (sum with zeros)."""
+    import numpy as np
+    from paper_1803_03922_b200 import engine
+    digests = ["ffffffffffffffff", "0000000000000001", "8000000000000000", "03be53e75d9c90ed"]
+    vals = np.array([int(d, 16) for d in digests], dtype=np.uint64).view(np.int64)
+    back = [f"{int(v):016x}" for v in vals.view(np.uint64)]
+    assert back == digests
