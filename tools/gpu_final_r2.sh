@@ -13,5 +13,5 @@ for N in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2956$N bench.py --gpus $N --impl reference > $O/ref_n$N.json 2> $O/ref_n$N.err; echo "ref$N rc=$?"
 done
 for P in 2 4; do timeout 900 python tools/group_bench.py $P $((24 + P / 2)) dobfs scramble 2>&1 | grep -v NCCL > $O/group_p$P.txt; DBFS_NVLS=1 timeout 900 python tools/group_bench.py $P $((24 + P / 2)) dobfs scramble 2>&1 | grep -v NCCL >> $O/group_p$P.txt; done
-timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29571 bench.py --gpus 4 --graph er --scale 28 --scaling strong --theta 64 --mode bfs --no-series --steps 2 > $O/bench_er_s28_bfs_n4.json 2> $O/bench_er_n4.err; echo "er4 rc=$?"
+for N in 2 4; do timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2957$N bench.py --gpus $N --graph er --scale 28 --scaling strong --theta 64 --mode bfs --no-series --no-cpu-baseline --steps 2 > $O/bench_er_s28_bfs_n$N.json 2> $O/bench_er_n$N.err; echo "er$N rc=$?"; done
 ls $O
