@@ -141,6 +141,8 @@ typedef struct {
     double finish_us;           /* device time of the barrier/apply phase */
     double sync_us[4];          /* persistent engines: visit compute (to the last local block), visit cross-GPU
                                    barrier wait, finish compute, finish cross-GPU wait */
+    double comm_us;             /* NCCL level loop (engine 1): measured device time of the level's exchange
+                                   (delegate-mask all-gather + record all-to-all), else 0 */
 } dbfs_iteration;
 
 const char *dbfs_last_error(void);

@@ -67,7 +67,7 @@ class IterationC(ctypes.Structure):
                 ("normal_bytes", i64), ("message_count", i64), ("pair_count", i64),
                 ("frontier_normals", i64), ("frontier_delegates", i64), ("work", i64 * 4), ("exec_dirs", i32 * 4),
                 ("task_avg_us", dbl * 8), ("task_max_us", dbl * 8), ("visit_us", dbl), ("finish_us", dbl),
-                ("sync_us", dbl * 4)]
+                ("sync_us", dbl * 4), ("comm_us", dbl)]
 
 
 P = ctypes.POINTER

@@ -27,6 +27,7 @@ class CommStats:
     message_count: list = field(default_factory=list)
     pair_count: list = field(default_factory=list)
     wire_bytes: int = 0  # bytes actually moved (8-byte records with parents, masks)
+    measured_time_s: float = 0.0  # NCCL level loop: measured exchange time (0: fused into the peer kernel)
 
     @property
     def total_mask_bytes(self) -> float:

@@ -723,6 +723,11 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     int64_t *st_all = st_dev + S;
     k_pack_status<<<1, 32, 0, ctx.stream>>>(Wk.ctl.p, L, p, st_dev);
     DBFS_LAUNCHED();
+    if (!ctx.ev_c0) {
+        DBFS_CUDA(cudaEventCreate(&ctx.ev_c0));
+        DBFS_CUDA(cudaEventCreate(&ctx.ev_c1));
+    }
+    DBFS_CUDA(cudaEventRecord(ctx.ev_c0, ctx.stream));  // the level's exchange starts
     nccl_allgather_bytes(ctx, st_dev, st_all, 8 * S);
     uint32_t *own = g.views_h[0].dnext[L & 1];  // (NVLS: the multicast-bound copy)
     nccl_allgather_bytes(ctx, own, g.mask_gather.p, nw_d * 4);
@@ -750,6 +755,14 @@ static bool dist_level(Graph &g, int L, int grid, std::vector<IterRec> &recs) {
     }
     uint2 *inbox = (L & 1) ? Wk.inbox1.p : Wk.inbox0.p;
     nccl_alltoallv_bytes(ctx, Wk.sendbuf.p, soff.data(), sbytes.data(), inbox, roff.data(), rbytes.data());
+    DBFS_CUDA(cudaEventRecord(ctx.ev_c1, ctx.stream));
+    {
+        DBFS_CUDA(cudaEventSynchronize(ctx.ev_c1));
+        float ms = 0.f;
+        DBFS_CUDA(cudaEventElapsedTime(&ms, ctx.ev_c0, ctx.ev_c1));
+        if ((int64_t)g.last_comm_us.size() <= L) g.last_comm_us.resize(L + 1, 0.0);
+        g.last_comm_us[L] = 1e3 * ms;
+    }
     g.h_status[S * p] = racc;
     DBFS_CUDA(cudaMemcpyAsync(&Wk.ctl.p->s[L % 3].inbox, &g.h_status[S * p], 8, cudaMemcpyHostToDevice, ctx.stream));
     if (g.views_h[0].uniquify) {
@@ -1029,6 +1042,7 @@ void run_bfs(Graph &g, const dbfs_bfs_options &o, dbfs_run_stats *st) {
     DBFS_CUDA(cudaStreamSynchronize(ctx.stream));
 
     const int64_t launches0 = g_kernel_launches;
+    g.last_comm_us.clear();
     const bool assemble = g.p > 1 && !g.dist;
     AsmArgs aa = make_asm(g, parents);
     int iterations = 0;
@@ -1904,6 +1918,7 @@ void iteration_summary(const Graph &g, const IterRec *x0, int64_t it, int last_l
     }
     r.message_count = msgs;
     r.pair_count = last_la ? (int64_t)g.p * g.p / g.p_gpu : (int64_t)g.p * g.p;
+    r.comm_us = it < (int64_t)g.last_comm_us.size() ? g.last_comm_us[it] : 0.0;
     *rec = r;
 }
 

@@ -211,6 +211,7 @@ struct Ctx {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;  // NCCL level loop: around each level's exchange
     int nranks = 1, rank = 0;
     int local_group = 0;             // every rank is a thread of this process (one device each):
                                      // peer arrays are mapped by pointer + peer access, not CUDA IPC
@@ -299,6 +300,7 @@ struct Graph {
     bool assembled = true;           // dist: global outputs gathered for the last run
     bool last_truncated = false;
     std::vector<IterRec> last_rec;   // [iteration][local worker]
+    std::vector<double> last_comm_us;  // NCCL level loop: measured exchange time per level
     std::vector<std::vector<unsigned long long>> last_send_matrix;
     int last_mode = 1, last_la = 0, last_uq = 0;
     // peer engine (dist): CUDA-IPC mapped peer arrays + a cross-GPU barrier

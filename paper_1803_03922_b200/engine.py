@@ -169,6 +169,7 @@ def _per_iteration(pg: PartitionedGraph, iterations: int):
             "mask_bytes": float(rec.mask_bytes),
             "normal_bytes": int(rec.normal_bytes),
         })
+        comm.measured_time_s += float(rec.comm_us) * 1e-6
         comm.mask_bytes.append(float(rec.mask_bytes))
         comm.normal_bytes.append(int(rec.normal_bytes))
         comm.message_count.append(int(rec.message_count))

@@ -57,6 +57,16 @@ for opts in (dict(), dict(uniquify=True), dict(uniquify=True, local_all2all=True
         if any(x[key] != runs[0][key] for x in runs[1:]):
             local_ok = False
             print(f"rank {rank}: engines disagree on {key} with {opts}", flush=True)
+# the NCCL level loop times its exchange (CommStats.measured_time_s); the peer
+# engine has no separate exchange step; the delegate bound covers both runs
+from paper_1803_03922_b200.cost_model import delegate_comm_check
+for e in engines:
+    run = api.run_bfs(pg, BfsOptions(source=roots[1], engine=e))
+    chk = delegate_comm_check(pg, run)
+    timed = run.comm_stats.measured_time_s > 0
+    if timed != (e == "host") or not chk["within_bound"]:
+        local_ok = False
+        print(f"rank {rank}: engine {e}: measured exchange {run.comm_stats.measured_time_s} s, check {chk}", flush=True)
 # bfs_batch: pipelined roots, full outputs and each rank's own vertices (local)
 from paper_1803_03922_b200.engine import bfs_batch
 for local in (False, True):
