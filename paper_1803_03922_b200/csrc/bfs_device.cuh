@@ -562,6 +562,10 @@ __device__ __forceinline__ void warp_send_batch(const View &V, int L, const bool
 
 enum { ACT_NN = 0, ACT_DELEG = 1, ACT_NORMAL = 2 };
 
+#ifndef DBFS_SEEN_L1
+#define DBFS_SEEN_L1 0
+#endif
+
 // Second stage of a push step: U columns per lane are resolved with all
 // status loads issued before any store (stores through the non-restrict state
 // pointers would otherwise serialise one L2 round trip per edge).
@@ -591,7 +595,9 @@ __device__ __forceinline__ void push_stage(const View &V, int L, const uint32_t 
         // (kept separately from the pre-state `vis`, which pulls and counters
         // need; F leaves seen == vis for the next level)
 #pragma unroll
-        for (int u = 0; u < U; u++) s[u] = (valid[u] && local[u]) ? __ldcg(&seen[tgt[u] >> 5]) : 0xffffffffu;
+        for (int u = 0; u < U; u++)
+            s[u] = (valid[u] && local[u]) ? ((DBFS_SEEN_L1 == 1 || (DBFS_SEEN_L1 == 2 && ACT == ACT_DELEG)) ? __ldca(&seen[tgt[u] >> 5]) : __ldcg(&seen[tgt[u] >> 5]))
+                                          : 0xffffffffu;
 #pragma unroll
         for (int u = 0; u < U; u++)
             if (ACT == ACT_DELEG && !((s[u] >> (tgt[u] & 31)) & 1u)) vc.dirty = 1;
@@ -862,6 +868,74 @@ struct WarpChunks {
     }
 };
 
+#ifndef DBFS_PULL_SPLIT
+#define DBFS_PULL_SPLIT 1
+#endif
+#ifndef DBFS_SPLIT_PROBE
+#define DBFS_SPLIT_PROBE 4
+#endif
+constexpr int SPROBE = DBFS_SPLIT_PROBE;  // head probes of 32 candidates in flight per lane (pull_split)
+// Candidates of one chunk (list[0, cnt)) in two passes: all row heads first
+// (PROBE groups of 32 in flight, hits recorded at once), the misses compacted
+// in place to the front of the list, then the misses' scans 32 per step, so a
+// warp's lanes all scan instead of idling beside resolved heads.
+template <class HitF>
+__device__ __forceinline__ void pull_split(unsigned cnt, uint32_t *list, const int64_t *__restrict__ off,
+                                           const uint32_t *__restrict__ col, const uint32_t *__restrict__ head,
+                                           const uint32_t *__restrict__ front, const uint32_t *filt,
+                                           unsigned long long &insp, HitF on_hit) {
+    const unsigned lane = lane_id();
+    unsigned nmiss = 0;
+    for (unsigned g0 = 0; g0 < cnt; g0 += 32 * SPROBE) {
+        uint32_t v[SPROBE], c0[SPROBE];
+        bool ok[SPROBE], h0[SPROBE];
+#pragma unroll
+        for (int q = 0; q < SPROBE; q++) {
+            unsigned i = g0 + q * 32 + lane;
+            ok[q] = i < cnt;
+            v[q] = ok[q] ? list[i] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < SPROBE; q++) c0[q] = ok[q] ? __ldg(&head[v[q]]) : 0u;
+#pragma unroll
+        for (int q = 0; q < SPROBE; q++) h0[q] = ok[q] && (!filt || coarse_hit(filt, c0[q])) && tbit(front, c0[q]);
+        __syncwarp();  // this step's list entries are in registers: misses may overwrite them
+#pragma unroll
+        for (int q = 0; q < SPROBE; q++) {
+            if (h0[q]) insp++;
+            on_hit(h0[q], v[q], c0[q]);
+            const bool miss = ok[q] && !h0[q];
+            const unsigned m = __ballot_sync(FULL, miss);
+            if (miss) list[nmiss + __popc(m & ((1u << lane) - 1u))] = v[q];
+            nmiss += __popc(m);
+        }
+    }
+    __syncwarp();
+    for (unsigned g0 = 0; g0 < nmiss; g0 += 32) {
+        const unsigned i = g0 + lane;
+        const bool ok = i < nmiss;
+        const uint32_t v = ok ? list[i] : 0u;
+        const int64_t b = ok ? __ldg(&off[v]) : 0, e = ok ? __ldg(&off[v + 1]) : 0;
+        PullRes r;
+        r.pos = -1;
+        r.col = 0;
+        int64_t j = e;
+        bool done = !ok || b + 1 >= e;
+        if (!done) done = lane_scan(col, front, filt, b + 1, e, j, r);
+        unsigned pend = __ballot_sync(FULL, !done);
+        while (pend) {
+            int l = __ffs(pend) - 1;
+            pend &= pend - 1;
+            int64_t jl = __shfl_sync(FULL, j, l), el = __shfl_sync(FULL, e, l);
+            PullRes rr = warp_scan_row(col, front, filt, jl, el);
+            if ((int)lane == l) r = rr;
+        }
+        const bool hit = ok && r.pos >= 0;
+        if (ok) insp += (unsigned long long)(hit ? r.pos - b + 1 : e - b);
+        on_hit(hit, v, r.col);
+    }
+}
+
 template <class CandF, class HitF>
 __device__ __forceinline__ void pull_kind(int64_t nw, int cw, int64_t gw, int64_t TW, unsigned *sched, uint32_t *list,
                                           const int64_t *__restrict__ off, const uint32_t *__restrict__ col,
@@ -874,6 +948,11 @@ __device__ __forceinline__ void pull_kind(int64_t nw, int cw, int64_t gw, int64_
         uint32_t word = wi >= 0 ? cand(wi) : 0u;
         unsigned cnt = warp_compact(word, wi, list);
         if (lane == 0) rows += cnt;
+        if (DBFS_PULL_SPLIT && head) {
+            pull_split(cnt, list, off, col, head, front, filt, insp, on_hit);
+            __syncwarp();
+            continue;
+        }
         // First probe of 4 groups at once (4 independent chains per lane):
         // offsets, first column, its status bit.  Most candidates resolve here
         // at dense levels; the rest continue with the geometric lane scan.
