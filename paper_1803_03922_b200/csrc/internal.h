@@ -393,4 +393,7 @@ void exclusive_scan_u32_to_i64(Ctx &ctx, const uint32_t *in, int64_t *out, int64
 void radix_sort_pairs(Ctx &ctx, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, uint32_t *vals_alt,
                       int64_t n, int bits, bool *result_in_alt);
 
+// widen.cpp: compact batch outputs widened on the host (streaming stores)
+void widen_host(const int8_t *l8, const int32_t *p32, int64_t n, int32_t *lv, int64_t *pa, int nthreads);
+
 }  // namespace dbfs

@@ -238,7 +238,7 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
     for s in sources:
         if not (0 <= s < pg.n):
             raise ValueError(f"source {s} out of range [0, {pg.n})")
-    entries, t_total = [], 0.0
+    entries, t_total, d2h = [], 0.0, 0
     if opts.engine == "host":
         for s in sources:
             run = run_bfs(pg, dataclasses.replace(opts, source=s))
@@ -270,6 +270,7 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
                                   parents=opts.parents, stats=True, options=opts, accounting=True,
                                   compact=True if pg.nranks > 1 else None)
             t_total += time.perf_counter() - t0
+            d2h += sum(int(st.d2h_bytes) for st in sts)
             digests = [None] * len(roots)
             if receiver:
                 from concurrent.futures import ThreadPoolExecutor  # digests after the timed call (hashlib drops the GIL)
@@ -302,6 +303,7 @@ def benchmark(pg: PartitionedGraph, sources, opts: BfsOptions) -> dict:
         "harmonic_teps": harmonic,
         "wall_s": t_total,
         "e2e_teps": len(sources) * (pg.m / 2) / t_total if t_total > 0 else 0.0,
+        "d2h_bytes": d2h,  # device -> host bytes of the batch calls (this process)
         "runs": runs,
     }
 
