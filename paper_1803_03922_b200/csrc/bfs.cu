@@ -322,12 +322,15 @@ __global__ void k_batch_prep(const View *__restrict__ views, GridBar *bar) {
 
 // Per-root iteration records of a batch (dbfs_bfs_batch with record_iterations):
 // the first rmax records of every worker into dst[it * W + w].
+// grid (STAGE_BLOCKS, W): only the records of the iterations that ran
+constexpr int STAGE_BLOCKS = 8;
 __global__ void k_stage_recs(const View *__restrict__ views, int W, int rmax, IterRec *__restrict__ dst) {
-    const int w = blockIdx.x;
+    const int w = blockIdx.y;
     const unsigned long long *src = reinterpret_cast<const unsigned long long *>(views[w].rec);
     static_assert(sizeof(IterRec) % 8 == 0, "records are copied in 8-byte words");
     constexpr int NW = sizeof(IterRec) / 8;
-    for (int i = threadIdx.x; i < rmax * NW; i += blockDim.x) {
+    const int nrec = min(rmax, views[w].ctl->last_level + 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrec * NW; i += gridDim.x * blockDim.x) {
         const int it = i / NW, j = i % NW;
         reinterpret_cast<unsigned long long *>(&dst[(size_t)it * W + w])[j] = src[i];
     }
@@ -352,7 +355,7 @@ __global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restric
 __global__ void k_pack_result(const int32_t *__restrict__ lv, int64_t n, int8_t *__restrict__ lv8, unsigned *esc) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = tid; q < (n >> 2); q += nth) {
-        const int4 l = reinterpret_cast<const int4 *>(lv)[q];
+        const int4 l = __ldcs(reinterpret_cast<const int4 *>(lv) + q);
         char4 c;
         c.x = pack_level(l.x, esc);
         c.y = pack_level(l.y, esc);
@@ -1582,7 +1585,7 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         DBFS_CUDA(cudaEventRecord(evs[2 * k + 1], ctx.stream));
         if (o0.parent_mode == 2) min_parents_device(g, src);  // untimed: after the traversal's end event
         if (want_rec) {
-            k_stage_recs<<<W, 256, 0, ctx.stream>>>(g.views.p, W, rmax, drec.p + (size_t)k * rmax * W);
+            k_stage_recs<<<dim3(STAGE_BLOCKS, W), 256, 0, ctx.stream>>>(g.views.p, W, rmax, drec.p + (size_t)k * rmax * W);
             DBFS_LAUNCHED();
         }
         if (esc_k && k >= 2) DBFS_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_done[k & 1], 0));
@@ -1741,9 +1744,20 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             }
         }
     }
-    if (btrace)
+    if (btrace) {
         fprintf(stderr, "[batch] %lld roots: setup %.2f ms, loop+sync %.2f ms (waits %.2f, widening %.2f)\n",
                 (long long)count, tb0 - tentry, now_ms() - tb0, t_wait, t_widen);
+        double tb = 0, tg = 0;  // device: traversals, and what runs between them
+        for (int64_t k = 0; k < count; k++) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, evs[2 * k], evs[2 * k + 1]);
+            if (k + 1 < count) cudaEventElapsedTime(&b, evs[2 * k + 1], evs[2 * k + 2]);
+            tb += a;
+            tg += b;
+        }
+        fprintf(stderr, "[batch] device: traversals %.3f ms/root, between traversals %.3f ms/root\n", tb / count,
+                count > 1 ? tg / (count - 1) : 0.0);
+    }
     std::vector<int2> hi(count);
     DBFS_CUDA(cudaMemcpy(hi.data(), info.p, sizeof(int2) * count, cudaMemcpyDeviceToHost));
     const int64_t launches = g_kernel_launches - launches0;
