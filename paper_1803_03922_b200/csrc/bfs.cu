@@ -354,16 +354,28 @@ __global__ void k_copy_bytes(const uint8_t *__restrict__ src, uint8_t *__restric
 // Compact wire form of the whole-graph outputs (single process): 4 entries per thread.
 __global__ void k_pack_result(const int32_t *__restrict__ lv, int64_t n, int8_t *__restrict__ lv8, unsigned *esc) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = tid; q < (n >> 2); q += nth) {
-        const int4 l = __ldcs(reinterpret_cast<const int4 *>(lv) + q);
-        char4 c;
-        c.x = pack_level(l.x, esc);
-        c.y = pack_level(l.y, esc);
-        c.z = pack_level(l.z, esc);
-        c.w = pack_level(l.w, esc);
-        reinterpret_cast<char4 *>(lv8)[q] = c;
+    constexpr int U = 4;  // int4 loads in flight per thread
+    const int64_t nq = n >> 2;
+    for (int64_t q0 = tid; q0 < nq; q0 += U * nth) {
+        int4 l[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t q = q0 + u * nth;
+            l[u] = q < nq ? __ldcs(reinterpret_cast<const int4 *>(lv) + q) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t q = q0 + u * nth;
+            if (q >= nq) break;
+            char4 c;
+            c.x = pack_level(l[u].x, esc);
+            c.y = pack_level(l[u].y, esc);
+            c.z = pack_level(l[u].z, esc);
+            c.w = pack_level(l[u].w, esc);
+            reinterpret_cast<char4 *>(lv8)[q] = c;
+        }
     }
-    for (int64_t i = ((n >> 2) << 2) + tid; i < n; i += nth) lv8[i] = pack_level(lv[i], esc);
+    for (int64_t i = (nq << 2) + tid; i < n; i += nth) lv8[i] = pack_level(lv[i], esc);
 }
 
 __global__ void __launch_bounds__(BT) k_init(const View *__restrict__ views, int W) {
