@@ -1391,6 +1391,10 @@ __device__ __forceinline__ void new_delegate(const View &V, int L, uint32_t x, i
     }
 }
 
+#ifndef DBFS_F1_FEW
+#define DBFS_F1_FEW 1
+#endif
+
 // F1: delegate mask OR-reduction (comm.py:75-98) -> delegates of level L+1,
 // their state, and the push lists of level L+1 (one packed atomic per warp
 // batch and kind keeps list positions and edge prefixes consistent).
@@ -1411,7 +1415,13 @@ __device__ void finish_delegates(const View &V, int L, int64_t gw, int64_t TW, u
     }
     __syncthreads();
     const unsigned long long src = s_src;
-    const bool dyn = src != 0;  // delegates were found: new-delegate work to balance
+    // delegates were found: new-delegate work to balance, unless this lone
+    // worker's level can have found only a few (every find took at least one
+    // executed nd / dd inspection): then a static sweep without claims
+    const LevelSlot &SW = V.ctl->s[L % 3];
+    const bool few = DBFS_F1_FEW && V.P_sources == 1 &&
+                     __ldcg(&SW.work[KIND_ND]) + __ldcg(&SW.work[KIND_DD]) < (unsigned long long)V.nw_d;
+    const bool dyn = src != 0 && !few;
     // remote masks: 32-word chunks, so every lane has a word and its sources'
     // loads are in flight together (8 per batch) -- NVLink latency, not bandwidth
     // (light levels -- nothing found -- sweep with a static stride: 32-word
