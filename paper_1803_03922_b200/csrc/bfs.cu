@@ -1622,7 +1622,13 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         const int blocks = ctx.num_sms * 4;
         // the host's cores shared by the ranks on it (launchers such as torchrun
         // pin OMP_NUM_THREADS to 1, so the count is set here explicitly)
-        const int host_threads = std::max(1, std::min(16, usable_cpus() / std::max(1, g.dist ? ctx.nranks : 1)));
+        // Whole-graph outputs in a distributed batch go to one receiving rank
+        // (benchmark(), device groups: rank 0), whose host widens n depths per
+        // root while the other ranks only wait on their GPUs: it takes the cores.
+        const bool sole_receiver = g.dist && !local;
+        const int host_threads =
+            sole_receiver ? std::max(1, std::min(32, usable_cpus() - (ctx.nranks - 1)))
+                          : std::max(1, std::min(16, usable_cpus() / std::max(1, g.dist ? ctx.nranks : 1)));
         // depths sent as int32 per root (rest int8): only into page-locked caller
         // arrays (a pageable destination would make the copy synchronous)
         const char *fs = getenv("DBFS_COMPACT_SPLIT");
