@@ -410,6 +410,7 @@ Graph::~Graph() {
     if (h_ctl) cudaFreeHost(h_ctl);
     if (batch_hrec) cudaFreeHost(batch_hrec);
     for (cudaEvent_t e : batch_evs) cudaEventDestroy(e);
+    for (cudaEvent_t e : batch_asm_evs) cudaEventDestroy(e);
     for (int h = 0; h < 3; h++) {
         if (hstage8[h]) cudaFreeHost(hstage8[h]);
         if (hstage32[h]) cudaFreeHost(hstage32[h]);
@@ -1531,7 +1532,13 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
     const double tb0 = now_ms();
-    double t_wait = 0, t_widen = 0;
+    double t_wait = 0, t_widen = 0, t_asm = 0;
+    if (btrace && g.batch_asm_evs.empty())
+        for (int i = 0; i < 4; i++) {
+            cudaEvent_t e;
+            DBFS_CUDA(cudaEventCreate(&e));
+            g.batch_asm_evs.push_back(e);
+        }
     if (compact) ensure_compact_staging(g, nout);
     set_smem_attrs();
     if (g.pgrid <= 0) {
@@ -1663,7 +1670,15 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
                     ca.gparent64 = want_par ? g.stage_pv[b].p : nullptr;
                     ca.parents = want_par;
                     ca.esc = g.esc.p + b;
+                    if (btrace) DBFS_CUDA(cudaEventRecord(g.batch_asm_evs[2 * (k & 1)], ctx.stream));
                     k_assemble<<<blocks, BT, 0, ctx.stream>>>(ca);
+                    if (btrace) {
+                        DBFS_CUDA(cudaEventRecord(g.batch_asm_evs[2 * (k & 1) + 1], ctx.stream));
+                        DBFS_CUDA(cudaEventSynchronize(g.batch_asm_evs[2 * (k & 1) + 1]));
+                        float am = 0;
+                        cudaEventElapsedTime(&am, g.batch_asm_evs[2 * (k & 1)], g.batch_asm_evs[2 * (k & 1) + 1]);
+                        t_asm += am;
+                    }
                     DBFS_LAUNCHED();
                 } else {
                     // the first split_of(k) depths travel as int32 straight into the
@@ -1773,8 +1788,8 @@ void run_bfs_batch(Graph &g, const dbfs_bfs_options &o0, const int64_t *roots, i
             tb += a;
             tg += b;
         }
-        fprintf(stderr, "[batch] device: traversals %.3f ms/root, between traversals %.3f ms/root\n", tb / count,
-                count > 1 ? tg / (count - 1) : 0.0);
+        fprintf(stderr, "[batch] device: traversals %.3f ms/root, between traversals %.3f ms/root (assembly %.3f)\n",
+                tb / count, count > 1 ? tg / (count - 1) : 0.0, t_asm / count);
     }
     std::vector<int2> hi(count);
     DBFS_CUDA(cudaMemcpy(hi.data(), info.p, sizeof(int2) * count, cudaMemcpyDeviceToHost));

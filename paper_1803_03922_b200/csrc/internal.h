@@ -328,6 +328,7 @@ struct Graph {
     DArray<IterRec> batch_drec;      // dbfs_bfs_batch scratch (grow-only): per-root records,
     IterRec *batch_hrec = nullptr;   //   their pinned host copy,
     DArray<int2> batch_info;         //   per-root (iterations, watchdog),
+    std::vector<cudaEvent_t> batch_asm_evs;  // DBFS_BATCH_TRACE: assembly timing
     std::vector<cudaEvent_t> batch_evs;  // and per-root timing events
     ~Graph();
     int32_t *levels_dev();
