@@ -178,34 +178,55 @@ __device__ __forceinline__ int8_t pack_level(int32_t l, unsigned *esc) {
 // Output i holds vertex first + i*step: the whole graph, or (distributed) the
 // vertices a rank owns, v mod p == rank -- a distributed Graph500 result.
 __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
-    for (int64_t o = tid; o < a.count; o += nth) {
-        const int64_t v = a.first + o * a.step;
-        const uint32_t di = a.del_id[v];
-        int32_t l;
-        parent_t par = -1;
-        if (di != 0xffffffffu) {
-            l = a.dlevel[di];
-            if (a.parents && l >= 0) {
+    // AU outputs per thread at a time, every load of the batch issued before
+    // the dependent ones: the peers' depths are NVLink round trips (~2 us), so
+    // one chain per thread left the assembly latency-bound
+    constexpr int AU = 8;
+    for (int64_t o0 = tid; o0 < a.count; o0 += AU * nth) {
+        uint32_t di[AU], w[AU], i[AU];
+        int32_t l[AU];
+        parent_t par[AU];
+#pragma unroll
+        for (int u = 0; u < AU; u++) {
+            const int64_t o = o0 + u * nth;
+            const int64_t v = a.first + (o < a.count ? o : 0) * a.step;
+            di[u] = o < a.count ? a.del_id[v] : 0xfffffffeu;  // 0xfffffffe: no output
+            w[u] = a.pd.mod((uint32_t)v);
+            i[u] = a.pd.div((uint32_t)v);
+        }
+#pragma unroll
+        for (int u = 0; u < AU; u++) {
+            par[u] = -1;
+            if (di[u] == 0xfffffffeu) continue;
+            if (di[u] != 0xffffffffu) {
+                l[u] = a.dlevel[di[u]];
+            } else {
+                l[u] = a.nlevel[w[u]][i[u]];
+                if (a.parents) par[u] = a.nparent[w[u]][i[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < AU; u++) {
+            const int64_t o = o0 + u * nth;
+            if (di[u] == 0xfffffffeu) continue;
+            if (a.parents && di[u] != 0xffffffffu && l[u] >= 0) {
                 if (a.n_dpar) {
-                    par = PARENT_MAX;
+                    parent_t m = PARENT_MAX;
                     for (int s = 0; s < a.n_dpar; s++) {
-                        const parent_t c = a.dpar_src[s][di];
-                        par = c < par ? c : par;
+                        const parent_t c = a.dpar_src[s][di[u]];
+                        m = c < m ? c : m;
                     }
+                    par[u] = m;
                 } else {
-                    par = a.dparent[di];
+                    par[u] = a.dparent[di[u]];
                 }
             }
-        } else {
-            const uint32_t w = a.pd.mod((uint32_t)v), i = a.pd.div((uint32_t)v);
-            l = a.nlevel[w][i];
-            if (a.parents) par = a.nparent[w][i];
-        }
-        if (a.glevel8 && o >= a.split) a.glevel8[o - a.split] = pack_level(l, a.esc);
-        else a.glevel[o] = l;
-        if (a.parents) {
-            if (a.gparent64) a.gparent64[o] = par;
-            else a.gparent[o] = par;
+            if (a.glevel8 && o >= a.split) a.glevel8[o - a.split] = pack_level(l[u], a.esc);
+            else a.glevel[o] = l[u];
+            if (a.parents) {
+                if (a.gparent64) a.gparent64[o] = par[u];
+                else a.gparent[o] = par[u];
+            }
         }
     }
 }
