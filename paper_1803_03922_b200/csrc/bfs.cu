@@ -181,7 +181,10 @@ __device__ void phase_assemble(const AsmArgs &a, int64_t tid, int64_t nth) {
     // AU outputs per thread at a time, every load of the batch issued before
     // the dependent ones: the peers' depths are NVLink round trips (~2 us), so
     // one chain per thread left the assembly latency-bound
-    constexpr int AU = 8;
+#ifndef DBFS_AU
+#define DBFS_AU 8
+#endif
+    constexpr int AU = DBFS_AU;
     for (int64_t o0 = tid; o0 < a.count; o0 += AU * nth) {
         uint32_t di[AU], w[AU], i[AU];
         int32_t l[AU];
