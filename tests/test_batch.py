@@ -98,3 +98,30 @@ def test_compact_rerun_leaves_device_state_consistent(api):
     outs = api.bfs_batch(pg2, [n, 2], parents="min", compact=False)
     lv, pa = outs[1]
     assert pa[2] == 2 and pa[1] == 2 and pa[3] == 2 and pa[0] == 1 and pa[n] == -1
+
+
+@pytest.mark.parametrize("split", ["0", "0.4", "1"])
+def test_compact_split_into_pinned_outputs(api, split, monkeypatch):
+    """The compact transfer into page-locked caller arrays: the first
+    DBFS_COMPACT_SPLIT of the depths travel as int32 straight into the caller's
+    array, the rest as int8 widened on the host (AVX2 streaming stores into an
+    arbitrarily aligned destination) -- every split gives the oracle's depths."""
+    from paper_1803_03922_b200 import _lib
+    monkeypatch.setenv("DBFS_COMPACT_SPLIT", split)
+    scale, seed, theta = 13, 5, 16
+    pg = api.partition_graph(api.build_rmat_graph(api.RmatParams(scale=scale, seed=seed)), theta,
+                             api.ClusterShape(1, 1))
+    src, dst = O.rmat_edges(scale, seed=seed)
+    og = O.partition(src, dst, 1 << scale, theta, 1, 1)
+    roots = [3, 4000, 77, 1234, 9]
+    n = pg.n
+    # one page-locked block, views at 4-byte offsets: destinations not 32-byte aligned
+    held = _lib.pinned_empty(len(roots) * (n + 3) + 8, np.int32)
+    outs = [(held.array[1 + i * (n + 3): 1 + i * (n + 3) + n], None) for i in range(len(roots))]
+    api.bfs_batch(pg, roots, outs=outs, parents=None, compact=True)
+    for r, (lv, _) in zip(roots, outs):
+        assert api.levels_digest(lv) == O.run_bfs(og, r, mode="dobfs")["levels_digest"], (split, r)
+    # benchmark() (its own pinned level arrays) reports the same digests
+    rep = api.benchmark(pg, roots, api.BfsOptions(mode="dobfs"))
+    for run in rep["runs"]:
+        assert run["levels_digest"] == O.run_bfs(og, run["source"], mode="dobfs")["levels_digest"]
