@@ -269,8 +269,10 @@ def roofline_of(ctx, pg, stats, dev_ms, world, dist, peaks, traffic=None):
     peak = peaks["hbm_gbs"] * world
     ach = float(np.mean(b_alg)) / t / 1e9
     ach_exec = float(np.mean(b_exec)) / t / 1e9
+    ncu = traffic or {}
     return {"bound": "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-            "traffic": traffic, "peak_source": peaks["source"] + (f" x {world} GPUs" if world > 1 else ""),
+            "traffic": ncu.get("dram_bytes_per_launch"), "ncu_limiters": ncu.get("limiters"),
+            "peak_source": peaks["source"] + (f" x {world} GPUs" if world > 1 else ""),
             "kernel": "k_bfs_persistent", "alg_bytes_per_launch": round(float(np.mean(b_alg))),
             "formula": "SURVEY 8(d): sum_k,dir insp[k][dir]*(c_k + s_k,dir) + 8*rows + 4*n, summed over GPUs",
             "executed": {"achieved": round(ach_exec, 2), "frac": round(ach_exec / peak, 4),
@@ -479,11 +481,12 @@ def run_ours(args, world, rank, local_rank):
 
 
 def _ncu_traffic():
-    """dram read+write bytes per launch of the BFS kernel from the committed ncu capture."""
+    """The committed ncu capture of the BFS kernel: dram read+write bytes per
+    launch and its unit utilisations (what limits it)."""
     path = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f)
     return None
 
 
