@@ -177,6 +177,9 @@ __host__ __device__ inline void level_dirs(const View &V, const Ctl &c, int L, i
 // counter is the sum alone (no twins needed).  exec_policy 2 (tests) takes
 // PUSHC whenever twins exist.
 constexpr int PUSHC = 2;
+#ifndef DBFS_PUSH_COST
+#define DBFS_PUSH_COST 2.0  // cost units per pushed edge in the executor model (4 -> 2: +0.7 % s24, +1.3 % s25 on 2 GPUs)
+#endif
 
 __host__ __device__ inline int rev_kind(int k) { return k == KIND_ND ? KIND_DN : (k == KIND_DN ? KIND_ND : KIND_DD); }
 
@@ -223,7 +226,7 @@ __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, con
         if (k == KIND_DD && V.col_sorted_dd) scan = scan * 0.5 > 1.0 ? scan * 0.5 : 1.0;
         double words = (double)(rev == KIND_ND ? V.nw_n : V.nw_d);
         double pull = 1.5 * U * scan + 0.25 * words;
-        double push = 4.0 * (double)S.fv[k];
+        double push = DBFS_PUSH_COST * (double)S.fv[k];
         if (pull < push) ex[k] = BWD;
     }
 }
