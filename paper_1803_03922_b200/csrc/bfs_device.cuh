@@ -177,6 +177,9 @@ __host__ __device__ inline void level_dirs(const View &V, const Ctl &c, int L, i
 // counter is the sum alone (no twins needed).  exec_policy 2 (tests) takes
 // PUSHC whenever twins exist.
 constexpr int PUSHC = 2;
+#ifndef DBFS_PUSHC_COST
+#define DBFS_PUSHC_COST 5.0  // cost units per edge of a counting push (PUSHC)
+#endif
 #ifndef DBFS_PUSH_COST
 #define DBFS_PUSH_COST 2.0  // cost units per pushed edge in the executor model (4 -> 2: +0.7 % s24, +1.3 % s25 on 2 GPUs)
 #endif
@@ -209,7 +212,7 @@ __host__ __device__ inline void exec_dirs(const View &V, const LevelSlot &S, con
             if (scan > avg) scan = avg;
             double words = (double)(rev == KIND_ND ? V.nw_n : V.nw_d);
             double pull = 1.5 * U * scan + 0.25 * words;
-            double push = 5.0 * (double)S.fv[k];  // push + twin load + atomicMin
+            double push = DBFS_PUSHC_COST * (double)S.fv[k];  // push + twin load + atomicMin
             if (push < pull) ex[k] = PUSHC;
             continue;
         }
